@@ -1,0 +1,445 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes view of the CPU parity oracle (liboracle.so).
+
+Imported only by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs.  The product package never imports this module.
+
+Every function mirrors a reference entry point (paths relative to
+/root/reference/proj) and returns numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
+_lib = None
+
+TARGETS = {"smooth": 0, "box": 1, "nonzero_bc": 2, "ball": 3, "sine_random": 4,
+           "zero": 5, "one": 6, "quadratic": 7}
+
+_P = C.c_void_p
+_I = C.c_int
+_D = C.c_double
+_pd = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_pi = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_pu8 = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+class OracleInvalidArgument(OracleError, ValueError):
+    pass
+
+
+def build():
+    """Compile the oracle (make) if the shared object is missing or stale."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        build()
+    L = C.CDLL(_LIB_PATH)
+    sig = {
+        "or_last_error": (C.c_char_p, []),
+        "or_set_num_threads": (None, [_I]),
+        "or_num_threads": (_I, []),
+        "or_build_structured_cube": (_I, [_I, C.POINTER(_P)]),
+        "or_mesh_free": (None, [_P]),
+        "or_mesh_new": (_I, [_I, _pd, _I, _pi, _pu8, C.POINTER(_P)]),
+        "or_mesh_info": (None, [_P, C.POINTER(_I), C.POINTER(_I)]),
+        "or_mesh_get": (None, [_P, _pd, _pi, _pu8, _pu8, _pi]),
+        "or_tet_volume": (_D, [_P, _I]),
+        "or_rule_size": (_I, [_I]),
+        "or_rule_get": (None, [_I, _pd, _pd]),
+        "or_target_eval": (_I, [_I, _I, C.c_uint64, _I, _pd, _pd]),
+        "or_pseudo_random_vec": (None, [_I, C.c_uint64, _pd]),
+        "or_build_system": (_I, [_P, _D, _I, C.c_uint64, C.POINTER(_P)]),
+        "or_system_free": (None, [_P]),
+        "or_system_n_dofs": (_I, [_P]),
+        "or_system_csr": (_P, [_P, _I]),
+        "or_system_get_f": (None, [_P, _pd]),
+        "or_system_get_dofmap": (None, [_P, _pi, _pi]),
+        "or_assemble_full": (_I, [_P, _I, C.POINTER(_P)]),
+        "or_assemble_load": (_I, [_P, _I, C.c_uint64, _pd]),
+        "or_csr_new": (_I, [_I, _I, C.c_int64, _pi, _pi, _pd, C.POINTER(_P)]),
+        "or_from_triplets": (_I, [_I, _I, C.c_int64, _pi, _pi, _pd, C.POINTER(_P)]),
+        "or_csr_free": (None, [_P]),
+        "or_csr_info": (None, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(C.c_int64)]),
+        "or_csr_get": (None, [_P, _pi, _pi, _pd]),
+        "or_spmv": (_I, [_P, _I, _pd, _pd]),
+        "or_dense_cholesky_solve": (_I, [_I, _pd, _pd, _pd]),
+        "or_dot": (_D, [_I, _pd, _pd]),
+        "or_coarsen_redblack": (_I, [_P, _pu8, C.POINTER(_P)]),
+        "or_galerkin_coarse": (_I, [_P, _P, C.POINTER(_P)]),
+        "or_sgs_sweep": (_I, [_P, _pd, _pd, _pd]),
+        "or_build_amg": (_I, [_P, _I, _I, C.POINTER(_P)]),
+        "or_amg_free": (None, [_P]),
+        "or_amg_num_levels": (_I, [_P]),
+        "or_amg_level_csr": (_P, [_P, _I, _I]),
+        "or_amg_level_flags": (_I, [_P, _I, _pu8]),
+        "or_amg_apply": (_I, [_P, _I, _pd, _pd]),
+        "or_pcg": (_I, [_P, _I, _P, _pd, _D, _I, _pd, C.POINTER(_I), C.POINTER(_I), _pd]),
+        "or_solve_system_amg": (_I, [_P, _D, _pd, C.POINTER(_I), C.POINTER(_I), C.POINTER(_D), C.POINTER(_D)]),
+        "or_l2_error_manufactured": (_I, [_P, _P, _pd, _D, C.POINTER(_D)]),
+        "or_h1_semi_error_manufactured": (_I, [_P, _P, _pd, _D, C.POINTER(_D)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    msg = lib().or_last_error().decode()
+    if rc == 1:
+        raise OracleInvalidArgument(msg)
+    raise OracleError(msg)
+
+
+def set_num_threads(n: int):
+    lib().or_set_num_threads(int(n))
+
+
+# ---------------------------------------------------------------- containers
+@dataclass
+class Csr:
+    rows: int
+    cols: int
+    rp: np.ndarray
+    ci: np.ndarray
+    v: np.ndarray
+
+    @property
+    def nnz(self):
+        return int(self.ci.size)
+
+    def dense(self):
+        D = np.zeros((self.rows, self.cols))
+        for r in range(self.rows):
+            s, e = self.rp[r], self.rp[r + 1]
+            D[r, self.ci[s:e]] = self.v[s:e]
+        return D
+
+    def handle(self):
+        h = _P()
+        _check(lib().or_csr_new(self.rows, self.cols, self.nnz, np.ascontiguousarray(self.rp, np.int32),
+                                np.ascontiguousarray(self.ci, np.int32),
+                                np.ascontiguousarray(self.v, np.float64), C.byref(h)))
+        return _Handle(h, lib().or_csr_free)
+
+    @staticmethod
+    def from_dense(D):
+        D = np.asarray(D, dtype=np.float64)
+        rp = [0]
+        ci, v = [], []
+        for r in range(D.shape[0]):
+            for c in range(D.shape[1]):
+                if D[r, c] != 0.0:
+                    ci.append(c)
+                    v.append(D[r, c])
+            rp.append(len(ci))
+        return Csr(D.shape[0], D.shape[1], np.array(rp, np.int32), np.array(ci, np.int32), np.array(v, np.float64))
+
+
+class _Handle:
+    def __init__(self, h, free):
+        self.h = h
+        self._free = free
+
+    def __del__(self):
+        if self.h and self._free is not None:
+            self._free(self.h)
+            self.h = None
+
+
+def _csr_from_handle(h) -> Csr:
+    rows, cols, nnz = _I(), _I(), C.c_int64()
+    lib().or_csr_info(h, C.byref(rows), C.byref(cols), C.byref(nnz))
+    rp = np.zeros(rows.value + 1, np.int32)
+    ci = np.zeros(max(nnz.value, 1), np.int32)
+    v = np.zeros(max(nnz.value, 1), np.float64)
+    lib().or_csr_get(h, rp, ci, v)
+    return Csr(rows.value, cols.value, rp, ci[: nnz.value].copy(), v[: nnz.value].copy())
+
+
+# ---------------------------------------------------------------- mesh
+@dataclass
+class Mesh:
+    n: int
+    xyz: np.ndarray
+    tets: np.ndarray
+    boundary: np.ndarray
+    refinement_edge: np.ndarray
+    generation: np.ndarray
+    _h: object = None
+
+
+def build_structured_cube(n: int) -> Mesh:
+    """mesh.cpp:29-65."""
+    h = _P()
+    _check(lib().or_build_structured_cube(int(n), C.byref(h)))
+    hh = _Handle(h, lib().or_mesh_free)
+    nv, nt = _I(), _I()
+    lib().or_mesh_info(h, C.byref(nv), C.byref(nt))
+    xyz = np.zeros((max(nv.value, 1), 3))
+    tets = np.zeros((max(nt.value, 1), 4), np.int32)
+    b = np.zeros(max(nv.value, 1), np.uint8)
+    re = np.zeros(max(nt.value, 1), np.uint8)
+    gen = np.zeros(max(nt.value, 1), np.int32)
+    lib().or_mesh_get(h, xyz, tets, b, re, gen)
+    return Mesh(n, xyz[: nv.value], tets[: nt.value], b[: nv.value], re[: nt.value], gen[: nt.value], hh)
+
+
+def mesh_from_arrays(xyz, tets, boundary) -> Mesh:
+    """A hand-built TetMesh (e.g. test_assembly.cpp:23-33's reference tet)."""
+    xyz = np.ascontiguousarray(xyz, np.float64)
+    tets = np.ascontiguousarray(tets, np.int32)
+    boundary = np.ascontiguousarray(boundary, np.uint8)
+    h = _P()
+    _check(lib().or_mesh_new(xyz.shape[0], xyz, tets.shape[0], tets, boundary, C.byref(h)))
+    return Mesh(-1, xyz, tets, boundary, np.full(tets.shape[0], 3, np.uint8), np.zeros(tets.shape[0], np.int32),
+                _Handle(h, lib().or_mesh_free))
+
+
+def tet_volume(mesh: Mesh, t: int) -> float:
+    return lib().or_tet_volume(mesh._h.h, int(t))
+
+
+def rule(rule_id: int):
+    """quadrature.cpp: 0 centroid, 1 degree-2, 2 degree-5 (14 pt), 3 subdivision64."""
+    n = lib().or_rule_size(rule_id)
+    pts = np.zeros((n, 4))
+    w = np.zeros(n)
+    lib().or_rule_get(rule_id, pts, w)
+    return pts, w
+
+
+def target_eval(kind: str, xyz, n: int = 0, seed: int = 0) -> np.ndarray:
+    xyz = np.ascontiguousarray(np.atleast_2d(xyz), np.float64)
+    out = np.zeros(xyz.shape[0])
+    _check(lib().or_target_eval(TARGETS[kind], int(n), int(seed), xyz.shape[0], xyz, out))
+    return out
+
+
+def pseudo_random_vec(n: int, seed: int) -> np.ndarray:
+    """tests/oracles.hpp:97-108."""
+    out = np.zeros(max(n, 1))
+    lib().or_pseudo_random_vec(int(n), int(seed), out)
+    return out[:n]
+
+
+# ---------------------------------------------------------------- system
+@dataclass
+class FemSystem:
+    rho: float
+    K: Csr
+    M: Csr
+    A: Csr
+    f: np.ndarray
+    vertex_to_dof: np.ndarray
+    dof_to_vertex: np.ndarray
+    _h: object = None
+
+    @property
+    def n_dofs(self):
+        return int(self.f.size)
+
+
+def build_system(mesh: Mesh, rho: float, target: str = "smooth", seed: int = 0) -> FemSystem:
+    """assembly.cpp:225-238."""
+    h = _P()
+    _check(lib().or_build_system(mesh._h.h, float(rho), TARGETS[target], int(seed), C.byref(h)))
+    hh = _Handle(h, lib().or_system_free)
+    nd = lib().or_system_n_dofs(h)
+    K = _csr_from_handle(lib().or_system_csr(h, 0))
+    M = _csr_from_handle(lib().or_system_csr(h, 1))
+    A = _csr_from_handle(lib().or_system_csr(h, 2))
+    f = np.zeros(max(nd, 1))
+    lib().or_system_get_f(h, f)
+    v2d = np.zeros(mesh.xyz.shape[0], np.int32)
+    d2v = np.zeros(max(nd, 1), np.int32)
+    lib().or_system_get_dofmap(h, v2d, d2v)
+    return FemSystem(rho, K, M, A, f[:nd], v2d, d2v[:nd], hh)
+
+
+def assemble_full(mesh: Mesh, which: str) -> Csr:
+    h = _P()
+    _check(lib().or_assemble_full(mesh._h.h, 0 if which == "K" else 1, C.byref(h)))
+    hh = _Handle(h, lib().or_csr_free)
+    return _csr_from_handle(hh.h)
+
+
+def assemble_load(mesh: Mesh, target: str, seed: int = 0) -> np.ndarray:
+    nd = int((mesh.boundary == 0).sum())
+    f = np.zeros(max(nd, 1))
+    _check(lib().or_assemble_load(mesh._h.h, TARGETS[target], int(seed), f))
+    return f[:nd]
+
+
+# ---------------------------------------------------------------- linalg
+def from_triplets(rows, cols, trips) -> Csr:
+    ti = np.array([t[0] for t in trips], np.int32)
+    tj = np.array([t[1] for t in trips], np.int32)
+    tv = np.array([t[2] for t in trips], np.float64)
+    if ti.size == 0:
+        ti = np.zeros(1, np.int32)[:0]
+    h = _P()
+    _check(lib().or_from_triplets(int(rows), int(cols), len(trips), np.ascontiguousarray(ti),
+                                  np.ascontiguousarray(tj), np.ascontiguousarray(tv), C.byref(h)))
+    hh = _Handle(h, lib().or_csr_free)
+    return _csr_from_handle(hh.h)
+
+
+def spmv(A: Csr, x) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.zeros(max(A.rows, 1))
+    ah = A.handle()
+    _check(lib().or_spmv(ah.h, x.size, x if x.size else np.zeros(1), y))
+    return y[: A.rows]
+
+
+def dot(a, b) -> float:
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    return lib().or_dot(a.size, a, b)
+
+
+def dense_cholesky_solve(A, b) -> np.ndarray:
+    A = np.ascontiguousarray(A, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    x = np.zeros(b.size)
+    _check(lib().or_dense_cholesky_solve(b.size, A, b, x))
+    return x
+
+
+# ---------------------------------------------------------------- amg
+def coarsen_redblack(A: Csr):
+    flags = np.zeros(max(A.rows, 1), np.uint8)
+    h = _P()
+    ah = A.handle()
+    _check(lib().or_coarsen_redblack(ah.h, flags, C.byref(h)))
+    hh = _Handle(h, lib().or_csr_free)
+    return flags[: A.rows], _csr_from_handle(hh.h)
+
+
+def galerkin_coarse(A: Csr, P: Csr) -> Csr:
+    h = _P()
+    ah, ph = A.handle(), P.handle()
+    _check(lib().or_galerkin_coarse(ah.h, ph.h, C.byref(h)))
+    hh = _Handle(h, lib().or_csr_free)
+    return _csr_from_handle(hh.h)
+
+
+def sgs_sweep(A: Csr, f, u) -> np.ndarray:
+    f = np.ascontiguousarray(f, np.float64)
+    u = np.ascontiguousarray(u, np.float64)
+    out = np.zeros(max(A.rows, 1))
+    ah = A.handle()
+    _check(lib().or_sgs_sweep(ah.h, f if f.size else np.zeros(1), u if u.size else np.zeros(1), out))
+    return out[: A.rows]
+
+
+class AmgHierarchy:
+    """amg.hpp:13-24 / amg.cpp:90-117."""
+
+    def __init__(self, A: Csr, coarsest_threshold: int = 64, smoothing_steps: int = 1):
+        h = _P()
+        ah = A.handle()
+        _check(lib().or_build_amg(ah.h, int(coarsest_threshold), int(smoothing_steps), C.byref(h)))
+        self._h = _Handle(h, lib().or_amg_free)
+        self.n = A.rows
+
+    @property
+    def num_levels(self):
+        return lib().or_amg_num_levels(self._h.h)
+
+    def level(self, l: int, which: str = "A"):
+        p = lib().or_amg_level_csr(self._h.h, int(l), {"A": 0, "P": 1, "Pt": 2}[which])
+        return None if not p else _csr_from_handle(p)
+
+    def flags(self, l: int):
+        A = self.level(l, "A")
+        f = np.zeros(max(A.rows, 1), np.uint8)
+        if lib().or_amg_level_flags(self._h.h, int(l), f) != 0:
+            return None
+        return f[: A.rows]
+
+    def apply(self, r) -> np.ndarray:
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.zeros(max(r.size, 1))
+        _check(lib().or_amg_apply(self._h.h, r.size, r if r.size else np.zeros(1), z))
+        return z[: r.size]
+
+
+def build_amg(A: Csr, coarsest_threshold: int = 64, smoothing_steps: int = 1) -> AmgHierarchy:
+    return AmgHierarchy(A, coarsest_threshold, smoothing_steps)
+
+
+@dataclass
+class PcgResult:
+    x: np.ndarray
+    iterations: int
+    converged: bool
+    residual_history: np.ndarray
+
+
+def pcg(A: Csr, precond="amg", f=None, tol=1e-8, max_iter=500, hierarchy: AmgHierarchy | None = None) -> PcgResult:
+    """linalg.cpp:64-102; precond in {'identity','jacobi','amg'}."""
+    f = np.ascontiguousarray(f, np.float64)
+    kind = {"identity": 0, "jacobi": 1, "amg": 2}[precond]
+    if kind == 2 and hierarchy is None:
+        hierarchy = build_amg(A)
+    x = np.zeros(max(f.size, 1))
+    hist = np.zeros(max(max_iter, 1))
+    it, conv = _I(), _I()
+    ah = A.handle()
+    _check(lib().or_pcg(ah.h, kind, hierarchy._h.h if hierarchy is not None else None,
+                        f if f.size else np.zeros(1), float(tol), int(max_iter), x, C.byref(it), C.byref(conv), hist))
+    return PcgResult(x[: f.size], it.value, bool(conv.value), hist[: it.value].copy())
+
+
+@dataclass
+class SolveOutcome:
+    u: np.ndarray
+    iterations: int
+    converged: bool
+    setup_seconds: float
+    solve_seconds: float
+
+
+def solve_system_amg(sys: FemSystem, tol: float = 1e-8) -> SolveOutcome:
+    """bench.cpp:185-241, PrecondKind::amg branch (:215-225)."""
+    u = np.zeros(max(sys.n_dofs, 1))
+    it, conv = _I(), _I()
+    ts, tv = _D(), _D()
+    _check(lib().or_solve_system_amg(sys._h.h, float(tol), u, C.byref(it), C.byref(conv), C.byref(ts), C.byref(tv)))
+    return SolveOutcome(u[: sys.n_dofs], it.value, bool(conv.value), ts.value, tv.value)
+
+
+def l2_error_manufactured(mesh: Mesh, sys: FemSystem, coeffs, rho_exact: float) -> float:
+    out = _D()
+    _check(lib().or_l2_error_manufactured(mesh._h.h, sys._h.h, np.ascontiguousarray(coeffs, np.float64),
+                                          float(rho_exact), C.byref(out)))
+    return out.value
+
+
+def h1_semi_error_manufactured(mesh: Mesh, sys: FemSystem, coeffs, rho_exact: float) -> float:
+    out = _D()
+    _check(lib().or_h1_semi_error_manufactured(mesh._h.h, sys._h.h, np.ascontiguousarray(coeffs, np.float64),
+                                               float(rho_exact), C.byref(out)))
+    return out.value

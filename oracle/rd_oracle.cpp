@@ -1,0 +1,1402 @@
+// rd_oracle.cpp -- TEST INFRASTRUCTURE ONLY: the CPU parity oracle.
+//
+// A line-by-line CPU restatement (no Eigen, which is absent from this image)
+// of the reference rdsolve solve path.  Citations are relative to
+// /root/reference/proj.  Parity status: the reference cannot be compiled here
+// (Eigen/doctest/CLI11 missing), so this oracle is pinned
+// against the reference's own known-answer tests (tests/test_*.cpp hand cases,
+// re-expressed in tests/test_oracle_kats.py) and Appendix A of SURVEY.md;
+// the Eigen-internal orders it restates (dot product, LLT) are marked
+// "restated, unverifiable here".
+//
+// Built with -O3 -ffp-contract=off and no -march, mirroring the reference's
+// Release flags (CMakeLists.txt:6-7,31): no FMA contraction anywhere.
+//
+// Nothing in the product path (paper_2102_03515_b200/) links or loads this.
+
+#include "rd_oracle.h"
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;  // std::numbers::pi (target.cpp:9)
+
+thread_local std::string g_err;
+
+// ---------------------------------------------------------------------------
+// parallel.cpp:12-73 -- fixed chunk grid (min(n,128) chunks, boundaries c*n/chunks),
+// work distributed over g_threads workers; reduce sums partials in chunk order.
+int g_threads = 1;
+
+int64_t chunk_count(int64_t n) { return std::min<int64_t>(n, 128); }
+
+void for_each_chunk(int64_t n, const std::function<void(int64_t, int64_t, int64_t)>& body) {
+  if (n <= 0) return;
+  const int64_t chunks = chunk_count(n);
+  auto run_chunk = [&](int64_t c) { body(c, c * n / chunks, (c + 1) * n / chunks); };
+  const int workers = static_cast<int>(std::min<int64_t>(g_threads, chunks));
+  if (workers <= 1) {
+    for (int64_t c = 0; c < chunks; ++c) run_chunk(c);
+    return;
+  }
+  std::atomic<int64_t> next(0);
+  auto work = [&]() {
+    for (;;) {
+      const int64_t c = next.fetch_add(1);
+      if (c >= chunks) return;
+      run_chunk(c);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < workers - 1; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+}
+
+void parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& body) {
+  for_each_chunk(n, [&](int64_t, int64_t b, int64_t e) { body(b, e); });
+}
+
+double parallel_reduce(int64_t n, const std::function<double(int64_t, int64_t)>& partial) {
+  if (n <= 0) return 0.0;
+  std::vector<double> parts(static_cast<size_t>(chunk_count(n)), 0.0);
+  for_each_chunk(n, [&](int64_t c, int64_t b, int64_t e) { parts[static_cast<size_t>(c)] = partial(b, e); });
+  double sum = 0.0;
+  for (double v : parts) sum += v;
+  return sum;
+}
+
+// ---------------------------------------------------------------------------
+// Containers (types.hpp:8-15): CSR with int32 indices, fp64 values.
+struct V3 {
+  double c[3];
+};
+
+struct Csr {
+  int rows = 0, cols = 0;
+  std::vector<int> rp{0};
+  std::vector<int> ci;
+  std::vector<double> v;
+  int64_t nnz() const { return static_cast<int64_t>(ci.size()); }
+};
+
+using Vec = std::vector<double>;
+
+// ---------------------------------------------------------------------------
+// mesh.cpp
+struct Mesh {
+  std::vector<V3> vertices;
+  std::vector<std::array<int, 4>> tets;
+  std::vector<uint8_t> boundary;
+  std::vector<uint8_t> refinement_edge;
+  std::vector<int> generation;
+  int nv() const { return static_cast<int>(vertices.size()); }
+  int nt() const { return static_cast<int>(tets.size()); }
+};
+
+// mesh.cpp:14-18
+bool on_unit_boundary(const V3& x) {
+  for (int c = 0; c < 3; ++c)
+    if (std::abs(x.c[c]) <= 1e-14 || std::abs(x.c[c] - 1.0) <= 1e-14) return true;
+  return false;
+}
+
+// mesh.cpp:29-65 (vertex id (k*nv+j)*nv+i, 6 Kuhn chains per cell in perms order, tag 3, gen 0)
+Mesh build_structured_cube(int n) {
+  if (n < 1) throw std::invalid_argument("build_structured_cube: n must be >= 1");
+  Mesh m;
+  const int nv = n + 1;
+  auto vid = [nv](int i, int j, int k) { return (k * nv + j) * nv + i; };
+  m.vertices.reserve(static_cast<size_t>(nv) * nv * nv);
+  for (int k = 0; k < nv; ++k)
+    for (int j = 0; j < nv; ++j)
+      for (int i = 0; i < nv; ++i) {
+        V3 x{{static_cast<double>(i) / n, static_cast<double>(j) / n, static_cast<double>(k) / n}};
+        m.vertices.push_back(x);
+        m.boundary.push_back(on_unit_boundary(x) ? 1 : 0);
+      }
+  constexpr int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  m.tets.reserve(static_cast<size_t>(n) * n * n * 6);
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i)
+        for (const auto& perm : perms) {
+          std::array<int, 4> t;
+          int c[3] = {i, j, k};
+          t[0] = vid(c[0], c[1], c[2]);
+          for (int s = 0; s < 3; ++s) {
+            c[perm[s]] += 1;
+            t[static_cast<size_t>(s) + 1] = vid(c[0], c[1], c[2]);
+          }
+          m.tets.push_back(t);
+          m.refinement_edge.push_back(3);
+          m.generation.push_back(0);
+        }
+  return m;
+}
+
+std::array<V3, 4> tet_vertices(const Mesh& m, int t) {
+  const auto& tt = m.tets[static_cast<size_t>(t)];
+  return {m.vertices[static_cast<size_t>(tt[0])], m.vertices[static_cast<size_t>(tt[1])],
+          m.vertices[static_cast<size_t>(tt[2])], m.vertices[static_cast<size_t>(tt[3])]};
+}
+
+// mesh.cpp:188-191: |(v1-v0) x (v2-v0) . (v3-v0)| / 6  (Eigen cross; 3-dot = (a0b0+a1b1)+a2b2)
+double tet_volume(const Mesh& m, int t) {
+  const auto v = tet_vertices(m, t);
+  double a[3], b[3], d[3];
+  for (int c = 0; c < 3; ++c) {
+    a[c] = v[1].c[c] - v[0].c[c];
+    b[c] = v[2].c[c] - v[0].c[c];
+    d[c] = v[3].c[c] - v[0].c[c];
+  }
+  const double x0 = a[1] * b[2] - a[2] * b[1];
+  const double x1 = a[2] * b[0] - a[0] * b[2];
+  const double x2 = a[0] * b[1] - a[1] * b[0];
+  const double dot = (x0 * d[0] + x1 * d[1]) + x2 * d[2];
+  return std::abs(dot) / 6.0;
+}
+
+// ---------------------------------------------------------------------------
+// quadrature.cpp
+struct Rule {
+  std::vector<std::array<double, 4>> pts;
+  std::vector<double> w;
+  int size() const { return static_cast<int>(w.size()); }
+};
+
+Rule make_centroid() {  // quadrature.cpp:14-19
+  Rule r;
+  r.pts.push_back({0.25, 0.25, 0.25, 0.25});
+  r.w.push_back(1.0);
+  return r;
+}
+
+Rule make_degree2() {  // quadrature.cpp:21-30
+  const double a = 0.1381966011250105;
+  const double b = 0.5854101966249685;
+  Rule r;
+  for (int i = 0; i < 4; ++i) {
+    std::array<double, 4> p{a, a, a, a};
+    p[static_cast<size_t>(i)] = b;
+    r.pts.push_back(p);
+    r.w.push_back(0.25);
+  }
+  return r;
+}
+
+Rule make_degree5() {  // quadrature.cpp:24-55 (14-point Keast, literal constants :27-32)
+  const double wa = 0.1126879257180162;
+  const double a = 0.3108859192633005;
+  const double wb = 0.0734930431163619;
+  const double b = 0.0927352503108912;
+  const double wc = 0.0425460207770812;
+  const double c = 0.0455037041256497;
+  Rule r;
+  for (int i = 0; i < 4; ++i) {
+    std::array<double, 4> p{a, a, a, a};
+    p[static_cast<size_t>(i)] = 1.0 - 3.0 * a;
+    r.pts.push_back(p);
+    r.w.push_back(wa);
+  }
+  for (int i = 0; i < 4; ++i) {
+    std::array<double, 4> p{b, b, b, b};
+    p[static_cast<size_t>(i)] = 1.0 - 3.0 * b;
+    r.pts.push_back(p);
+    r.w.push_back(wb);
+  }
+  for (int i = 0; i < 4; ++i)
+    for (int j = i + 1; j < 4; ++j) {
+      const double m = 0.5 - c;
+      std::array<double, 4> p{m, m, m, m};
+      p[static_cast<size_t>(i)] = c;
+      p[static_cast<size_t>(j)] = c;
+      r.pts.push_back(p);
+      r.w.push_back(wc);
+    }
+  return r;
+}
+
+// quadrature.cpp:57-82: three levels of centroid subdivision; every value is a
+// dyadic rational (denominators <= 256), so the column means are exact in any order.
+Rule make_subdivision64() {
+  using Cell = std::array<std::array<double, 4>, 4>;  // cell[row][col], row = vertex
+  std::vector<Cell> cells(1);
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) cells[0][static_cast<size_t>(i)][static_cast<size_t>(j)] = i == j ? 1.0 : 0.0;
+  auto colmean = [](const Cell& c) {
+    std::array<double, 4> g{};
+    for (int j = 0; j < 4; ++j) {
+      double s = 0.0;
+      for (int i = 0; i < 4; ++i) s += c[static_cast<size_t>(i)][static_cast<size_t>(j)];
+      g[static_cast<size_t>(j)] = s / 4.0;
+    }
+    return g;
+  };
+  for (int level = 0; level < 3; ++level) {
+    std::vector<Cell> next;
+    for (const Cell& cell : cells) {
+      const auto g = colmean(cell);
+      for (int i = 0; i < 4; ++i) {
+        Cell child = cell;
+        child[static_cast<size_t>(i)] = g;
+        next.push_back(child);
+      }
+    }
+    cells.swap(next);
+  }
+  Rule r;
+  for (const Cell& cell : cells) {
+    r.pts.push_back(colmean(cell));
+    r.w.push_back(1.0 / static_cast<double>(cells.size()));
+  }
+  return r;
+}
+
+const Rule& rule_by_id(int id) {
+  static const Rule r0 = make_centroid(), r1 = make_degree2(), r2 = make_degree5(),
+                    r3 = make_subdivision64();
+  switch (id) {
+    case 0: return r0;
+    case 1: return r1;
+    case 2: return r2;
+    case 3: return r3;
+  }
+  throw std::invalid_argument("unknown rule");
+}
+
+// quadrature.cpp:106-114: p = Zero; p += lambda_k * v_k, k = 0..3
+V3 physical_point(const std::array<double, 4>& lam, const std::array<V3, 4>& v) {
+  V3 p{{0.0, 0.0, 0.0}};
+  for (int k = 0; k < 4; ++k)
+    for (int c = 0; c < 3; ++c) p.c[c] = p.c[c] + lam[static_cast<size_t>(k)] * v[static_cast<size_t>(k)].c[c];
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// target.cpp (+ ball, sine+random: BASELINE configs 2/3)
+enum Smoothness { smooth_h2, discontinuous, smooth_nonzero_bc };
+
+double sin3(const V3& x) {  // target.cpp:12-15
+  return std::sin(kPi * x.c[0]) * std::sin(kPi * x.c[1]) * std::sin(kPi * x.c[2]);
+}
+
+// tests/oracles.hpp:97-108 splitmix64 on [-1,1)
+void pseudo_random(int n, uint64_t seed, double* out) {
+  uint64_t s = seed + 0x9e3779b97f4a7c15ULL;
+  for (int i = 0; i < n; ++i) {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    z = z ^ (z >> 31);
+    out[i] = 2.0 * (static_cast<double>(z >> 11) * 0x1.0p-53) - 1.0;
+  }
+}
+
+struct Target {
+  int kind = OR_TARGET_SMOOTH;
+  Smoothness tag = smooth_h2;
+  int n = 0;                 // lattice resolution (sine+random only)
+  std::vector<double> nodal;  // (n+1)^3 random nodal values, zero on the boundary
+
+  // P1 interpolant on the Kuhn lattice: cell = floor(n x) clamped, local
+  // coordinates sorted descending pick the chain (ties -> first in mesh.cpp:46 perms order).
+  double interp(const V3& x) const {
+    const int nv = n + 1;
+    int cell[3];
+    double xi[3];
+    for (int d = 0; d < 3; ++d) {
+      const double s = x.c[d] * static_cast<double>(n);
+      int ci = static_cast<int>(std::floor(s));
+      ci = std::min(std::max(ci, 0), n - 1);
+      cell[d] = ci;
+      xi[d] = s - static_cast<double>(ci);
+    }
+    constexpr int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    int p = 0;
+    for (; p < 5; ++p)
+      if (xi[perms[p][0]] >= xi[perms[p][1]] && xi[perms[p][1]] >= xi[perms[p][2]]) break;
+    const int* pm = perms[p];
+    const double lam[4] = {1.0 - xi[pm[0]], xi[pm[0]] - xi[pm[1]], xi[pm[1]] - xi[pm[2]], xi[pm[2]]};
+    int c[3] = {cell[0], cell[1], cell[2]};
+    double val = 0.0;
+    val = val + lam[0] * nodal[static_cast<size_t>((c[2] * nv + c[1]) * nv + c[0])];
+    for (int s = 0; s < 3; ++s) {
+      c[pm[s]] += 1;
+      val = val + lam[s + 1] * nodal[static_cast<size_t>((c[2] * nv + c[1]) * nv + c[0])];
+    }
+    return val;
+  }
+
+  double operator()(const V3& x) const {
+    switch (kind) {
+      case OR_TARGET_SMOOTH: return sin3(x);  // target.cpp:17-23
+      case OR_TARGET_BOX: {                  // target.cpp:25-35 (open box)
+        const bool inside = x.c[0] > 0.25 && x.c[0] < 0.75 && x.c[1] > 0.25 && x.c[1] < 0.75 &&
+                            x.c[2] > 0.25 && x.c[2] < 0.75;
+        return inside ? 1.0 : 0.0;
+      }
+      case OR_TARGET_NONZERO_BC: return 1.0 + sin3(x);  // target.cpp:37-43
+      case OR_TARGET_BALL: {  // open ball r=0.25 at (1/2,1/2,1/2), squared-distance test
+        const double dx = x.c[0] - 0.5, dy = x.c[1] - 0.5, dz = x.c[2] - 0.5;
+        return (dx * dx + dy * dy) + dz * dz < 0.0625 ? 1.0 : 0.0;
+      }
+      case OR_TARGET_SINE_RANDOM: return sin3(x) + 0.1 * interp(x);
+      case OR_TARGET_ZERO: return 0.0;                                // test_assembly.cpp:102-106
+      case OR_TARGET_ONE: return 1.0;                                 // test_assembly.cpp:108-124
+      case OR_TARGET_QUADRATIC: return x.c[0] * x.c[1] + 2.0 * x.c[2];  // test_assembly.cpp:37
+    }
+    throw std::invalid_argument("unknown target");
+  }
+};
+
+Target make_target(int kind, int n, uint64_t seed) {
+  Target t;
+  t.kind = kind;
+  switch (kind) {
+    case OR_TARGET_SMOOTH: t.tag = smooth_h2; break;
+    case OR_TARGET_BOX: t.tag = discontinuous; break;
+    case OR_TARGET_NONZERO_BC: t.tag = smooth_nonzero_bc; break;
+    case OR_TARGET_BALL: t.tag = discontinuous; break;
+    case OR_TARGET_SINE_RANDOM: {
+      if (n < 1) throw std::invalid_argument("sine+random target needs n >= 1");
+      t.tag = smooth_h2;
+      t.n = n;
+      const int nv = n + 1;
+      const int total = nv * nv * nv;
+      t.nodal.resize(static_cast<size_t>(total));
+      pseudo_random(total, seed, t.nodal.data());
+      for (int k = 0; k < nv; ++k)
+        for (int j = 0; j < nv; ++j)
+          for (int i = 0; i < nv; ++i)
+            if (i == 0 || j == 0 || k == 0 || i == n || j == n || k == n)
+              t.nodal[static_cast<size_t>((k * nv + j) * nv + i)] = 0.0;
+      break;
+    }
+    case OR_TARGET_ZERO:
+    case OR_TARGET_ONE:
+    case OR_TARGET_QUADRATIC: t.tag = smooth_h2; break;
+    default: throw std::invalid_argument("unknown target kind");
+  }
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// assembly.cpp
+struct VertexTets {
+  std::vector<int> offset, tet;
+};
+
+VertexTets build_vertex_tets(const Mesh& m) {  // assembly.cpp:14-31 (counting sort, ascending tets)
+  VertexTets a;
+  a.offset.assign(static_cast<size_t>(m.nv()) + 1, 0);
+  for (const auto& t : m.tets)
+    for (int v : t) ++a.offset[static_cast<size_t>(v) + 1];
+  for (size_t v = 1; v < a.offset.size(); ++v) a.offset[v] += a.offset[v - 1];
+  a.tet.resize(static_cast<size_t>(4) * m.nt());
+  std::vector<int> cur(a.offset.begin(), a.offset.end() - 1);
+  for (int t = 0; t < m.nt(); ++t)
+    for (int v : m.tets[static_cast<size_t>(t)]) a.tet[static_cast<size_t>(cur[static_cast<size_t>(v)]++)] = t;
+  return a;
+}
+
+struct LocalGeom {
+  double volume;
+  double grad[4][3];
+};
+
+// assembly.cpp:33-51 with Eigen's 3x3 determinant (bruteforce_det3_helper) and
+// cofactor inverse (compute_inverse_size3_helper) -- exact for n = 2^k lattices.
+LocalGeom local_geom(const std::array<V3, 4>& v) {
+  double J[3][3];
+  for (int r = 0; r < 3; ++r) {
+    J[r][0] = v[1].c[r] - v[0].c[r];
+    J[r][1] = v[2].c[r] - v[0].c[r];
+    J[r][2] = v[3].c[r] - v[0].c[r];
+  }
+  auto det3 = [&](int a, int b, int c) { return J[0][a] * (J[1][b] * J[2][c] - J[1][c] * J[2][b]); };
+  const double det = det3(0, 1, 2) - det3(1, 0, 2) + det3(2, 0, 1);
+  LocalGeom g;
+  g.volume = std::abs(det) / 6.0;
+  if (!(g.volume > 0.0)) throw std::runtime_error("assembly: degenerate tet");
+  auto cof = [&](int i, int j) {
+    const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+    return J[i1][j1] * J[i2][j2] - J[i1][j2] * J[i2][j1];
+  };
+  const double c0[3] = {cof(0, 0), cof(1, 0), cof(2, 0)};
+  const double d2 = (c0[0] * J[0][0] + c0[1] * J[1][0]) + c0[2] * J[2][0];
+  const double invdet = 1.0 / d2;
+  double inv[3][3];
+  inv[0][0] = c0[0] * invdet;
+  inv[0][1] = c0[1] * invdet;
+  inv[0][2] = c0[2] * invdet;
+  inv[1][0] = cof(0, 1) * invdet;
+  inv[1][1] = cof(1, 1) * invdet;
+  inv[1][2] = cof(2, 1) * invdet;
+  inv[2][0] = cof(0, 2) * invdet;
+  inv[2][1] = cof(1, 2) * invdet;
+  inv[2][2] = cof(2, 2) * invdet;
+  for (int i = 0; i < 3; ++i)
+    for (int c = 0; c < 3; ++c) g.grad[i + 1][c] = inv[i][c];
+  for (int c = 0; c < 3; ++c) g.grad[0][c] = -((g.grad[1][c] + g.grad[2][c]) + g.grad[3][c]);
+  return g;
+}
+
+double dot3(const double* a, const double* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+
+// assembly.cpp:53-132: row-gather assembly of cK*K + cM*M; columns = sorted unique
+// dofs of incident-tet vertices; per slot accumulate over incident tets ascending,
+// jv = 0..3; then prune exact zeros.
+Csr assemble_matrix(const Mesh& m, const std::vector<int>& row_of_vert,
+                    const std::vector<int>& vert_of_row, double cK, double cM) {
+  const VertexTets adj = build_vertex_tets(m);
+  const int n = static_cast<int>(vert_of_row.size());
+  std::vector<std::vector<int>> cols(static_cast<size_t>(n));
+  parallel_for(n, [&](int64_t rb, int64_t re) {
+    std::vector<int> cand;
+    for (int64_t r = rb; r < re; ++r) {
+      const int v = vert_of_row[static_cast<size_t>(r)];
+      cand.clear();
+      for (int k = adj.offset[static_cast<size_t>(v)]; k < adj.offset[static_cast<size_t>(v) + 1]; ++k) {
+        const int t = adj.tet[static_cast<size_t>(k)];
+        for (int w : m.tets[static_cast<size_t>(t)]) {
+          const int c = row_of_vert[static_cast<size_t>(w)];
+          if (c >= 0) cand.push_back(c);
+        }
+      }
+      std::sort(cand.begin(), cand.end());
+      cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+      cols[static_cast<size_t>(r)] = cand;
+    }
+  });
+  std::vector<int> rp(static_cast<size_t>(n) + 1, 0);
+  for (int r = 0; r < n; ++r)
+    rp[static_cast<size_t>(r) + 1] = rp[static_cast<size_t>(r)] + static_cast<int>(cols[static_cast<size_t>(r)].size());
+  std::vector<double> vals(static_cast<size_t>(rp[static_cast<size_t>(n)]), 0.0);
+  parallel_for(n, [&](int64_t rb, int64_t re) {
+    for (int64_t r = rb; r < re; ++r) {
+      const auto& rc = cols[static_cast<size_t>(r)];
+      double* va = vals.data() + rp[static_cast<size_t>(r)];
+      const int v = vert_of_row[static_cast<size_t>(r)];
+      for (int k = adj.offset[static_cast<size_t>(v)]; k < adj.offset[static_cast<size_t>(v) + 1]; ++k) {
+        const int t = adj.tet[static_cast<size_t>(k)];
+        const auto& tet = m.tets[static_cast<size_t>(t)];
+        const LocalGeom g = local_geom(tet_vertices(m, t));
+        int iv = 0;
+        while (tet[static_cast<size_t>(iv)] != v) ++iv;
+        for (int jv = 0; jv < 4; ++jv) {
+          const int c = row_of_vert[static_cast<size_t>(tet[static_cast<size_t>(jv)])];
+          if (c < 0) continue;
+          double val = 0.0;
+          if (cK != 0.0) val += cK * g.volume * dot3(g.grad[iv], g.grad[jv]);
+          if (cM != 0.0) val += cM * g.volume * (iv == jv ? 0.1 : 0.05);
+          const auto pos = std::lower_bound(rc.begin(), rc.end(), c) - rc.begin();
+          va[pos] += val;
+        }
+      }
+    }
+  });
+  // prune (v != 0.0) and compress (assembly.cpp:129-130)
+  Csr A;
+  A.rows = n;
+  A.cols = n;
+  A.rp.assign(static_cast<size_t>(n) + 1, 0);
+  for (int r = 0; r < n; ++r) {
+    const auto& rc = cols[static_cast<size_t>(r)];
+    for (size_t q = 0; q < rc.size(); ++q) {
+      const double x = vals[static_cast<size_t>(rp[static_cast<size_t>(r)]) + q];
+      if (x != 0.0) {
+        A.ci.push_back(rc[q]);
+        A.v.push_back(x);
+      }
+    }
+    A.rp[static_cast<size_t>(r) + 1] = static_cast<int>(A.ci.size());
+  }
+  return A;
+}
+
+struct DofMap {
+  std::vector<int> vertex_to_dof, dof_to_vertex;
+  int n_dofs() const { return static_cast<int>(dof_to_vertex.size()); }
+};
+
+DofMap interior_dof_map(const Mesh& m) {  // assembly.cpp:187-197
+  DofMap d;
+  d.vertex_to_dof.assign(static_cast<size_t>(m.nv()), -1);
+  for (int v = 0; v < m.nv(); ++v)
+    if (!m.boundary[static_cast<size_t>(v)]) {
+      d.vertex_to_dof[static_cast<size_t>(v)] = d.n_dofs();
+      d.dof_to_vertex.push_back(v);
+    }
+  return d;
+}
+
+const Rule& rule_for(const Target& t) {  // assembly.cpp:140-144
+  return t.tag == discontinuous ? rule_by_id(3) : rule_by_id(2);
+}
+
+// assembly.cpp:146-174: f_r = sum_{t ascending} vol_t * sum_q (w_q u(x_q)) lambda_q,iv
+Vec load_vector(const Mesh& m, const DofMap& dm, const Target& target) {
+  const VertexTets adj = build_vertex_tets(m);
+  const Rule& rule = rule_for(target);
+  Vec f(static_cast<size_t>(dm.n_dofs()));
+  parallel_for(dm.n_dofs(), [&](int64_t rb, int64_t re) {
+    for (int64_t r = rb; r < re; ++r) {
+      const int v = dm.dof_to_vertex[static_cast<size_t>(r)];
+      double s = 0.0;
+      for (int k = adj.offset[static_cast<size_t>(v)]; k < adj.offset[static_cast<size_t>(v) + 1]; ++k) {
+        const int t = adj.tet[static_cast<size_t>(k)];
+        const auto& tet = m.tets[static_cast<size_t>(t)];
+        int iv = 0;
+        while (tet[static_cast<size_t>(iv)] != v) ++iv;
+        const auto verts = tet_vertices(m, t);
+        const double vol = tet_volume(m, t);
+        double acc = 0.0;
+        for (int q = 0; q < rule.size(); ++q) {
+          const V3 x = physical_point(rule.pts[static_cast<size_t>(q)], verts);
+          acc += rule.w[static_cast<size_t>(q)] * target(x) * rule.pts[static_cast<size_t>(q)][static_cast<size_t>(iv)];
+        }
+        s += vol * acc;
+      }
+      f[static_cast<size_t>(r)] = s;
+    }
+  });
+  return f;
+}
+
+struct System {
+  double rho = 1.0;
+  Csr K, M, A;
+  Vec f;
+  DofMap dm;
+};
+
+// Eigen sparse union add (CwiseBinaryOp<scalar_sum_op>): both -> l + r, one side -> x + 0 / 0 + x.
+Csr scaled_sum(double rho, const Csr& K, const Csr& M) {
+  Csr A;
+  A.rows = K.rows;
+  A.cols = K.cols;
+  A.rp.assign(static_cast<size_t>(K.rows) + 1, 0);
+  for (int r = 0; r < K.rows; ++r) {
+    int a = K.rp[static_cast<size_t>(r)], ae = K.rp[static_cast<size_t>(r) + 1];
+    int b = M.rp[static_cast<size_t>(r)], be = M.rp[static_cast<size_t>(r) + 1];
+    while (a < ae || b < be) {
+      if (a < ae && b < be && K.ci[static_cast<size_t>(a)] == M.ci[static_cast<size_t>(b)]) {
+        A.ci.push_back(K.ci[static_cast<size_t>(a)]);
+        A.v.push_back(rho * K.v[static_cast<size_t>(a)] + M.v[static_cast<size_t>(b)]);
+        ++a;
+        ++b;
+      } else if (a < ae && (b >= be || K.ci[static_cast<size_t>(a)] < M.ci[static_cast<size_t>(b)])) {
+        A.ci.push_back(K.ci[static_cast<size_t>(a)]);
+        A.v.push_back(rho * K.v[static_cast<size_t>(a)] + 0.0);
+        ++a;
+      } else {
+        A.ci.push_back(M.ci[static_cast<size_t>(b)]);
+        A.v.push_back(0.0 + M.v[static_cast<size_t>(b)]);
+        ++b;
+      }
+    }
+    A.rp[static_cast<size_t>(r) + 1] = static_cast<int>(A.ci.size());
+  }
+  return A;
+}
+
+System build_system(const Mesh& m, double rho, const Target& target) {  // assembly.cpp:225-238
+  if (!(rho > 0.0)) throw std::invalid_argument("build_system: rho must be > 0");
+  System s;
+  s.rho = rho;
+  s.dm = interior_dof_map(m);
+  s.K = assemble_matrix(m, s.dm.vertex_to_dof, s.dm.dof_to_vertex, 1.0, 0.0);
+  s.M = assemble_matrix(m, s.dm.vertex_to_dof, s.dm.dof_to_vertex, 0.0, 1.0);
+  s.A = scaled_sum(rho, s.K, s.M);
+  s.f = load_vector(m, s.dm, target);
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// linalg.cpp
+Csr from_triplets(int rows, int cols, const std::vector<int>& ti, const std::vector<int>& tj,
+                  const std::vector<double>& tv) {  // linalg.cpp:11-17 (setFromTriplets: dups summed in insertion order; prune)
+  const size_t n = ti.size();
+  std::vector<size_t> order(n);
+  for (size_t k = 0; k < n; ++k) order[k] = k;
+  for (size_t k = 0; k < n; ++k)
+    if (ti[k] < 0 || ti[k] >= rows || tj[k] < 0 || tj[k] >= cols)
+      throw std::invalid_argument("from_triplets: index out of range");
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+    return ti[a] != ti[b] ? ti[a] < ti[b] : tj[a] < tj[b];
+  });
+  Csr A;
+  A.rows = rows;
+  A.cols = cols;
+  A.rp.assign(static_cast<size_t>(rows) + 1, 0);
+  size_t k = 0;
+  for (int r = 0; r < rows; ++r) {
+    while (k < n && ti[order[k]] == r) {
+      const int c = tj[order[k]];
+      double s = tv[order[k]];
+      ++k;
+      while (k < n && ti[order[k]] == r && tj[order[k]] == c) s += tv[order[k++]];
+      if (s != 0.0) {
+        A.ci.push_back(c);
+        A.v.push_back(s);
+      }
+    }
+    A.rp[static_cast<size_t>(r) + 1] = static_cast<int>(A.ci.size());
+  }
+  return A;
+}
+
+// linalg.cpp:19-33: y_i = ((0 + v0 x0) + v1 x1) + ... in column order
+Vec spmv(const Csr& A, const Vec& x) {
+  if (A.cols != static_cast<int>(x.size())) throw std::invalid_argument("spmv: dimension mismatch");
+  Vec y(static_cast<size_t>(A.rows));
+  parallel_for(A.rows, [&](int64_t b, int64_t e) {
+    for (int64_t i = b; i < e; ++i) {
+      double s = 0.0;
+      for (int k = A.rp[static_cast<size_t>(i)]; k < A.rp[static_cast<size_t>(i) + 1]; ++k)
+        s += A.v[static_cast<size_t>(k)] * x[static_cast<size_t>(A.ci[static_cast<size_t>(k)])];
+      y[static_cast<size_t>(i)] = s;
+    }
+  });
+  return y;
+}
+
+// Eigen 3.4 VectorXd::dot with SSE2 (packet of 2, two packet accumulators,
+// Redux.h LinearVectorizedTraversal) -- restated, unverifiable here (no Eigen).
+double eigen_dot(const double* a, const double* b, int64_t n) {
+  if (n <= 0) return 0.0;
+  const int64_t aligned2 = (n / 4) * 4, aligned = (n / 2) * 2;
+  double res;
+  if (aligned) {
+    double p0a = a[0] * b[0], p0b = a[1] * b[1];
+    if (aligned > 2) {
+      double p1a = a[2] * b[2], p1b = a[3] * b[3];
+      for (int64_t i = 4; i < aligned2; i += 4) {
+        p0a = p0a + a[i] * b[i];
+        p0b = p0b + a[i + 1] * b[i + 1];
+        p1a = p1a + a[i + 2] * b[i + 2];
+        p1b = p1b + a[i + 3] * b[i + 3];
+      }
+      p0a = p0a + p1a;
+      p0b = p0b + p1b;
+      if (aligned > aligned2) {
+        p0a = p0a + a[aligned2] * b[aligned2];
+        p0b = p0b + a[aligned2 + 1] * b[aligned2 + 1];
+      }
+    }
+    res = p0a + p0b;
+    for (int64_t i = aligned; i < n; ++i) res = res + a[i] * b[i];
+  } else {
+    res = a[0] * b[0];
+  }
+  return res;
+}
+
+double dot(const Vec& a, const Vec& b) { return eigen_dot(a.data(), b.data(), static_cast<int64_t>(a.size())); }
+
+// Dense Cholesky (Eigen LLT<MatrixXd>, linalg.cpp:46-51, amg.cpp:111-115).  Eigen's
+// blocked kernel order is unverifiable here; this is the left-looking order the
+// device's one-CTA factorization uses (so oracle and device agree bit-for-bit).
+struct Llt {
+  int n = 0;
+  std::vector<double> L;  // row-major lower factor
+  bool ok = true;
+};
+
+Llt llt_compute(int n, const std::vector<double>& A) {
+  Llt f;
+  f.n = n;
+  f.L.assign(static_cast<size_t>(n) * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double s = A[static_cast<size_t>(j) * n + j];
+    for (int k = 0; k < j; ++k) s -= f.L[static_cast<size_t>(j) * n + k] * f.L[static_cast<size_t>(j) * n + k];
+    if (!(s > 0.0)) {
+      f.ok = false;
+      return f;
+    }
+    const double d = std::sqrt(s);
+    f.L[static_cast<size_t>(j) * n + j] = d;
+    for (int i = j + 1; i < n; ++i) {
+      double t = A[static_cast<size_t>(i) * n + j];
+      for (int k = 0; k < j; ++k) t -= f.L[static_cast<size_t>(i) * n + k] * f.L[static_cast<size_t>(j) * n + k];
+      f.L[static_cast<size_t>(i) * n + j] = t / d;
+    }
+  }
+  return f;
+}
+
+Vec llt_solve(const Llt& f, const Vec& b) {
+  const int n = f.n;
+  Vec y(static_cast<size_t>(n)), x(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    double s = b[static_cast<size_t>(i)];
+    for (int k = 0; k < i; ++k) s -= f.L[static_cast<size_t>(i) * n + k] * y[static_cast<size_t>(k)];
+    y[static_cast<size_t>(i)] = s / f.L[static_cast<size_t>(i) * n + i];
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = y[static_cast<size_t>(i)];
+    for (int k = i + 1; k < n; ++k) s -= f.L[static_cast<size_t>(k) * n + i] * x[static_cast<size_t>(k)];
+    x[static_cast<size_t>(i)] = s / f.L[static_cast<size_t>(i) * n + i];
+  }
+  return x;
+}
+
+std::vector<double> to_dense(const Csr& A) {
+  std::vector<double> D(static_cast<size_t>(A.rows) * A.cols, 0.0);
+  for (int r = 0; r < A.rows; ++r)
+    for (int k = A.rp[static_cast<size_t>(r)]; k < A.rp[static_cast<size_t>(r) + 1]; ++k)
+      D[static_cast<size_t>(r) * A.cols + A.ci[static_cast<size_t>(k)]] = A.v[static_cast<size_t>(k)];
+  return D;
+}
+
+// ---------------------------------------------------------------------------
+// amg.cpp
+std::pair<std::vector<uint8_t>, Csr> coarsen_redblack(const Csr& A) {  // amg.cpp:7-56
+  const int n = A.rows;
+  enum : uint8_t { unmarked = 0, coarse = 1, fine = 2 };
+  std::vector<uint8_t> state(static_cast<size_t>(n), unmarked);
+  for (int i = 0; i < n; ++i) {
+    if (state[static_cast<size_t>(i)] != unmarked) continue;
+    state[static_cast<size_t>(i)] = coarse;
+    for (int k = A.rp[static_cast<size_t>(i)]; k < A.rp[static_cast<size_t>(i) + 1]; ++k) {
+      const int j = A.ci[static_cast<size_t>(k)];
+      if (j != i && state[static_cast<size_t>(j)] == unmarked) state[static_cast<size_t>(j)] = fine;
+    }
+  }
+  for (int i = 0; i < n; ++i) {  // guard :22-29
+    if (state[static_cast<size_t>(i)] != fine) continue;
+    bool has_coarse = false;
+    for (int k = A.rp[static_cast<size_t>(i)]; k < A.rp[static_cast<size_t>(i) + 1] && !has_coarse; ++k)
+      has_coarse = A.ci[static_cast<size_t>(k)] != i && state[static_cast<size_t>(A.ci[static_cast<size_t>(k)])] == coarse;
+    if (!has_coarse) state[static_cast<size_t>(i)] = coarse;
+  }
+  std::vector<int> cidx(static_cast<size_t>(n), -1);
+  int nc = 0;
+  for (int i = 0; i < n; ++i)
+    if (state[static_cast<size_t>(i)] == coarse) cidx[static_cast<size_t>(i)] = nc++;
+  std::vector<int> ti, tj;
+  std::vector<double> tv;
+  for (int i = 0; i < n; ++i) {
+    if (state[static_cast<size_t>(i)] == coarse) {
+      ti.push_back(i);
+      tj.push_back(cidx[static_cast<size_t>(i)]);
+      tv.push_back(1.0);
+      continue;
+    }
+    int count = 0;
+    for (int k = A.rp[static_cast<size_t>(i)]; k < A.rp[static_cast<size_t>(i) + 1]; ++k)
+      if (A.ci[static_cast<size_t>(k)] != i && state[static_cast<size_t>(A.ci[static_cast<size_t>(k)])] == coarse) ++count;
+    const double w = 1.0 / count;
+    for (int k = A.rp[static_cast<size_t>(i)]; k < A.rp[static_cast<size_t>(i) + 1]; ++k)
+      if (A.ci[static_cast<size_t>(k)] != i && state[static_cast<size_t>(A.ci[static_cast<size_t>(k)])] == coarse) {
+        ti.push_back(i);
+        tj.push_back(cidx[static_cast<size_t>(A.ci[static_cast<size_t>(k)])]);
+        tv.push_back(w);
+      }
+  }
+  Csr P = from_triplets(n, nc, ti, tj, tv);
+  std::vector<uint8_t> flags(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) flags[static_cast<size_t>(i)] = state[static_cast<size_t>(i)] == coarse ? 1 : 0;
+  return {std::move(flags), std::move(P)};
+}
+
+Csr transpose(const Csr& A) {  // SpMat(P.transpose()): rows of the result ascending in column
+  Csr T;
+  T.rows = A.cols;
+  T.cols = A.rows;
+  T.rp.assign(static_cast<size_t>(A.cols) + 1, 0);
+  for (int c : A.ci) ++T.rp[static_cast<size_t>(c) + 1];
+  for (size_t c = 1; c < T.rp.size(); ++c) T.rp[c] += T.rp[c - 1];
+  T.ci.resize(A.ci.size());
+  T.v.resize(A.v.size());
+  std::vector<int> cur(T.rp.begin(), T.rp.end() - 1);
+  for (int r = 0; r < A.rows; ++r)
+    for (int k = A.rp[static_cast<size_t>(r)]; k < A.rp[static_cast<size_t>(r) + 1]; ++k) {
+      const int c = A.ci[static_cast<size_t>(k)];
+      const int pos = cur[static_cast<size_t>(c)]++;
+      T.ci[static_cast<size_t>(pos)] = r;
+      T.v[static_cast<size_t>(pos)] = A.v[static_cast<size_t>(k)];
+    }
+  return T;
+}
+
+// Eigen conservative_sparse_sparse_product for RowMajor x RowMajor: output row j
+// accumulates, in order over A's row j entries (k, a_jk) and then B's row k
+// entries (i, b_ki), values[i] = b_ki * a_jk on first touch, += afterwards;
+// columns sorted; no pruning.
+Csr spgemm(const Csr& A, const Csr& B) {
+  Csr C;
+  C.rows = A.rows;
+  C.cols = B.cols;
+  C.rp.assign(static_cast<size_t>(A.rows) + 1, 0);
+  std::vector<double> values(static_cast<size_t>(B.cols), 0.0);
+  std::vector<char> mask(static_cast<size_t>(B.cols), 0);
+  std::vector<int> idx;
+  for (int j = 0; j < A.rows; ++j) {
+    idx.clear();
+    for (int ka = A.rp[static_cast<size_t>(j)]; ka < A.rp[static_cast<size_t>(j) + 1]; ++ka) {
+      const double y = A.v[static_cast<size_t>(ka)];
+      const int k = A.ci[static_cast<size_t>(ka)];
+      for (int kb = B.rp[static_cast<size_t>(k)]; kb < B.rp[static_cast<size_t>(k) + 1]; ++kb) {
+        const int i = B.ci[static_cast<size_t>(kb)];
+        const double x = B.v[static_cast<size_t>(kb)];
+        if (!mask[static_cast<size_t>(i)]) {
+          mask[static_cast<size_t>(i)] = 1;
+          values[static_cast<size_t>(i)] = x * y;
+          idx.push_back(i);
+        } else {
+          values[static_cast<size_t>(i)] += x * y;
+        }
+      }
+    }
+    std::sort(idx.begin(), idx.end());
+    for (int i : idx) {
+      C.ci.push_back(i);
+      C.v.push_back(values[static_cast<size_t>(i)]);
+      mask[static_cast<size_t>(i)] = 0;
+    }
+    C.rp[static_cast<size_t>(j) + 1] = static_cast<int>(C.ci.size());
+  }
+  return C;
+}
+
+Csr prune(const Csr& A) {
+  Csr B;
+  B.rows = A.rows;
+  B.cols = A.cols;
+  B.rp.assign(static_cast<size_t>(A.rows) + 1, 0);
+  for (int r = 0; r < A.rows; ++r) {
+    for (int k = A.rp[static_cast<size_t>(r)]; k < A.rp[static_cast<size_t>(r) + 1]; ++k)
+      if (A.v[static_cast<size_t>(k)] != 0.0) {
+        B.ci.push_back(A.ci[static_cast<size_t>(k)]);
+        B.v.push_back(A.v[static_cast<size_t>(k)]);
+      }
+    B.rp[static_cast<size_t>(r) + 1] = static_cast<int>(B.ci.size());
+  }
+  return B;
+}
+
+Csr galerkin_coarse(const Csr& A, const Csr& P) {  // amg.cpp:58-65
+  if (A.cols != P.rows) throw std::invalid_argument("galerkin_coarse: dims");
+  const Csr AP = spgemm(A, P);
+  const Csr Pt = transpose(P);
+  return prune(spgemm(Pt, AP));
+}
+
+// amg.cpp:67-88: forward i = 0..n-1 then backward; s = f_i; s -= v x_col (col != i); x_i = s/d
+Vec sgs_sweep(const Csr& A, const Vec& f, const Vec& u) {
+  const int n = A.rows;
+  Vec x = u;
+  auto relax = [&](int i) {
+    double s = f[static_cast<size_t>(i)];
+    double d = 0.0;
+    for (int k = A.rp[static_cast<size_t>(i)]; k < A.rp[static_cast<size_t>(i) + 1]; ++k) {
+      if (A.ci[static_cast<size_t>(k)] == i)
+        d = A.v[static_cast<size_t>(k)];
+      else
+        s -= A.v[static_cast<size_t>(k)] * x[static_cast<size_t>(A.ci[static_cast<size_t>(k)])];
+    }
+    if (d == 0.0) throw std::runtime_error("sgs_sweep: zero diagonal");
+    x[static_cast<size_t>(i)] = s / d;
+  };
+  for (int i = 0; i < n; ++i) relax(i);
+  for (int i = n - 1; i >= 0; --i) relax(i);
+  return x;
+}
+
+struct Level {
+  Csr A, P, Pt;
+  std::vector<uint8_t> flags;
+  bool has_p = false;
+};
+
+struct Amg {
+  std::vector<Level> levels;
+  Llt coarsest;
+  int smoothing_steps = 1;
+};
+
+Amg build_amg(const Csr& A, int threshold, int m) {  // amg.cpp:90-117
+  Amg h;
+  h.smoothing_steps = m;
+  Csr current = A;
+  while (current.rows > threshold) {
+    Level lv;
+    lv.A = current;
+    auto fp = coarsen_redblack(lv.A);
+    if (fp.second.cols >= fp.second.rows) break;
+    lv.flags = std::move(fp.first);
+    lv.P = std::move(fp.second);
+    lv.Pt = transpose(lv.P);
+    lv.has_p = true;
+    current = galerkin_coarse(lv.A, lv.P);
+    h.levels.push_back(std::move(lv));
+  }
+  Level last;
+  last.A = current;
+  h.levels.push_back(std::move(last));
+  if (current.rows > 0) {
+    h.coarsest = llt_compute(current.rows, to_dense(current));
+    if (!h.coarsest.ok) throw std::runtime_error("build_amg: coarsest level not positive definite");
+  }
+  return h;
+}
+
+Vec vcycle(const Amg& h, size_t level, const Vec& r) {  // amg.cpp:119-132
+  const Level& lv = h.levels[level];
+  if (level + 1 == h.levels.size()) return llt_solve(h.coarsest, r);
+  Vec z(r.size(), 0.0);
+  for (int s = 0; s < h.smoothing_steps; ++s) z = sgs_sweep(lv.A, r, z);
+  const Vec Az = spmv(lv.A, z);
+  Vec res(r.size());
+  for (size_t i = 0; i < r.size(); ++i) res[i] = r[i] - Az[i];
+  const Vec rc = spmv(lv.Pt, res);
+  const Vec zc = vcycle(h, level + 1, rc);
+  const Vec Pz = spmv(lv.P, zc);
+  for (size_t i = 0; i < z.size(); ++i) z[i] = z[i] + Pz[i];
+  for (int s = 0; s < h.smoothing_steps; ++s) z = sgs_sweep(lv.A, r, z);
+  return z;
+}
+
+Vec amg_apply(const Amg& h, const Vec& r) {  // amg.cpp:136-141
+  if (h.levels.empty() || static_cast<int>(r.size()) != h.levels.front().A.rows)
+    throw std::invalid_argument("amg_apply: dimension mismatch");
+  if (r.empty()) return r;
+  return vcycle(h, 0, r);
+}
+
+struct PcgOut {
+  Vec x;
+  int iterations = 0;
+  bool converged = false;
+  std::vector<double> history;
+};
+
+// linalg.cpp:64-102
+PcgOut pcg(const std::function<Vec(const Vec&)>& apply_A, const std::function<Vec(const Vec&)>& apply_P,
+           const Vec& f, double tol, int max_iter) {
+  PcgOut out;
+  const size_t n = f.size();
+  out.x.assign(n, 0.0);
+  Vec r = f;
+  Vec z = apply_P(r);
+  double rz = dot(r, z);
+  if (rz < 0.0) throw std::runtime_error("pcg: preconditioner not positive definite");
+  const double rz0 = rz;
+  if (rz0 == 0.0) {
+    out.converged = true;
+    return out;
+  }
+  Vec p = z;
+  for (int it = 1; it <= max_iter; ++it) {
+    const Vec Ap = apply_A(p);
+    const double pAp = dot(p, Ap);
+    if (pAp <= 0.0) throw std::runtime_error("pcg: operator not positive definite (p'Ap <= 0)");
+    const double alpha = rz / pAp;
+    for (size_t i = 0; i < n; ++i) out.x[i] = out.x[i] + alpha * p[i];
+    for (size_t i = 0; i < n; ++i) r[i] = r[i] - alpha * Ap[i];
+    z = apply_P(r);
+    const double rz_next = dot(r, z);
+    if (rz_next < 0.0) throw std::runtime_error("pcg: preconditioner not positive definite");
+    const double rel = std::sqrt(rz_next / rz0);
+    out.iterations = it;
+    out.history.push_back(rel);
+    if (rel <= tol) {
+      out.converged = true;
+      return out;
+    }
+    const double beta = rz_next / rz;
+    rz = rz_next;
+    for (size_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+  }
+  return out;
+}
+
+std::vector<double> nodal_field(const Mesh& m, const DofMap& dm, const double* c) {  // assembly.cpp:358-363
+  std::vector<double> nodal(static_cast<size_t>(m.nv()), 0.0);
+  for (int d = 0; d < dm.n_dofs(); ++d) nodal[static_cast<size_t>(dm.dof_to_vertex[static_cast<size_t>(d)])] = c[d];
+  return nodal;
+}
+
+struct Exact {  // target.cpp:45-58
+  double c;
+  double u(const V3& x) const { return c * sin3(x); }
+  void grad(const V3& x, double* g) const {
+    const double sx = std::sin(kPi * x.c[0]), cx = std::cos(kPi * x.c[0]);
+    const double sy = std::sin(kPi * x.c[1]), cy = std::cos(kPi * x.c[1]);
+    const double sz = std::sin(kPi * x.c[2]), cz = std::cos(kPi * x.c[2]);
+    g[0] = c * kPi * cx * sy * sz;
+    g[1] = c * kPi * sx * cy * sz;
+    g[2] = c * kPi * sx * sy * cz;
+  }
+};
+
+Exact manufactured_exact(double rho) {
+  if (rho < 0.0) throw std::invalid_argument("manufactured_exact: rho must be >= 0");
+  return Exact{1.0 / (3.0 * rho * kPi * kPi + 1.0)};
+}
+
+// assembly.cpp:265-285
+double l2_error(const Mesh& m, const DofMap& dm, const double* coeffs, const Exact& ex) {
+  const auto nodal = nodal_field(m, dm, coeffs);
+  const Rule& rule = rule_by_id(2);
+  const double err2 = parallel_reduce(m.nt(), [&](int64_t b, int64_t e) {
+    double s = 0.0;
+    for (int64_t t = b; t < e; ++t) {
+      const auto verts = tet_vertices(m, static_cast<int>(t));
+      const auto& tet = m.tets[static_cast<size_t>(t)];
+      double acc = 0.0;
+      for (int q = 0; q < rule.size(); ++q) {
+        const auto& lam = rule.pts[static_cast<size_t>(q)];
+        const V3 x = physical_point(lam, verts);
+        double u = 0.0;
+        for (int i = 0; i < 4; ++i) u += lam[static_cast<size_t>(i)] * nodal[static_cast<size_t>(tet[static_cast<size_t>(i)])];
+        const double d = u - ex.u(x);
+        acc += rule.w[static_cast<size_t>(q)] * d * d;
+      }
+      s += tet_volume(m, static_cast<int>(t)) * acc;
+    }
+    return s;
+  });
+  return std::sqrt(err2);
+}
+
+// assembly.cpp:287-310
+double h1_semi_error(const Mesh& m, const DofMap& dm, const double* coeffs, const Exact& ex) {
+  const auto nodal = nodal_field(m, dm, coeffs);
+  const Rule& rule = rule_by_id(2);
+  const double err2 = parallel_reduce(m.nt(), [&](int64_t b, int64_t e) {
+    double s = 0.0;
+    for (int64_t t = b; t < e; ++t) {
+      const auto verts = tet_vertices(m, static_cast<int>(t));
+      const LocalGeom g = local_geom(verts);
+      const auto& tet = m.tets[static_cast<size_t>(t)];
+      double gu[3] = {0.0, 0.0, 0.0};
+      for (int i = 0; i < 4; ++i)
+        for (int c = 0; c < 3; ++c) gu[c] = gu[c] + nodal[static_cast<size_t>(tet[static_cast<size_t>(i)])] * g.grad[i][c];
+      double acc = 0.0;
+      for (int q = 0; q < rule.size(); ++q) {
+        const V3 x = physical_point(rule.pts[static_cast<size_t>(q)], verts);
+        double ge[3];
+        ex.grad(x, ge);
+        const double d0 = gu[0] - ge[0], d1 = gu[1] - ge[1], d2 = gu[2] - ge[2];
+        acc += rule.w[static_cast<size_t>(q)] * ((d0 * d0 + d1 * d1) + d2 * d2);
+      }
+      s += g.volume * acc;
+    }
+    return s;
+  });
+  return std::sqrt(err2);
+}
+
+template <class F>
+int guard(F&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C surface
+struct or_mesh {
+  Mesh m;
+};
+struct or_csr {
+  Csr a;
+};
+struct or_system {
+  System s;
+  or_csr views[3];
+};
+struct or_amg {
+  Amg h;
+  std::vector<or_csr> views;  // 3 per level
+};
+
+extern "C" {
+
+const char* or_last_error(void) { return g_err.c_str(); }
+void or_set_num_threads(int n) { g_threads = n < 1 ? 1 : n; }
+int or_num_threads(void) { return g_threads; }
+
+int or_build_structured_cube(int n, or_mesh** out) {
+  return guard([&] { *out = new or_mesh{build_structured_cube(n)}; });
+}
+void or_mesh_free(or_mesh* m) { delete m; }
+int or_mesh_new(int nv, const double* xyz, int nt, const int* tets, const uint8_t* boundary, or_mesh** out) {
+  return guard([&] {
+    auto* m = new or_mesh;
+    for (int v = 0; v < nv; ++v) {
+      m->m.vertices.push_back(V3{{xyz[3 * v], xyz[3 * v + 1], xyz[3 * v + 2]}});
+      m->m.boundary.push_back(boundary[v]);
+    }
+    for (int t = 0; t < nt; ++t) {
+      m->m.tets.push_back({tets[4 * t], tets[4 * t + 1], tets[4 * t + 2], tets[4 * t + 3]});
+      m->m.refinement_edge.push_back(3);
+      m->m.generation.push_back(0);
+    }
+    *out = m;
+  });
+}
+void or_mesh_info(const or_mesh* m, int* nv, int* nt) {
+  *nv = m->m.nv();
+  *nt = m->m.nt();
+}
+void or_mesh_get(const or_mesh* m, double* xyz, int* tets, uint8_t* bnd, uint8_t* re, int* gen) {
+  const Mesh& M = m->m;
+  for (int v = 0; v < M.nv(); ++v)
+    for (int c = 0; c < 3; ++c) {
+      if (xyz) xyz[3 * v + c] = M.vertices[static_cast<size_t>(v)].c[c];
+    }
+  for (int t = 0; t < M.nt(); ++t)
+    for (int c = 0; c < 4; ++c)
+      if (tets) tets[4 * t + c] = M.tets[static_cast<size_t>(t)][static_cast<size_t>(c)];
+  if (bnd) std::memcpy(bnd, M.boundary.data(), M.boundary.size());
+  if (re) std::memcpy(re, M.refinement_edge.data(), M.refinement_edge.size());
+  if (gen) std::memcpy(gen, M.generation.data(), M.generation.size() * sizeof(int));
+}
+double or_tet_volume(const or_mesh* m, int t) { return tet_volume(m->m, t); }
+
+int or_rule_size(int rule) { return rule_by_id(rule).size(); }
+void or_rule_get(int rule, double* pts, double* w) {
+  const Rule& r = rule_by_id(rule);
+  for (int q = 0; q < r.size(); ++q) {
+    for (int k = 0; k < 4; ++k) pts[4 * q + k] = r.pts[static_cast<size_t>(q)][static_cast<size_t>(k)];
+    w[q] = r.w[static_cast<size_t>(q)];
+  }
+}
+
+int or_target_eval(int kind, int n, uint64_t seed, int npts, const double* xyz, double* out) {
+  return guard([&] {
+    const Target t = make_target(kind, n, seed);
+    for (int i = 0; i < npts; ++i) out[i] = t(V3{{xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]}});
+  });
+}
+void or_pseudo_random_vec(int n, uint64_t seed, double* out) { pseudo_random(n, seed, out); }
+
+static int mesh_resolution(const Mesh& m) {
+  // structured cube: (n+1)^3 vertices
+  int n = 0;
+  while ((n + 1) * (n + 1) * (n + 1) < m.nv()) ++n;
+  return n;
+}
+
+int or_build_system(const or_mesh* m, double rho, int kind, uint64_t seed, or_system** out) {
+  return guard([&] {
+    const Target t = make_target(kind, kind == OR_TARGET_SINE_RANDOM ? mesh_resolution(m->m) : 0, seed);
+    auto* s = new or_system;
+    s->s = build_system(m->m, rho, t);
+    *out = s;
+  });
+}
+void or_system_free(or_system* s) { delete s; }
+int or_system_n_dofs(const or_system* s) { return s->s.dm.n_dofs(); }
+or_csr* or_system_csr(or_system* s, int which) {
+  const Csr& c = which == 0 ? s->s.K : which == 1 ? s->s.M : s->s.A;
+  s->views[which].a = c;
+  return &s->views[which];
+}
+void or_system_get_f(const or_system* s, double* f) { std::memcpy(f, s->s.f.data(), s->s.f.size() * sizeof(double)); }
+void or_system_get_dofmap(const or_system* s, int* v2d, int* d2v) {
+  if (v2d) std::memcpy(v2d, s->s.dm.vertex_to_dof.data(), s->s.dm.vertex_to_dof.size() * sizeof(int));
+  if (d2v) std::memcpy(d2v, s->s.dm.dof_to_vertex.data(), s->s.dm.dof_to_vertex.size() * sizeof(int));
+}
+int or_assemble_full(const or_mesh* m, int which, or_csr** out) {
+  return guard([&] {
+    std::vector<int> rows(static_cast<size_t>(m->m.nv()));
+    for (int i = 0; i < m->m.nv(); ++i) rows[static_cast<size_t>(i)] = i;
+    *out = new or_csr{assemble_matrix(m->m, rows, rows, which == 0 ? 1.0 : 0.0, which == 1 ? 1.0 : 0.0)};
+  });
+}
+int or_assemble_load(const or_mesh* m, int kind, uint64_t seed, double* f) {
+  return guard([&] {
+    const Target t = make_target(kind, kind == OR_TARGET_SINE_RANDOM ? mesh_resolution(m->m) : 0, seed);
+    const DofMap dm = interior_dof_map(m->m);
+    const Vec v = load_vector(m->m, dm, t);
+    std::memcpy(f, v.data(), v.size() * sizeof(double));
+  });
+}
+
+int or_csr_new(int rows, int cols, int64_t nnz, const int* rp, const int* ci, const double* v, or_csr** out) {
+  return guard([&] {
+    auto* c = new or_csr;
+    c->a.rows = rows;
+    c->a.cols = cols;
+    c->a.rp.assign(rp, rp + rows + 1);
+    c->a.ci.assign(ci, ci + nnz);
+    c->a.v.assign(v, v + nnz);
+    *out = c;
+  });
+}
+int or_from_triplets(int rows, int cols, int64_t n, const int* ti, const int* tj, const double* tv, or_csr** out) {
+  return guard([&] {
+    *out = new or_csr{from_triplets(rows, cols, std::vector<int>(ti, ti + n), std::vector<int>(tj, tj + n),
+                                    std::vector<double>(tv, tv + n))};
+  });
+}
+void or_csr_free(or_csr* a) { delete a; }
+void or_csr_info(const or_csr* a, int* rows, int* cols, int64_t* nnz) {
+  *rows = a->a.rows;
+  *cols = a->a.cols;
+  *nnz = a->a.nnz();
+}
+void or_csr_get(const or_csr* a, int* rp, int* ci, double* v) {
+  if (rp) std::memcpy(rp, a->a.rp.data(), a->a.rp.size() * sizeof(int));
+  if (ci) std::memcpy(ci, a->a.ci.data(), a->a.ci.size() * sizeof(int));
+  if (v) std::memcpy(v, a->a.v.data(), a->a.v.size() * sizeof(double));
+}
+
+int or_spmv(const or_csr* a, int nx, const double* x, double* y) {
+  return guard([&] {
+    const Vec r = spmv(a->a, Vec(x, x + nx));
+    std::memcpy(y, r.data(), r.size() * sizeof(double));
+  });
+}
+int or_dense_cholesky_solve(int n, const double* A, const double* b, double* x) {
+  return guard([&] {
+    const Llt f = llt_compute(n, std::vector<double>(A, A + static_cast<size_t>(n) * n));
+    if (!f.ok) throw std::runtime_error("dense_cholesky_solve: matrix not positive definite");
+    const Vec r = llt_solve(f, Vec(b, b + n));
+    std::memcpy(x, r.data(), r.size() * sizeof(double));
+  });
+}
+double or_dot(int n, const double* a, const double* b) { return eigen_dot(a, b, n); }
+
+int or_coarsen_redblack(const or_csr* a, uint8_t* flags, or_csr** p_out) {
+  return guard([&] {
+    auto fp = coarsen_redblack(a->a);
+    std::memcpy(flags, fp.first.data(), fp.first.size());
+    *p_out = new or_csr{std::move(fp.second)};
+  });
+}
+int or_galerkin_coarse(const or_csr* a, const or_csr* p, or_csr** out) {
+  return guard([&] { *out = new or_csr{galerkin_coarse(a->a, p->a)}; });
+}
+int or_sgs_sweep(const or_csr* a, const double* f, const double* u, double* out) {
+  return guard([&] {
+    const int n = a->a.rows;
+    const Vec r = sgs_sweep(a->a, Vec(f, f + n), Vec(u, u + n));
+    std::memcpy(out, r.data(), r.size() * sizeof(double));
+  });
+}
+int or_build_amg(const or_csr* a, int thr, int m, or_amg** out) {
+  return guard([&] {
+    auto* h = new or_amg;
+    h->h = build_amg(a->a, thr, m);
+    h->views.resize(h->h.levels.size() * 3);
+    *out = h;
+  });
+}
+void or_amg_free(or_amg* h) { delete h; }
+int or_amg_num_levels(const or_amg* h) { return static_cast<int>(h->h.levels.size()); }
+or_csr* or_amg_level_csr(or_amg* h, int level, int which) {
+  if (level < 0 || level >= static_cast<int>(h->h.levels.size())) return nullptr;
+  const Level& lv = h->h.levels[static_cast<size_t>(level)];
+  if (which != 0 && !lv.has_p) return nullptr;
+  or_csr* v = &h->views[static_cast<size_t>(level) * 3 + static_cast<size_t>(which)];
+  v->a = which == 0 ? lv.A : which == 1 ? lv.P : lv.Pt;
+  return v;
+}
+int or_amg_level_flags(const or_amg* h, int level, uint8_t* flags) {
+  const Level& lv = h->h.levels[static_cast<size_t>(level)];
+  if (!lv.has_p) return 1;
+  std::memcpy(flags, lv.flags.data(), lv.flags.size());
+  return 0;
+}
+int or_amg_apply(const or_amg* h, int n, const double* r, double* z) {
+  return guard([&] {
+    const Vec out = amg_apply(h->h, Vec(r, r + n));
+    std::memcpy(z, out.data(), out.size() * sizeof(double));
+  });
+}
+
+int or_pcg(const or_csr* a, int precond, const or_amg* h, const double* f, double tol, int max_iter, double* x,
+           int* iterations, int* converged, double* history) {
+  return guard([&] {
+    const Csr& A = a->a;
+    const int n = A.rows;
+    std::function<Vec(const Vec&)> P;
+    if (precond == 0) {
+      P = [](const Vec& r) { return r; };
+    } else if (precond == 1) {
+      Vec d(static_cast<size_t>(n), 0.0);
+      for (int i = 0; i < n; ++i)
+        for (int k = A.rp[static_cast<size_t>(i)]; k < A.rp[static_cast<size_t>(i) + 1]; ++k)
+          if (A.ci[static_cast<size_t>(k)] == i) d[static_cast<size_t>(i)] = A.v[static_cast<size_t>(k)];
+      for (double v : d)
+        if (v <= 0.0) throw std::runtime_error("jacobi_precond: non-positive diagonal");
+      P = [d](const Vec& r) {
+        Vec z(r.size());
+        for (size_t i = 0; i < r.size(); ++i) z[i] = r[i] / d[i];
+        return z;
+      };
+    } else {
+      if (!h) throw std::invalid_argument("pcg: amg preconditioner requires a hierarchy");
+      P = [h](const Vec& r) { return amg_apply(h->h, r); };
+    }
+    const PcgOut o = pcg([&A](const Vec& v) { return spmv(A, v); }, P, Vec(f, f + n), tol, max_iter);
+    std::memcpy(x, o.x.data(), o.x.size() * sizeof(double));
+    *iterations = o.iterations;
+    *converged = o.converged ? 1 : 0;
+    if (history) std::memcpy(history, o.history.data(), o.history.size() * sizeof(double));
+  });
+}
+
+int or_solve_system_amg(const or_system* s, double tol, double* u, int* iterations, int* converged,
+                        double* setup_seconds, double* solve_seconds) {
+  return guard([&] {
+    using clk = std::chrono::steady_clock;
+    *iterations = 0;
+    *converged = 0;
+    *setup_seconds = *solve_seconds = 0.0;
+    if (s->s.f.empty()) {
+      *converged = 1;
+      return;
+    }
+    const auto t0 = clk::now();
+    const Amg h = build_amg(s->s.A, 64, 1);
+    const auto t1 = clk::now();
+    const Csr& A = s->s.A;
+    const PcgOut o = pcg([&A](const Vec& v) { return spmv(A, v); }, [&h](const Vec& r) { return amg_apply(h, r); },
+                         s->s.f, tol, 500);
+    const auto t2 = clk::now();
+    std::memcpy(u, o.x.data(), o.x.size() * sizeof(double));
+    *iterations = o.iterations;
+    *converged = o.converged ? 1 : 0;
+    *setup_seconds = std::chrono::duration<double>(t1 - t0).count();
+    *solve_seconds = std::chrono::duration<double>(t2 - t1).count();
+  });
+}
+
+int or_l2_error_manufactured(const or_mesh* m, const or_system* s, const double* coeffs, double rho, double* out) {
+  return guard([&] { *out = l2_error(m->m, s->s.dm, coeffs, manufactured_exact(rho)); });
+}
+int or_h1_semi_error_manufactured(const or_mesh* m, const or_system* s, const double* coeffs, double rho,
+                                  double* out) {
+  return guard([&] { *out = h1_semi_error(m->m, s->s.dm, coeffs, manufactured_exact(rho)); });
+}
+
+}  // extern "C"

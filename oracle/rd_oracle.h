@@ -1,0 +1,114 @@
+/*
+ * rd_oracle.h -- TEST INFRASTRUCTURE ONLY (parity checker), never the product.
+ *
+ * C-callable surface of the CPU restatement of the reference's AMG-PCG solve
+ * path (rdsolve, arXiv 2102.03515).  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load liboracle.so.
+ *
+ * Every object is an opaque heap handle freed with or_free().  Functions that
+ * can fail return an int status (0 = ok, 1 = invalid_argument, 2 =
+ * runtime_error, mirroring the reference's exception types) and leave the
+ * message in or_last_error().
+ */
+#ifndef RD_ORACLE_H
+#define RD_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct or_mesh or_mesh;
+typedef struct or_system or_system;
+typedef struct or_csr or_csr;
+typedef struct or_amg or_amg;
+
+const char* or_last_error(void);
+void or_set_num_threads(int n);
+int or_num_threads(void);
+
+/* mesh.cpp:29-65 */
+int or_build_structured_cube(int n, or_mesh** out);
+void or_mesh_free(or_mesh* m);
+/* a hand-built mesh (test_assembly.cpp:23-33 reference tet) */
+int or_mesh_new(int nv, const double* xyz, int nt, const int* tets, const uint8_t* boundary,
+                or_mesh** out);
+void or_mesh_info(const or_mesh* m, int* n_vertices, int* n_tets);
+void or_mesh_get(const or_mesh* m, double* xyz, int* tets, uint8_t* boundary,
+                 uint8_t* refinement_edge, int* generation);
+double or_tet_volume(const or_mesh* m, int t);
+
+/* quadrature.cpp: rule 0 centroid, 1 degree2, 2 degree5 (14pt), 3 subdivision64 */
+int or_rule_size(int rule);
+void or_rule_get(int rule, double* points /* size x 4 */, double* weights);
+
+/* target.cpp + the two BASELINE targets (ball, sine+random) */
+enum { OR_TARGET_SMOOTH = 0, OR_TARGET_BOX = 1, OR_TARGET_NONZERO_BC = 2,
+       OR_TARGET_BALL = 3, OR_TARGET_SINE_RANDOM = 4,
+       /* test-only targets from the reference's assembly tests */
+       OR_TARGET_ZERO = 5, OR_TARGET_ONE = 6, OR_TARGET_QUADRATIC = 7 };
+int or_target_eval(int kind, int n, uint64_t seed, int npts, const double* xyz,
+                   double* out);
+void or_pseudo_random_vec(int n, uint64_t seed, double* out);
+
+/* assembly.cpp:225-238 build_system */
+int or_build_system(const or_mesh* m, double rho, int target_kind, uint64_t seed,
+                    or_system** out);
+void or_system_free(or_system* s);
+int or_system_n_dofs(const or_system* s);
+/* which: 0 = K, 1 = M, 2 = A */
+or_csr* or_system_csr(or_system* s, int which); /* borrowed */
+void or_system_get_f(const or_system* s, double* f);
+void or_system_get_dofmap(const or_system* s, int* vertex_to_dof, int* dof_to_vertex);
+/* assembly.cpp full (pre-elimination) matrices: which 0 = K, 1 = M */
+int or_assemble_full(const or_mesh* m, int which, or_csr** out);
+int or_assemble_load(const or_mesh* m, int target_kind, uint64_t seed, double* f);
+
+/* CSR containers (types.hpp:14, linalg.cpp:11-17) */
+int or_csr_new(int rows, int cols, int64_t nnz, const int* rp, const int* ci,
+               const double* v, or_csr** out);
+int or_from_triplets(int rows, int cols, int64_t n, const int* ti, const int* tj,
+                     const double* tv, or_csr** out);
+void or_csr_free(or_csr* a);
+void or_csr_info(const or_csr* a, int* rows, int* cols, int64_t* nnz);
+void or_csr_get(const or_csr* a, int* rp, int* ci, double* v);
+
+/* linalg.cpp */
+int or_spmv(const or_csr* a, int nx, const double* x, double* y);
+int or_dense_cholesky_solve(int n, const double* a_rowmajor, const double* b, double* x);
+double or_dot(int n, const double* a, const double* b);
+
+/* amg.cpp */
+int or_coarsen_redblack(const or_csr* a, uint8_t* flags, or_csr** p_out);
+int or_galerkin_coarse(const or_csr* a, const or_csr* p, or_csr** out);
+int or_sgs_sweep(const or_csr* a, const double* f, const double* u, double* out);
+int or_build_amg(const or_csr* a, int coarsest_threshold, int smoothing_steps,
+                 or_amg** out);
+void or_amg_free(or_amg* h);
+int or_amg_num_levels(const or_amg* h);
+/* which: 0 = A, 1 = P, 2 = Pt ; borrowed, NULL when absent */
+or_csr* or_amg_level_csr(or_amg* h, int level, int which);
+int or_amg_level_flags(const or_amg* h, int level, uint8_t* flags);
+int or_amg_apply(const or_amg* h, int n, const double* r, double* z);
+
+/* linalg.cpp:64-102; precond: 0 identity, 1 jacobi, 2 amg (uses h) */
+int or_pcg(const or_csr* a, int precond, const or_amg* h, const double* f,
+           double tol, int max_iter, double* x, int* iterations, int* converged,
+           double* history /* >= max_iter entries, may be NULL */);
+
+/* bench.cpp:185-241 solve_system, AMG branch */
+int or_solve_system_amg(const or_system* s, double tol, double* u, int* iterations,
+                        int* converged, double* setup_seconds, double* solve_seconds);
+
+/* assembly.cpp:265-310 error norms against the closed form (manufactured_exact) */
+int or_l2_error_manufactured(const or_mesh* m, const or_system* s, const double* coeffs,
+                             double rho_exact, double* out);
+int or_h1_semi_error_manufactured(const or_mesh* m, const or_system* s,
+                                  const double* coeffs, double rho_exact, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif
