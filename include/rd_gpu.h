@@ -1,0 +1,171 @@
+/*
+ * rd_gpu.h -- C-ABI of the B200-native AMG-PCG solve path (arXiv 2102.03515).
+ *
+ * This is the drop-in boundary.  Each entry point replaces one function of
+ * the reference C++ library rdsolve; the replaced interface is cited as
+ * file:line relative to /root/reference/proj.  Plain pointers and sizes
+ * only: no torch, no Eigen, no C++ types.  INTEGRATION.md shows the thin
+ * rd:: C++ layer a maintainer adds on the reference side.
+ *
+ * Vectors (double*) may be HOST or DEVICE pointers; the library inspects
+ * them (cudaPointerGetAttributes).  Calls that take host pointers are
+ * synchronous; calls on device pointers are stream-ordered on the context's
+ * stream, and device-detected errors (zero diagonal, loss of positive
+ * definiteness) are returned by the call itself when it must synchronise
+ * anyway (pcg, solve_system) or by the next rd_gpu_synchronize().
+ *
+ * Status codes map one-to-one onto the reference's exceptions
+ * (SURVEY.md §8(b)); a thin C++ layer rethrows them.
+ */
+#ifndef RD_GPU_H
+#define RD_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status */
+#define RD_OK 0
+#define RD_EINVAL 1       /* std::invalid_argument (dimension / parameter errors)        */
+#define RD_ERUNTIME 2     /* std::runtime_error (generic)                                */
+#define RD_ENOTSPD 3      /* runtime_error: pcg "operator/preconditioner not positive
+                             definite", build_amg "coarsest level not positive definite",
+                             dense_cholesky_solve "matrix not positive definite"          */
+#define RD_EZERODIAG 4    /* runtime_error: "sgs_sweep: zero diagonal" (amg.cpp:82)       */
+#define RD_ECUDA 5        /* CUDA runtime failure                                         */
+#define RD_ENCCL 6        /* NCCL failure (multi-GPU)                                     */
+#define RD_EDEGENERATE 7  /* runtime_error: "assembly: degenerate tet" (assembly.cpp:46)  */
+
+typedef struct rd_ctx rd_ctx;
+typedef struct rd_mesh rd_mesh;
+typedef struct rd_csr rd_csr;
+typedef struct rd_system rd_system;
+typedef struct rd_amg rd_amg;
+
+/* ------------------------------------------------------------ context */
+/* One device, one stream (NULL: the library creates a non-blocking stream). */
+int rd_gpu_ctx_create(int device, void* cuda_stream, rd_ctx** out);
+void rd_gpu_ctx_destroy(rd_ctx* ctx);
+const char* rd_gpu_last_error(const rd_ctx* ctx);
+void* rd_gpu_ctx_stream(rd_ctx* ctx);
+/* Waits for the stream; returns the first device-detected error, if any. */
+int rd_gpu_synchronize(rd_ctx* ctx);
+/* Number of rd_gpu kernels launched on this context so far. */
+int64_t rd_gpu_launch_count(const rd_ctx* ctx);
+const char* rd_gpu_version(void);
+/* cudaMemcpyDefault between any host/device buffers, ordered on the ctx stream, synchronous */
+int rd_gpu_copy(rd_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+/* ------------------------------------------------------------ mesh */
+/* replaces rd::build_structured_cube(int n)            mesh.hpp:36, mesh.cpp:29-65 */
+int rd_gpu_build_structured_cube(rd_ctx* ctx, int n, rd_mesh** out);
+/* uploads a host rd::TetMesh (vertices AoS xyz, tets int[4], boundary flags)  mesh.hpp:13-24 */
+int rd_gpu_mesh_create(rd_ctx* ctx, int n_vertices, const double* xyz, int n_tets,
+                       const int32_t* tets, const uint8_t* boundary, rd_mesh** out);
+void rd_gpu_mesh_free(rd_mesh* mesh);
+/* lattice_n = n for build_structured_cube meshes, -1 otherwise */
+int rd_gpu_mesh_info(const rd_mesh* mesh, int* n_vertices, int* n_tets, int* lattice_n);
+int rd_gpu_mesh_download(const rd_mesh* mesh, double* xyz, int32_t* tets, uint8_t* boundary);
+
+/* ------------------------------------------------------------ assembly */
+/* TargetField (target.hpp:12-16).  kinds 0-2 are the reference's targets
+ * (target.cpp:17-43); 3 (ball) and 4 (sine + 0.1 * seeded random P1 field)
+ * are the BASELINE.json config targets; 5-7 are the reference tests'
+ * zero / one / x*y+2z loads (test_assembly.cpp:37,102-154).               */
+enum {
+  RD_TARGET_SMOOTH = 0,
+  RD_TARGET_BOX = 1,
+  RD_TARGET_NONZERO_BC = 2,
+  RD_TARGET_BALL = 3,
+  RD_TARGET_SINE_RANDOM = 4,
+  RD_TARGET_ZERO = 5,
+  RD_TARGET_ONE = 6,
+  RD_TARGET_QUADRATIC = 7
+};
+typedef struct {
+  int kind;
+  uint64_t seed; /* splitmix64 seed for RD_TARGET_SINE_RANDOM (tests/oracles.hpp:97-108) */
+} rd_target;
+
+/* replaces rd::build_system(mesh, rho, target)   assembly.hpp:48, assembly.cpp:225-238
+ * K (pruned), M (pruned), A = rho*K + M (not pruned), load f -- all on device. */
+int rd_gpu_build_system(rd_ctx* ctx, const rd_mesh* mesh, double rho, const rd_target* target,
+                        rd_system** out);
+void rd_gpu_system_free(rd_system* sys);
+int rd_gpu_system_n_dofs(const rd_system* sys);
+/* which: 0 = K, 1 = M, 2 = A.  Borrowed; lives as long as sys. */
+const rd_csr* rd_gpu_system_matrix(const rd_system* sys, int which);
+/* device pointer to the load vector f (n_dofs doubles); borrowed */
+const double* rd_gpu_system_load(const rd_system* sys);
+/* DofMap (assembly.hpp:15-22); either pointer may be NULL */
+int rd_gpu_system_dofmap(const rd_system* sys, int32_t* vertex_to_dof, int32_t* dof_to_vertex);
+
+/* ------------------------------------------------------------ CSR */
+/* SpMat = Eigen::SparseMatrix<double, RowMajor, int> (types.hpp:14): row_ptr
+ * int32[rows+1], col_idx int32[nnz] (ascending per row), values fp64[nnz].
+ * Arrays may be host or device pointers; the handle owns a device copy. */
+int rd_gpu_csr_create(rd_ctx* ctx, int rows, int cols, int64_t nnz, const int32_t* row_ptr,
+                      const int32_t* col_idx, const double* values, rd_csr** out);
+void rd_gpu_csr_free(rd_csr* a);
+int rd_gpu_csr_info(const rd_csr* a, int* rows, int* cols, int64_t* nnz);
+int rd_gpu_csr_download(const rd_csr* a, int32_t* row_ptr, int32_t* col_idx, double* values);
+
+/* ------------------------------------------------------------ kernels */
+/* replaces rd::spmv(A, x)                                linalg.hpp:30, linalg.cpp:19-33 */
+int rd_gpu_spmv(rd_ctx* ctx, const rd_csr* a, const double* x, double* y);
+/* deterministic device dot product (fixed reduction tree) */
+int rd_gpu_dot(rd_ctx* ctx, int n, const double* a, const double* b, double* out);
+/* replaces rd::coarsen_redblack(A)                       amg.hpp:29, amg.cpp:7-56 */
+int rd_gpu_coarsen_redblack(rd_ctx* ctx, const rd_csr* a, uint8_t* flags, rd_csr** p_out);
+/* replaces rd::galerkin_coarse(A, P)                     amg.hpp:31, amg.cpp:58-65 */
+int rd_gpu_galerkin_coarse(rd_ctx* ctx, const rd_csr* a, const rd_csr* p, rd_csr** out);
+/* replaces rd::sgs_sweep(A, f, u)                        amg.hpp:34, amg.cpp:67-88 */
+int rd_gpu_sgs_sweep(rd_ctx* ctx, const rd_csr* a, const double* f, const double* u, double* out);
+
+/* ------------------------------------------------------------ AMG */
+/* replaces rd::build_amg(A, coarsest_threshold, smoothing_steps)  amg.hpp:36-37, amg.cpp:90-117.
+ * The handle keeps its own copy of A; A may be freed afterwards. */
+int rd_gpu_amg_setup(rd_ctx* ctx, const rd_csr* a, int coarsest_threshold, int smoothing_steps,
+                     rd_amg** out);
+void rd_gpu_amg_free(rd_amg* h);
+int rd_gpu_amg_num_levels(const rd_amg* h);
+/* which: 0 = A_l, 1 = P_l, 2 = Pt_l (NULL on the coarsest level); borrowed */
+const rd_csr* rd_gpu_amg_level_matrix(const rd_amg* h, int level, int which);
+/* coarse_flag of level l (1 = C), host buffer of rows(A_l) bytes */
+int rd_gpu_amg_level_flags(const rd_amg* h, int level, uint8_t* flags);
+/* 1 if level l runs the structured (lattice-stencil) smoother, 0 for the generic one */
+int rd_gpu_amg_level_structured(const rd_amg* h, int level);
+/* replaces rd::amg_apply(h, r) / amg_precond(h)          amg.hpp:39-42, amg.cpp:119-145 */
+int rd_gpu_amg_apply(rd_amg* h, const double* r, double* z);
+
+/* ------------------------------------------------------------ PCG */
+typedef struct {
+  int iterations;
+  int converged;
+} rd_pcg_report;
+
+/* replaces rd::pcg(A, amg_precond(h), f, tol, max_iter)  linalg.hpp:46-49, linalg.cpp:64-102.
+ * amg == NULL selects the identity preconditioner.  residual_history (host,
+ * >= max_iter doubles) may be NULL.  Zero initial guess. */
+int rd_gpu_pcg(rd_ctx* ctx, const rd_csr* a, rd_amg* amg, const double* f, double tol, int max_iter,
+               double* x, rd_pcg_report* report, double* residual_history);
+
+/* replaces rd::solve_system(mesh, sys, PrecondKind::amg, p, tol)  bench.hpp:48-57, bench.cpp:185-225:
+ * build_amg(A) [setup_seconds], pcg(A, amg, f, tol, 500) [solve_seconds]. */
+typedef struct {
+  int iterations;
+  int converged;
+  double setup_seconds;
+  double solve_seconds;
+} rd_solve_outcome;
+int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, double tol, double* u,
+                            rd_solve_outcome* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RD_GPU_H */

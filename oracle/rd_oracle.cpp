@@ -747,9 +747,9 @@ Vec llt_solve(const Llt& f, const Vec& b) {
     for (int k = 0; k < i; ++k) s -= f.L[static_cast<size_t>(i) * n + k] * y[static_cast<size_t>(k)];
     y[static_cast<size_t>(i)] = s / f.L[static_cast<size_t>(i) * n + i];
   }
-  for (int i = n - 1; i >= 0; --i) {
+  for (int i = n - 1; i >= 0; --i) {  // back substitution, sums in descending k
     double s = y[static_cast<size_t>(i)];
-    for (int k = i + 1; k < n; ++k) s -= f.L[static_cast<size_t>(k) * n + i] * x[static_cast<size_t>(k)];
+    for (int k = n - 1; k > i; --k) s -= f.L[static_cast<size_t>(k) * n + i] * x[static_cast<size_t>(k)];
     x[static_cast<size_t>(i)] = s / f.L[static_cast<size_t>(i) * n + i];
   }
   return x;

@@ -1,0 +1,637 @@
+// assembly.cu -- device mesh generation and P1 assembly (mesh.cpp:29-65,
+// assembly.cpp:14-238) on sm_100a.
+//
+// Data layout in HBM: vertices AoS fp64[nv][3]; tets int32[nt][4] in the
+// reference's Kuhn-chain order; vertex->tet CSR with ascending tet ids (the
+// order every per-row accumulation below relies on).
+//
+// Assembly is row-gather and owner-computes, exactly like the reference: row r
+// (vertex v) visits its incident tets in ascending id and accumulates into the
+// slot found by binary search in its sorted column list.  K and M are
+// accumulated separately, pruned separately, then A = rho*K + M is formed as
+// Eigen's union sum (rho*K_ij + M_ij, no FMA, no pruning) -- App. B.
+//
+// The load vector integrates every tet ONCE (all four local test functions,
+// same per-slot operation order as the reference's per-row loop) and then
+// gathers per row in ascending tet order: bit-identical to the reference's
+// 4x-redundant row loop with a quarter of the quadrature work.
+#include <algorithm>
+#include <cmath>
+
+#include "internal.hpp"
+
+namespace rdg {
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+// ---------------------------------------------------------------- quadrature rules
+// quadrature.cpp:24-82, built on the host with the reference's own expressions
+struct Rules {
+  double p14[14][4];
+  double w14[14];
+  double p64[64][4];
+  double w64[64];
+};
+__constant__ Rules c_rules;
+
+Rules make_rules() {
+  Rules r{};
+  const double wa = 0.1126879257180162, a = 0.3108859192633005;
+  const double wb = 0.0734930431163619, b = 0.0927352503108912;
+  const double wc = 0.0425460207770812, c = 0.0455037041256497;
+  int q = 0;
+  for (int i = 0; i < 4; ++i, ++q) {
+    for (int k = 0; k < 4; ++k) r.p14[q][k] = a;
+    r.p14[q][i] = 1.0 - 3.0 * a;
+    r.w14[q] = wa;
+  }
+  for (int i = 0; i < 4; ++i, ++q) {
+    for (int k = 0; k < 4; ++k) r.p14[q][k] = b;
+    r.p14[q][i] = 1.0 - 3.0 * b;
+    r.w14[q] = wb;
+  }
+  for (int i = 0; i < 4; ++i)
+    for (int j = i + 1; j < 4; ++j, ++q) {
+      for (int k = 0; k < 4; ++k) r.p14[q][k] = 0.5 - c;
+      r.p14[q][i] = c;
+      r.p14[q][j] = c;
+      r.w14[q] = wc;
+    }
+  // subdivision64: 3 levels of centroid splitting (dyadic, exact)
+  struct Cell {
+    double m[4][4];
+  };
+  std::vector<Cell> cells(1);
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) cells[0].m[i][j] = i == j ? 1.0 : 0.0;
+  auto colmean = [](const Cell& cl, double* g) {
+    for (int j = 0; j < 4; ++j) {
+      double s = 0.0;
+      for (int i = 0; i < 4; ++i) s += cl.m[i][j];
+      g[j] = s / 4.0;
+    }
+  };
+  for (int level = 0; level < 3; ++level) {
+    std::vector<Cell> next;
+    for (const Cell& cl : cells) {
+      double g[4];
+      colmean(cl, g);
+      for (int i = 0; i < 4; ++i) {
+        Cell ch = cl;
+        for (int j = 0; j < 4; ++j) ch.m[i][j] = g[j];
+        next.push_back(ch);
+      }
+    }
+    cells.swap(next);
+  }
+  for (int k = 0; k < 64; ++k) {
+    colmean(cells[k], r.p64[k]);
+    r.w64[k] = 1.0 / 64.0;
+  }
+  return r;
+}
+
+void upload_rules(Ctx& c) {
+  static bool done = false;
+  if (done) return;
+  const Rules r = make_rules();
+  RDG_CUDA(cudaMemcpyToSymbolAsync(c_rules, &r, sizeof(Rules), 0, cudaMemcpyHostToDevice, c.stream));
+  RDG_CUDA(cudaStreamSynchronize(c.stream));
+  done = true;
+}
+
+// ---------------------------------------------------------------- mesh
+__device__ __forceinline__ bool on_unit_boundary(double x, double y, double z) {  // mesh.cpp:14-18
+  return fabs(x) <= 1e-14 || fabs(x - 1.0) <= 1e-14 || fabs(y) <= 1e-14 || fabs(y - 1.0) <= 1e-14 ||
+         fabs(z) <= 1e-14 || fabs(z - 1.0) <= 1e-14;
+}
+
+__global__ void cube_vertices_kernel(int n, double* xyz, uint8_t* bnd) {
+  const int nv = n + 1;
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= (int64_t)nv * nv * nv) return;
+  const int i = (int)(v % nv), j = (int)((v / nv) % nv), k = (int)(v / ((int64_t)nv * nv));
+  const double x = __ddiv_rn((double)i, (double)n), y = __ddiv_rn((double)j, (double)n),
+               z = __ddiv_rn((double)k, (double)n);
+  xyz[3 * v] = x;
+  xyz[3 * v + 1] = y;
+  xyz[3 * v + 2] = z;
+  bnd[v] = on_unit_boundary(x, y, z) ? 1 : 0;
+}
+
+__global__ void cube_tets_kernel(int n, int* tets) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * n * n * 6) return;
+  const int nv = n + 1;
+  const int p = (int)(t % 6);
+  const int64_t cell = t / 6;
+  int c[3] = {(int)(cell % n), (int)((cell / n) % n), (int)(cell / ((int64_t)n * n))};
+  const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  int4 out;
+  out.x = (c[2] * nv + c[1]) * nv + c[0];
+  c[perms[p][0]] += 1;
+  out.y = (c[2] * nv + c[1]) * nv + c[0];
+  c[perms[p][1]] += 1;
+  out.z = (c[2] * nv + c[1]) * nv + c[0];
+  c[perms[p][2]] += 1;
+  out.w = (c[2] * nv + c[1]) * nv + c[0];
+  reinterpret_cast<int4*>(tets)[t] = out;
+}
+
+// ---------------------------------------------------------------- dof map, adjacency
+__global__ void interior_flag_kernel(int nv, const uint8_t* __restrict__ bnd, int* flag) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nv) flag[v] = bnd[v] ? 0 : 1;
+}
+
+__global__ void dofmap_kernel(int nv, const uint8_t* __restrict__ bnd, const int* __restrict__ off, int* v2d,
+                              int* d2v) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  if (bnd[v]) {
+    v2d[v] = -1;
+  } else {
+    v2d[v] = off[v];
+    d2v[off[v]] = v;
+  }
+}
+
+__global__ void vt_count_kernel(int nt, const int* __restrict__ tets, int* cnt) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < (int64_t)nt * 4) atomicAdd(cnt + tets[k], 1);
+}
+
+__global__ void vt_fill_kernel(int nt, const int* __restrict__ tets, int* cursor, int* vt) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (int64_t)nt * 4) return;
+  const int pos = atomicAdd(cursor + tets[k], 1);
+  vt[pos] = (int)(k >> 2);
+}
+
+__global__ void sort_segments_kernel(int n, const int* __restrict__ off, int* a) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int b = off[v], e = off[v + 1];
+  for (int k = b + 1; k < e; ++k) {
+    const int key = a[k];
+    int j = k - 1;
+    while (j >= b && a[j] > key) {
+      a[j + 1] = a[j];
+      --j;
+    }
+    a[j + 1] = key;
+  }
+}
+
+// ---------------------------------------------------------------- pattern
+constexpr int kMaxRowCols = 128;
+
+// unique sorted dofs of all vertices of the incident tets (assembly.cpp:61-80)
+template <bool FILL>
+__global__ void pattern_kernel(int nd, const int* __restrict__ d2v, const int* __restrict__ v2d,
+                               const int* __restrict__ vto, const int* __restrict__ vt,
+                               const int* __restrict__ tets, int* cnt, const int* __restrict__ rp, int* ci,
+                               int* err) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nd) return;
+  const int v = d2v[r];
+  int cols[kMaxRowCols];
+  int u = 0;
+  for (int k = vto[v]; k < vto[v + 1]; ++k) {
+    const int4 t = reinterpret_cast<const int4*>(tets)[vt[k]];
+    const int w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = v2d[w[q]];
+      if (c < 0) continue;
+      // sorted insert (dedup)
+      int pos = 0;
+      while (pos < u && cols[pos] < c) ++pos;
+      if (pos < u && cols[pos] == c) continue;
+      if (u == kMaxRowCols) {
+        atomicExch(err, RD_EINVAL);
+        return;
+      }
+      for (int m = u; m > pos; --m) cols[m] = cols[m - 1];
+      cols[pos] = c;
+      ++u;
+    }
+  }
+  if (!FILL) {
+    cnt[r] = u;
+  } else {
+    const int o = rp[r];
+    for (int q = 0; q < u; ++q) ci[o + q] = cols[q];
+  }
+}
+
+// ---------------------------------------------------------------- geometry
+struct Geom {
+  double vol;
+  double g[4][3];
+};
+
+// assembly.cpp:38-51 with Eigen's 3x3 determinant and cofactor inverse (the
+// oracle's restatement, operation for operation)
+__device__ __forceinline__ bool local_geom(const double* v0, const double* v1, const double* v2, const double* v3,
+                                           Geom& G) {
+  double J[3][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    J[r][0] = __dsub_rn(v1[r], v0[r]);
+    J[r][1] = __dsub_rn(v2[r], v0[r]);
+    J[r][2] = __dsub_rn(v3[r], v0[r]);
+  }
+  auto det3 = [&](int a, int b, int c) {
+    return __dmul_rn(J[0][a], __dsub_rn(__dmul_rn(J[1][b], J[2][c]), __dmul_rn(J[1][c], J[2][b])));
+  };
+  const double det = __dadd_rn(__dsub_rn(det3(0, 1, 2), det3(1, 0, 2)), det3(2, 0, 1));
+  G.vol = __ddiv_rn(fabs(det), 6.0);
+  if (!(G.vol > 0.0)) return false;
+  auto cof = [&](int i, int j) {
+    const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+    return __dsub_rn(__dmul_rn(J[i1][j1], J[i2][j2]), __dmul_rn(J[i1][j2], J[i2][j1]));
+  };
+  const double c0[3] = {cof(0, 0), cof(1, 0), cof(2, 0)};
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(c0[0], J[0][0]), __dmul_rn(c0[1], J[1][0])), __dmul_rn(c0[2], J[2][0]));
+  const double invdet = __ddiv_rn(1.0, d2);
+  G.g[1][0] = __dmul_rn(c0[0], invdet);
+  G.g[1][1] = __dmul_rn(c0[1], invdet);
+  G.g[1][2] = __dmul_rn(c0[2], invdet);
+  G.g[2][0] = __dmul_rn(cof(0, 1), invdet);
+  G.g[2][1] = __dmul_rn(cof(1, 1), invdet);
+  G.g[2][2] = __dmul_rn(cof(2, 1), invdet);
+  G.g[3][0] = __dmul_rn(cof(0, 2), invdet);
+  G.g[3][1] = __dmul_rn(cof(1, 2), invdet);
+  G.g[3][2] = __dmul_rn(cof(2, 2), invdet);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) G.g[0][c] = -__dadd_rn(__dadd_rn(G.g[1][c], G.g[2][c]), G.g[3][c]);
+  return true;
+}
+
+__device__ __forceinline__ double dot3(const double* a, const double* b) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[0]), __dmul_rn(a[1], b[1])), __dmul_rn(a[2], b[2]));
+}
+
+// assembly.cpp:97-126: per row, tets ascending, jv = 0..3 -> K and M slots
+__global__ void values_kernel(int nd, const int* __restrict__ d2v, const int* __restrict__ v2d,
+                              const int* __restrict__ vto, const int* __restrict__ vt,
+                              const int* __restrict__ tets, const double* __restrict__ xyz,
+                              const int* __restrict__ rp, const int* __restrict__ ci, double* Kf, double* Mf,
+                              int* err) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nd) return;
+  const int v = d2v[r];
+  const int rb = rp[r], re = rp[r + 1];
+  for (int q = rb; q < re; ++q) {
+    Kf[q] = 0.0;
+    Mf[q] = 0.0;
+  }
+  for (int k = vto[v]; k < vto[v + 1]; ++k) {
+    const int4 t4 = reinterpret_cast<const int4*>(tets)[vt[k]];
+    const int tv[4] = {t4.x, t4.y, t4.z, t4.w};
+    Geom G;
+    if (!local_geom(xyz + 3 * (int64_t)tv[0], xyz + 3 * (int64_t)tv[1], xyz + 3 * (int64_t)tv[2],
+                    xyz + 3 * (int64_t)tv[3], G)) {
+      atomicExch(err, RD_EDEGENERATE);
+      return;
+    }
+    int iv = 0;
+    while (tv[iv] != v) ++iv;
+#pragma unroll
+    for (int jv = 0; jv < 4; ++jv) {
+      const int c = v2d[tv[jv]];
+      if (c < 0) continue;
+      // K: val = 0.0; val += (1.0*vol) * dot  -- M: val = 0.0; val += (1.0*vol) * (0.1|0.05)
+      const double valK = __dadd_rn(0.0, __dmul_rn(__dmul_rn(1.0, G.vol), dot3(G.g[iv], G.g[jv])));
+      const double valM = __dadd_rn(0.0, __dmul_rn(__dmul_rn(1.0, G.vol), iv == jv ? 0.1 : 0.05));
+      int lo = rb, hi = re;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ci[mid] < c)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      Kf[lo] = __dadd_rn(Kf[lo], valK);
+      Mf[lo] = __dadd_rn(Mf[lo], valM);
+    }
+  }
+}
+
+// counts of the pruned K, pruned M, and their union (A)
+__global__ void split_count_kernel(int nd, const int* __restrict__ rp, const double* __restrict__ Kf,
+                                   const double* __restrict__ Mf, int* kc, int* mc, int* ac) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nd) return;
+  int a = 0, b = 0, u = 0;
+  for (int q = rp[r]; q < rp[r + 1]; ++q) {
+    const bool k = Kf[q] != 0.0, m = Mf[q] != 0.0;
+    a += k;
+    b += m;
+    u += (k || m);
+  }
+  kc[r] = a;
+  mc[r] = b;
+  ac[r] = u;
+}
+
+__global__ void split_fill_kernel(int nd, double rho, const int* __restrict__ rp, const int* __restrict__ ci,
+                                  const double* __restrict__ Kf, const double* __restrict__ Mf,
+                                  const int* __restrict__ krp, int* kci, double* kv, const int* __restrict__ mrp,
+                                  int* mci, double* mv, const int* __restrict__ arp, int* aci, double* av) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nd) return;
+  int ko = krp[r], mo = mrp[r], ao = arp[r];
+  for (int q = rp[r]; q < rp[r + 1]; ++q) {
+    const double kq = Kf[q], mq = Mf[q];
+    const bool k = kq != 0.0, m = mq != 0.0;
+    const int c = ci[q];
+    if (k) {
+      kci[ko] = c;
+      kv[ko++] = kq;
+    }
+    if (m) {
+      mci[mo] = c;
+      mv[mo++] = mq;
+    }
+    if (k || m) {
+      aci[ao] = c;
+      // Eigen union sum: both -> rho*K + M, K only -> rho*K + 0, M only -> 0 + M
+      av[ao++] = k && m ? __dadd_rn(__dmul_rn(rho, kq), mq) : (k ? __dadd_rn(__dmul_rn(rho, kq), 0.0) : __dadd_rn(0.0, mq));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- targets (target.cpp + BASELINE)
+__device__ __forceinline__ double sin3(double x, double y, double z) {
+  return __dmul_rn(__dmul_rn(sin(__dmul_rn(kPi, x)), sin(__dmul_rn(kPi, y))), sin(__dmul_rn(kPi, z)));
+}
+
+// P1 interpolant of the nodal field on the Kuhn lattice (oracle Target::interp)
+__device__ double lattice_interp(const double* __restrict__ nodal, int n, double x, double y, double z) {
+  const int nv = n + 1;
+  const double p[3] = {x, y, z};
+  int cell[3];
+  double xi[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double s = __dmul_rn(p[d], (double)n);
+    int c = (int)floor(s);
+    c = min(max(c, 0), n - 1);
+    cell[d] = c;
+    xi[d] = __dsub_rn(s, (double)c);
+  }
+  const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  int pi = 0;
+  for (; pi < 5; ++pi)
+    if (xi[perms[pi][0]] >= xi[perms[pi][1]] && xi[perms[pi][1]] >= xi[perms[pi][2]]) break;
+  const int p0 = perms[pi][0], p1 = perms[pi][1], p2 = perms[pi][2];
+  const double lam[4] = {__dsub_rn(1.0, xi[p0]), __dsub_rn(xi[p0], xi[p1]), __dsub_rn(xi[p1], xi[p2]), xi[p2]};
+  int c[3] = {cell[0], cell[1], cell[2]};
+  double val = 0.0;
+  val = __dadd_rn(val, __dmul_rn(lam[0], nodal[(c[2] * nv + c[1]) * nv + c[0]]));
+  c[p0] += 1;
+  val = __dadd_rn(val, __dmul_rn(lam[1], nodal[(c[2] * nv + c[1]) * nv + c[0]]));
+  c[p1] += 1;
+  val = __dadd_rn(val, __dmul_rn(lam[2], nodal[(c[2] * nv + c[1]) * nv + c[0]]));
+  c[p2] += 1;
+  val = __dadd_rn(val, __dmul_rn(lam[3], nodal[(c[2] * nv + c[1]) * nv + c[0]]));
+  return val;
+}
+
+__device__ __forceinline__ double target_eval(int kind, double x, double y, double z, const double* nodal, int n) {
+  switch (kind) {
+    case RD_TARGET_SMOOTH: return sin3(x, y, z);
+    case RD_TARGET_BOX:
+      return (x > 0.25 && x < 0.75 && y > 0.25 && y < 0.75 && z > 0.25 && z < 0.75) ? 1.0 : 0.0;
+    case RD_TARGET_NONZERO_BC: return __dadd_rn(1.0, sin3(x, y, z));
+    case RD_TARGET_BALL: {
+      const double dx = __dsub_rn(x, 0.5), dy = __dsub_rn(y, 0.5), dz = __dsub_rn(z, 0.5);
+      return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)) < 0.0625 ? 1.0 : 0.0;
+    }
+    case RD_TARGET_SINE_RANDOM:
+      return __dadd_rn(sin3(x, y, z), __dmul_rn(0.1, lattice_interp(nodal, n, x, y, z)));
+    case RD_TARGET_ZERO: return 0.0;
+    case RD_TARGET_ONE: return 1.0;
+    case RD_TARGET_QUADRATIC: return __dadd_rn(__dmul_rn(x, y), __dmul_rn(2.0, z));
+  }
+  return 0.0;
+}
+
+// splitmix64 nodal field (tests/oracles.hpp:97-108), zeroed on the boundary
+__global__ void random_nodal_kernel(int n, uint64_t seed, double* nodal) {
+  const int nv = n + 1;
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= (int64_t)nv * nv * nv) return;
+  const int i = (int)(v % nv), j = (int)((v / nv) % nv), k = (int)(v / ((int64_t)nv * nv));
+  if (i == 0 || j == 0 || k == 0 || i == n || j == n || k == n) {
+    nodal[v] = 0.0;
+    return;
+  }
+  uint64_t z = seed + 0x9e3779b97f4a7c15ULL + (uint64_t)(v + 1) * 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  z = z ^ (z >> 31);
+  nodal[v] = __dsub_rn(__dmul_rn(2.0, __dmul_rn((double)(z >> 11), 0x1.0p-53)), 1.0);
+}
+
+// per tet: vol (mesh.cpp:188-191 cross-product formula) and acc[iv] =
+// sum_q (w_q u(x_q)) lambda_q,iv for all four iv (assembly.cpp:152-171)
+template <int NQ>
+__global__ void load_tet_kernel(int nt, const int* __restrict__ tets, const double* __restrict__ xyz, int kind,
+                                const double* __restrict__ nodal, int n, double* tacc, double* tvol) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const int4 t4 = reinterpret_cast<const int4*>(tets)[t];
+  const int tv[4] = {t4.x, t4.y, t4.z, t4.w};
+  double V[4][3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) V[k][c] = xyz[3 * (int64_t)tv[k] + c];
+  double a[3], b[3], d[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    a[c] = __dsub_rn(V[1][c], V[0][c]);
+    b[c] = __dsub_rn(V[2][c], V[0][c]);
+    d[c] = __dsub_rn(V[3][c], V[0][c]);
+  }
+  const double x0 = __dsub_rn(__dmul_rn(a[1], b[2]), __dmul_rn(a[2], b[1]));
+  const double x1 = __dsub_rn(__dmul_rn(a[2], b[0]), __dmul_rn(a[0], b[2]));
+  const double x2 = __dsub_rn(__dmul_rn(a[0], b[1]), __dmul_rn(a[1], b[0]));
+  const double dt = __dadd_rn(__dadd_rn(__dmul_rn(x0, d[0]), __dmul_rn(x1, d[1])), __dmul_rn(x2, d[2]));
+  tvol[t] = __ddiv_rn(fabs(dt), 6.0);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int q = 0; q < NQ; ++q) {
+    const double* lam = NQ == 14 ? c_rules.p14[q] : c_rules.p64[q];
+    const double w = NQ == 14 ? c_rules.w14[q] : c_rules.w64[q];
+    double X[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s = __dadd_rn(s, __dmul_rn(lam[k], V[k][c]));
+      X[c] = s;
+    }
+    const double wu = __dmul_rn(w, target_eval(kind, X[0], X[1], X[2], nodal, n));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] = __dadd_rn(acc[k], __dmul_rn(wu, lam[k]));
+  }
+  reinterpret_cast<double4*>(tacc)[t] = make_double4(acc[0], acc[1], acc[2], acc[3]);
+}
+
+__global__ void load_gather_kernel(int nd, const int* __restrict__ d2v, const int* __restrict__ vto,
+                                   const int* __restrict__ vt, const int* __restrict__ tets,
+                                   const double* __restrict__ tacc, const double* __restrict__ tvol, double* f) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nd) return;
+  const int v = d2v[r];
+  double s = 0.0;
+  for (int k = vto[v]; k < vto[v + 1]; ++k) {
+    const int t = vt[k];
+    const int4 t4 = reinterpret_cast<const int4*>(tets)[t];
+    const int iv = t4.x == v ? 0 : t4.y == v ? 1 : t4.z == v ? 2 : 3;
+    s = __dadd_rn(s, __dmul_rn(tvol[t], tacc[4 * (int64_t)t + iv]));
+  }
+  f[r] = s;
+}
+
+int read_flag(Ctx& c, const int* d) {
+  int h = 0;
+  RDG_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  RDG_CUDA(cudaStreamSynchronize(c.stream));
+  return h;
+}
+
+}  // namespace
+
+void build_structured_cube(Ctx& c, int n, DMesh& m) {
+  if (n < 1) throw Error(RD_EINVAL, "build_structured_cube: n must be >= 1");
+  const int64_t nv = (int64_t)(n + 1) * (n + 1) * (n + 1), nt = (int64_t)n * n * n * 6;
+  if (nt * 4 > 0x7fffffffLL) throw Error(RD_EINVAL, "build_structured_cube: n too large for int32 tet ids");
+  m.nv = (int)nv;
+  m.nt = (int)nt;
+  m.lattice_n = n;
+  m.xyz.alloc(nv * 3, c.stream);
+  m.boundary.alloc(nv, c.stream);
+  m.tets.alloc(nt * 4, c.stream);
+  cube_vertices_kernel<<<div_up(nv, 256), 256, 0, c.stream>>>(n, m.xyz.p, m.boundary.p);
+  RDG_LAUNCH_CHECK();
+  cube_tets_kernel<<<div_up(nt, 256), 256, 0, c.stream>>>(n, m.tets.p);
+  RDG_LAUNCH_CHECK();
+  c.launches += 2;
+}
+
+void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, DSystem& s) {
+  if (!(rho > 0.0)) throw Error(RD_EINVAL, "build_system: rho must be > 0");
+  if (kind < 0 || kind > RD_TARGET_QUADRATIC) throw Error(RD_EINVAL, "build_system: unknown target kind");
+  if (kind == RD_TARGET_SINE_RANDOM && m.lattice_n < 1)
+    throw Error(RD_EINVAL, "build_system: the sine+random target needs a build_structured_cube mesh");
+  upload_rules(c);
+  s.rho = rho;
+  s.nv = m.nv;
+  const int nv = m.nv, nt = m.nt;
+  DBuf<int> err(1, c.stream);
+  RDG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.stream));
+  // ---- interior dof map (assembly.cpp:187-197)
+  DBuf<int> flag(std::max(nv, 1), c.stream), off(nv + 1, c.stream);
+  interior_flag_kernel<<<div_up(nv, 256), 256, 0, c.stream>>>(nv, m.boundary.p, flag.p);
+  RDG_LAUNCH_CHECK();
+  s.n_dofs = (int)exclusive_scan(c, flag.p, off.p, nv);
+  const int nd = s.n_dofs;
+  s.v2d.alloc(std::max(nv, 1), c.stream);
+  s.d2v.alloc(std::max(nd, 1), c.stream);
+  dofmap_kernel<<<div_up(nv, 256), 256, 0, c.stream>>>(nv, m.boundary.p, off.p, s.v2d.p, s.d2v.p);
+  RDG_LAUNCH_CHECK();
+  c.launches += 2;
+  // ---- vertex -> tet CSR, ascending tets (assembly.cpp:14-31)
+  DBuf<int> vcnt(nv + 1, c.stream), vto(nv + 1, c.stream), vt(std::max<int64_t>((int64_t)nt * 4, 1), c.stream);
+  RDG_CUDA(cudaMemsetAsync(vcnt.p, 0, sizeof(int) * (nv + 1), c.stream));
+  vt_count_kernel<<<div_up((int64_t)nt * 4, 256), 256, 0, c.stream>>>(nt, m.tets.p, vcnt.p);
+  RDG_LAUNCH_CHECK();
+  exclusive_scan(c, vcnt.p, vto.p, nv);
+  RDG_CUDA(cudaMemcpyAsync(vcnt.p, vto.p, sizeof(int) * nv, cudaMemcpyDeviceToDevice, c.stream));
+  vt_fill_kernel<<<div_up((int64_t)nt * 4, 256), 256, 0, c.stream>>>(nt, m.tets.p, vcnt.p, vt.p);
+  RDG_LAUNCH_CHECK();
+  sort_segments_kernel<<<div_up(nv, 256), 256, 0, c.stream>>>(nv, vto.p, vt.p);
+  RDG_LAUNCH_CHECK();
+  c.launches += 3;
+  // ---- pattern
+  DBuf<int> rcnt(std::max(nd, 1), c.stream), frp(nd + 1, c.stream);
+  if (nd) {
+    pattern_kernel<false><<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p,
+                                                                 rcnt.p, nullptr, nullptr, err.p);
+    RDG_LAUNCH_CHECK();
+    ++c.launches;
+  }
+  if (read_flag(c, err.p)) throw Error(RD_EINVAL, "assembly: row has more than 128 columns");
+  const int64_t zf = exclusive_scan(c, rcnt.p, frp.p, nd);
+  DBuf<int> fci(std::max<int64_t>(zf, 1), c.stream);
+  DBuf<double> Kf(std::max<int64_t>(zf, 1), c.stream), Mf(std::max<int64_t>(zf, 1), c.stream);
+  if (nd) {
+    pattern_kernel<true><<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p,
+                                                                nullptr, frp.p, fci.p, err.p);
+    RDG_LAUNCH_CHECK();
+    values_kernel<<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p, m.xyz.p,
+                                                         frp.p, fci.p, Kf.p, Mf.p, err.p);
+    RDG_LAUNCH_CHECK();
+    c.launches += 2;
+  }
+  if (read_flag(c, err.p)) throw Error(RD_EDEGENERATE, "assembly: degenerate tet");
+  // ---- prune K, M; A = rho*K + M (assembly.cpp:129,234)
+  DBuf<int> kc(std::max(nd, 1), c.stream), mc(std::max(nd, 1), c.stream), ac(std::max(nd, 1), c.stream);
+  if (nd) {
+    split_count_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, frp.p, Kf.p, Mf.p, kc.p, mc.p, ac.p);
+    RDG_LAUNCH_CHECK();
+    ++c.launches;
+  }
+  DCsr* mats[3] = {&s.K, &s.M, &s.A};
+  int* cnts[3] = {kc.p, mc.p, ac.p};
+  for (int w = 0; w < 3; ++w) {
+    DCsr& X = *mats[w];
+    X = DCsr{};
+    X.rows = X.cols = nd;
+    X.rp.alloc(nd + 1, c.stream);
+    X.nnz = exclusive_scan(c, cnts[w], X.rp.p, nd);
+    X.ci.alloc(X.nnz, c.stream);
+    X.v.alloc(X.nnz, c.stream);
+  }
+  if (nd) {
+    split_fill_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, rho, frp.p, fci.p, Kf.p, Mf.p, s.K.rp.p, s.K.ci.p,
+                                                             s.K.v.p, s.M.rp.p, s.M.ci.p, s.M.v.p, s.A.rp.p,
+                                                             s.A.ci.p, s.A.v.p);
+    RDG_LAUNCH_CHECK();
+    ++c.launches;
+  }
+  // ---- load vector (assembly.cpp:140-174)
+  s.f.alloc(std::max(nd, 1), c.stream);
+  if (nd) {
+    DBuf<double> nodal;
+    const int n = m.lattice_n;
+    if (kind == RD_TARGET_SINE_RANDOM) {
+      nodal.alloc(nv, c.stream);
+      random_nodal_kernel<<<div_up(nv, 256), 256, 0, c.stream>>>(n, seed, nodal.p);
+      RDG_LAUNCH_CHECK();
+      ++c.launches;
+    }
+    DBuf<double> tacc((size_t)nt * 4, c.stream), tvol(nt, c.stream);
+    const bool disc = kind == RD_TARGET_BOX || kind == RD_TARGET_BALL;  // Smoothness::discontinuous
+    if (disc)
+      load_tet_kernel<64><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, kind, nodal.p, n, tacc.p,
+                                                                 tvol.p);
+    else
+      load_tet_kernel<14><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, kind, nodal.p, n, tacc.p,
+                                                                 tvol.p);
+    RDG_LAUNCH_CHECK();
+    load_gather_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, s.d2v.p, vto.p, vt.p, m.tets.p, tacc.p, tvol.p,
+                                                              s.f.p);
+    RDG_LAUNCH_CHECK();
+    c.launches += 2;
+  }
+  RDG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+}  // namespace rdg

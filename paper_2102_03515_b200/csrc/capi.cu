@@ -1,0 +1,498 @@
+// capi.cu -- the extern "C" boundary declared in include/rd_gpu.h.
+//
+// Each function converts rdg::Error into the status code that maps onto the
+// reference's exception type and leaves the message in rd_gpu_last_error().
+#include <chrono>
+#include <cstring>
+
+#include "internal.hpp"
+
+using namespace rdg;
+
+namespace {
+
+thread_local std::string g_noctx_err;
+
+template <class F>
+int guard(rd_ctx* ctx, F&& fn) {
+  try {
+    fn();
+    return RD_OK;
+  } catch (const Error& e) {
+    (ctx ? ctx->c.err : g_noctx_err) = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    (ctx ? ctx->c.err : g_noctx_err) = "out of host memory";
+    return RD_ERUNTIME;
+  } catch (const std::exception& e) {
+    (ctx ? ctx->c.err : g_noctx_err) = e.what();
+    return RD_ERUNTIME;
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// device view of an input vector (copies host data into tmp)
+template <class T>
+const T* in_dev(Ctx& c, const T* p, size_t n, DBuf<T>& tmp) {
+  if (n == 0) return p;
+  if (!p) throw Error(RD_EINVAL, "null vector");
+  if (is_device_ptr(p)) return p;
+  tmp.alloc(n, c.stream);
+  RDG_CUDA(cudaMemcpyAsync(tmp.p, p, sizeof(T) * n, cudaMemcpyHostToDevice, c.stream));
+  return tmp.p;
+}
+
+// device destination for an output vector; call finish() to copy back
+template <class T>
+struct OutVec {
+  Ctx& c;
+  T* user;
+  size_t n;
+  DBuf<T> tmp;
+  bool host;
+  OutVec(Ctx& cc, T* p, size_t nn) : c(cc), user(p), n(nn), host(!is_device_ptr(p)) {
+    if (n && !p) throw Error(RD_EINVAL, "null output vector");
+    if (host && n) tmp.alloc(n, c.stream);
+  }
+  T* dev() { return host ? tmp.p : user; }
+  void finish() {
+    if (host && n) RDG_CUDA(cudaMemcpyAsync(user, tmp.p, sizeof(T) * n, cudaMemcpyDeviceToHost, c.stream));
+  }
+};
+
+int take_device_error(Ctx& c) {
+  int h = 0;
+  RDG_CUDA(cudaMemcpyAsync(&h, c.d_err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  RDG_CUDA(cudaStreamSynchronize(c.stream));
+  if (h) RDG_CUDA(cudaMemsetAsync(c.d_err, 0, sizeof(int), c.stream));
+  return h;
+}
+
+void sync_and_raise(Ctx& c) {
+  const int e = take_device_error(c);
+  if (e == RD_EZERODIAG) throw Error(e, "sgs_sweep: zero diagonal");
+  if (e) throw Error(e, "device error");
+}
+
+void require(bool ok, const char* msg) {
+  if (!ok) throw Error(RD_EINVAL, msg);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rd_gpu_version(void) { return "rd_gpu 0.1 (sm_100a)"; }
+
+int rd_gpu_ctx_create(int device, void* stream, rd_ctx** out) {
+  return guard(nullptr, [&] {
+    require(out != nullptr, "rd_gpu_ctx_create: out is null");
+    RDG_CUDA(cudaSetDevice(device));
+    auto* ctx = new rd_ctx;
+    Ctx& c = ctx->c;
+    c.device = device;
+    RDG_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
+    if (stream) {
+      c.stream = static_cast<cudaStream_t>(stream);
+      c.own_stream = false;
+    } else {
+      RDG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    RDG_CUDA(cudaMalloc(&c.d_err, sizeof(int)));
+    RDG_CUDA(cudaMalloc(&c.d_counter, 64 * sizeof(unsigned)));
+    RDG_CUDA(cudaMalloc(&c.d_partials, Ctx::kMaxPartials * sizeof(double)));
+    RDG_CUDA(cudaMallocHost(&c.h_pinned, 64 * sizeof(double)));
+    RDG_CUDA(cudaMemsetAsync(c.d_err, 0, sizeof(int), c.stream));
+    RDG_CUDA(cudaMemsetAsync(c.d_counter, 0, 64 * sizeof(unsigned), c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    *out = ctx;
+  });
+}
+
+void rd_gpu_ctx_destroy(rd_ctx* ctx) {
+  if (!ctx) return;
+  Ctx& c = ctx->c;
+  cudaStreamSynchronize(c.stream);
+  cudaFree(c.d_err);
+  cudaFree(c.d_counter);
+  cudaFree(c.d_partials);
+  cudaFreeHost(c.h_pinned);
+  if (c.own_stream) cudaStreamDestroy(c.stream);
+  delete ctx;
+}
+
+const char* rd_gpu_last_error(const rd_ctx* ctx) { return ctx ? ctx->c.err.c_str() : g_noctx_err.c_str(); }
+void* rd_gpu_ctx_stream(rd_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.stream) : nullptr; }
+int64_t rd_gpu_launch_count(const rd_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int rd_gpu_copy(rd_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guard(ctx, [&] {
+    if (!bytes) return;
+    require(dst && src, "rd_gpu_copy: null pointer");
+    RDG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->c.stream));
+    RDG_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int rd_gpu_synchronize(rd_ctx* ctx) {
+  return guard(ctx, [&] { sync_and_raise(ctx->c); });
+}
+
+// ------------------------------------------------------------ mesh
+int rd_gpu_build_structured_cube(rd_ctx* ctx, int n, rd_mesh** out) {
+  return guard(ctx, [&] {
+    auto m = std::make_unique<rd_mesh>();
+    m->ctx = ctx;
+    build_structured_cube(ctx->c, n, m->m);
+    *out = m.release();
+  });
+}
+
+int rd_gpu_mesh_create(rd_ctx* ctx, int nv, const double* xyz, int nt, const int32_t* tets, const uint8_t* bnd,
+                       rd_mesh** out) {
+  return guard(ctx, [&] {
+    require(nv >= 0 && nt >= 0, "rd_gpu_mesh_create: negative size");
+    Ctx& c = ctx->c;
+    auto m = std::make_unique<rd_mesh>();
+    m->ctx = ctx;
+    m->m.nv = nv;
+    m->m.nt = nt;
+    m->m.lattice_n = -1;
+    m->m.xyz.alloc((size_t)nv * 3, c.stream);
+    m->m.tets.alloc((size_t)nt * 4, c.stream);
+    m->m.boundary.alloc(nv, c.stream);
+    const cudaMemcpyKind k = cudaMemcpyDefault;
+    if (nv) RDG_CUDA(cudaMemcpyAsync(m->m.xyz.p, xyz, sizeof(double) * 3 * nv, k, c.stream));
+    if (nt) RDG_CUDA(cudaMemcpyAsync(m->m.tets.p, tets, sizeof(int) * 4 * nt, k, c.stream));
+    if (nv) RDG_CUDA(cudaMemcpyAsync(m->m.boundary.p, bnd, nv, k, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    *out = m.release();
+  });
+}
+
+void rd_gpu_mesh_free(rd_mesh* m) {
+  if (!m) return;
+  cudaStreamSynchronize(m->ctx->c.stream);
+  delete m;
+}
+
+int rd_gpu_mesh_info(const rd_mesh* m, int* nv, int* nt, int* lat) {
+  if (!m) return RD_EINVAL;
+  if (nv) *nv = m->m.nv;
+  if (nt) *nt = m->m.nt;
+  if (lat) *lat = m->m.lattice_n;
+  return RD_OK;
+}
+
+int rd_gpu_mesh_download(const rd_mesh* m, double* xyz, int32_t* tets, uint8_t* bnd) {
+  return guard(m->ctx, [&] {
+    Ctx& c = m->ctx->c;
+    if (xyz && m->m.nv) RDG_CUDA(cudaMemcpyAsync(xyz, m->m.xyz.p, sizeof(double) * 3 * m->m.nv, cudaMemcpyDefault, c.stream));
+    if (tets && m->m.nt) RDG_CUDA(cudaMemcpyAsync(tets, m->m.tets.p, sizeof(int) * 4 * m->m.nt, cudaMemcpyDefault, c.stream));
+    if (bnd && m->m.nv) RDG_CUDA(cudaMemcpyAsync(bnd, m->m.boundary.p, m->m.nv, cudaMemcpyDefault, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+// ------------------------------------------------------------ system
+int rd_gpu_build_system(rd_ctx* ctx, const rd_mesh* mesh, double rho, const rd_target* target, rd_system** out) {
+  return guard(ctx, [&] {
+    require(mesh && target && out, "rd_gpu_build_system: null argument");
+    auto s = std::make_unique<rd_system>();
+    s->ctx = ctx;
+    build_system(ctx->c, mesh->m, rho, target->kind, target->seed, s->s);
+    DCsr* mats[3] = {&s->s.K, &s->s.M, &s->s.A};
+    for (int w = 0; w < 3; ++w) {
+      s->views[w].ctx = ctx;
+      s->views[w].a = mats[w];
+    }
+    *out = s.release();
+  });
+}
+
+void rd_gpu_system_free(rd_system* s) {
+  if (!s) return;
+  cudaStreamSynchronize(s->ctx->c.stream);
+  delete s;
+}
+int rd_gpu_system_n_dofs(const rd_system* s) { return s ? s->s.n_dofs : -1; }
+const rd_csr* rd_gpu_system_matrix(const rd_system* s, int which) {
+  if (!s || which < 0 || which > 2) return nullptr;
+  return &s->views[which];
+}
+const double* rd_gpu_system_load(const rd_system* s) { return s ? s->s.f.p : nullptr; }
+int rd_gpu_system_dofmap(const rd_system* s, int32_t* v2d, int32_t* d2v) {
+  return guard(s->ctx, [&] {
+    Ctx& c = s->ctx->c;
+    if (v2d && s->s.nv) RDG_CUDA(cudaMemcpyAsync(v2d, s->s.v2d.p, sizeof(int) * s->s.nv, cudaMemcpyDefault, c.stream));
+    if (d2v && s->s.n_dofs)
+      RDG_CUDA(cudaMemcpyAsync(d2v, s->s.d2v.p, sizeof(int) * s->s.n_dofs, cudaMemcpyDefault, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+// ------------------------------------------------------------ CSR
+int rd_gpu_csr_create(rd_ctx* ctx, int rows, int cols, int64_t nnz, const int32_t* rp, const int32_t* ci,
+                      const double* v, rd_csr** out) {
+  return guard(ctx, [&] {
+    require(rows >= 0 && cols >= 0 && nnz >= 0 && nnz <= 0x7fffffffLL, "rd_gpu_csr_create: bad size");
+    require(rp != nullptr && out != nullptr, "rd_gpu_csr_create: null argument");
+    Ctx& c = ctx->c;
+    auto h = std::make_unique<rd_csr>();
+    h->ctx = ctx;
+    h->owned = std::make_unique<DCsr>();
+    DCsr& A = *h->owned;
+    A.rows = rows;
+    A.cols = cols;
+    A.nnz = nnz;
+    A.rp.alloc(rows + 1, c.stream);
+    A.ci.alloc(nnz, c.stream);
+    A.v.alloc(nnz, c.stream);
+    RDG_CUDA(cudaMemcpyAsync(A.rp.p, rp, sizeof(int) * (rows + 1), cudaMemcpyDefault, c.stream));
+    if (nnz) {
+      RDG_CUDA(cudaMemcpyAsync(A.ci.p, ci, sizeof(int) * nnz, cudaMemcpyDefault, c.stream));
+      RDG_CUDA(cudaMemcpyAsync(A.v.p, v, sizeof(double) * nnz, cudaMemcpyDefault, c.stream));
+    }
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    h->a = h->owned.get();
+    *out = h.release();
+  });
+}
+
+void rd_gpu_csr_free(rd_csr* a) {
+  if (!a || !a->owned) return;  // borrowed views are owned by their system / hierarchy
+  cudaStreamSynchronize(a->ctx->c.stream);
+  delete a;
+}
+
+int rd_gpu_csr_info(const rd_csr* a, int* rows, int* cols, int64_t* nnz) {
+  if (!a || !a->a) return RD_EINVAL;
+  if (rows) *rows = a->a->rows;
+  if (cols) *cols = a->a->cols;
+  if (nnz) *nnz = a->a->nnz;
+  return RD_OK;
+}
+
+int rd_gpu_csr_download(const rd_csr* a, int32_t* rp, int32_t* ci, double* v) {
+  return guard(a->ctx, [&] {
+    Ctx& c = a->ctx->c;
+    const DCsr& A = *a->a;
+    if (rp) RDG_CUDA(cudaMemcpyAsync(rp, A.rp.p, sizeof(int) * (A.rows + 1), cudaMemcpyDefault, c.stream));
+    if (ci && A.nnz) RDG_CUDA(cudaMemcpyAsync(ci, A.ci.p, sizeof(int) * A.nnz, cudaMemcpyDefault, c.stream));
+    if (v && A.nnz) RDG_CUDA(cudaMemcpyAsync(v, A.v.p, sizeof(double) * A.nnz, cudaMemcpyDefault, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+// ------------------------------------------------------------ kernels
+int rd_gpu_spmv(rd_ctx* ctx, const rd_csr* a, const double* x, double* y) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    const DCsr& A = *a->a;
+    DBuf<double> tx;
+    const double* xd = in_dev(c, x, A.cols, tx);
+    OutVec<double> yo(c, y, A.rows);
+    spmv(c, A, xd, yo.dev());
+    yo.finish();
+    if (yo.host) RDG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int rd_gpu_dot(rd_ctx* ctx, int n, const double* a, const double* b, double* out) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    DBuf<double> ta, tb, r(1, c.stream);
+    const double* ad = in_dev(c, a, n, ta);
+    const double* bd = in_dev(c, b, n, tb);
+    dot(c, n, ad, bd, r.p);
+    RDG_CUDA(cudaMemcpyAsync(out, r.p, sizeof(double), cudaMemcpyDefault, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int rd_gpu_coarsen_redblack(rd_ctx* ctx, const rd_csr* a, uint8_t* flags, rd_csr** p_out) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    auto P = std::make_unique<rd_csr>();
+    P->ctx = ctx;
+    P->owned = std::make_unique<DCsr>();
+    DBuf<uint8_t> fl;
+    const std::vector<uint8_t> h = coarsen(c, *a->a, fl, *P->owned);
+    if (flags && !h.empty()) std::memcpy(flags, h.data(), h.size());
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    P->a = P->owned.get();
+    *p_out = P.release();
+  });
+}
+
+int rd_gpu_galerkin_coarse(rd_ctx* ctx, const rd_csr* a, const rd_csr* p, rd_csr** out) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    require(a->a->cols == p->a->rows, "galerkin_coarse: dims");
+    auto R = std::make_unique<rd_csr>();
+    R->ctx = ctx;
+    DCsr Pt = transpose(c, *p->a);
+    R->owned = std::make_unique<DCsr>(galerkin(c, *a->a, *p->a, Pt));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    R->a = R->owned.get();
+    *out = R.release();
+  });
+}
+
+int rd_gpu_sgs_sweep(rd_ctx* ctx, const rd_csr* a, const double* f, const double* u, double* out) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    DCsr& A = *a->a;
+    require(A.rows == A.cols, "sgs_sweep: matrix must be square");
+    const int n = A.rows;
+    if (!A.lat.ok) detect_lattice(c, A);
+    DBuf<double> tf, tu, t(std::max(n, 1), c.stream);
+    const double* fd = in_dev(c, f, n, tf);
+    const double* ud = in_dev(c, u, n, tu);
+    OutVec<double> o(c, out, n);
+    gs_pass(c, A, fd, ud, t.p, true);
+    gs_pass(c, A, fd, t.p, o.dev(), false);
+    o.finish();
+    sync_and_raise(c);
+  });
+}
+
+// ------------------------------------------------------------ AMG
+int rd_gpu_amg_setup(rd_ctx* ctx, const rd_csr* a, int thr, int m, rd_amg** out) {
+  return guard(ctx, [&] {
+    require(a && out, "build_amg: null argument");
+    require(a->a->rows == a->a->cols, "build_amg: matrix must be square");
+    require(m >= 0, "build_amg: smoothing_steps must be >= 0");
+    auto h = std::make_unique<rd_amg>();
+    h->ctx = ctx;
+    build_hierarchy(ctx->c, *a->a, thr, m, h->h);
+    const size_t L = h->h.levels.size();
+    h->views.resize(3 * L);
+    for (size_t l = 0; l < L; ++l) {
+      Level& lv = h->h.levels[l];
+      DCsr* mats[3] = {&lv.A, lv.has_p ? &lv.P : nullptr, lv.has_p ? &lv.Pt : nullptr};
+      for (int w = 0; w < 3; ++w) {
+        h->views[3 * l + w].ctx = ctx;
+        h->views[3 * l + w].a = mats[w];
+      }
+    }
+    RDG_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    *out = h.release();
+  });
+}
+
+void rd_gpu_amg_free(rd_amg* h) {
+  if (!h) return;
+  cudaStreamSynchronize(h->ctx->c.stream);
+  delete h;
+}
+
+int rd_gpu_amg_num_levels(const rd_amg* h) { return h ? (int)h->h.levels.size() : -1; }
+
+const rd_csr* rd_gpu_amg_level_matrix(const rd_amg* h, int level, int which) {
+  if (!h || level < 0 || level >= (int)h->h.levels.size() || which < 0 || which > 2) return nullptr;
+  const rd_csr* v = &h->views[3 * level + which];
+  return v->a ? v : nullptr;
+}
+
+int rd_gpu_amg_level_flags(const rd_amg* h, int level, uint8_t* flags) {
+  return guard(h->ctx, [&] {
+    require(level >= 0 && level < (int)h->h.levels.size(), "amg_level_flags: bad level");
+    const Level& lv = h->h.levels[level];
+    require(lv.has_p, "amg_level_flags: the coarsest level has no splitting");
+    RDG_CUDA(cudaMemcpyAsync(flags, lv.flags.p, lv.A.rows, cudaMemcpyDefault, h->ctx->c.stream));
+    RDG_CUDA(cudaStreamSynchronize(h->ctx->c.stream));
+  });
+}
+
+int rd_gpu_amg_level_structured(const rd_amg* h, int level) {
+  if (!h || level < 0 || level >= (int)h->h.levels.size()) return -1;
+  return h->h.levels[level].A.lat.ok ? 1 : 0;
+}
+
+int rd_gpu_amg_apply(rd_amg* h, const double* r, double* z) {
+  return guard(h->ctx, [&] {
+    Ctx& c = h->ctx->c;
+    const int n = h->h.levels.empty() ? 0 : h->h.levels[0].A.rows;
+    if (n == 0) return;
+    DBuf<double> tr;
+    const double* rd = in_dev(c, r, n, tr);
+    OutVec<double> zo(c, z, n);
+    vcycle(c, h->h, rd, zo.dev(), nullptr);
+    zo.finish();
+    if (zo.host || tr.p) sync_and_raise(c);
+  });
+}
+
+// ------------------------------------------------------------ PCG / solve_system
+int rd_gpu_pcg(rd_ctx* ctx, const rd_csr* a, rd_amg* amg, const double* f, double tol, int max_iter, double* x,
+               rd_pcg_report* rep, double* hist) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    const DCsr& A = *a->a;
+    require(A.rows == A.cols, "pcg: matrix must be square");
+    if (amg) require(!amg->h.levels.empty() && amg->h.levels[0].A.rows == A.rows, "amg_apply: dimension mismatch");
+    const int n = A.rows;
+    DBuf<double> tf, hd(std::max(max_iter, 1), c.stream);
+    const double* fd = in_dev(c, f, n, tf);
+    OutVec<double> xo(c, x, n);
+    const PcgResultDev r = pcg_device(c, A, amg ? &amg->h : nullptr, fd, tol, max_iter, xo.dev(), hd.p);
+    xo.finish();
+    if (hist && r.iterations > 0)
+      RDG_CUDA(cudaMemcpyAsync(hist, hd.p, sizeof(double) * r.iterations, cudaMemcpyDefault, c.stream));
+    sync_and_raise(c);
+    if (rep) {
+      rep->iterations = r.iterations;
+      rep->converged = r.converged ? 1 : 0;
+    }
+  });
+}
+
+int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, double tol, double* u,
+                            rd_solve_outcome* out) {
+  return guard(ctx, [&] {
+    using clk = std::chrono::steady_clock;
+    Ctx& c = ctx->c;
+    const DCsr& A = *a->a;
+    const int n = A.rows;
+    *out = rd_solve_outcome{0, 0, 0.0, 0.0};
+    if (n == 0) {  // bench.cpp:187-191
+      out->converged = 1;
+      return;
+    }
+    DBuf<double> tf;
+    const double* fd = in_dev(c, f, n, tf);
+    OutVec<double> uo(c, u, n);
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    const auto t0 = clk::now();
+    Hierarchy h;
+    build_hierarchy(c, A, 64, 1, h);
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    const auto t1 = clk::now();
+    const PcgResultDev r = pcg_device(c, A, &h, fd, tol, 500, uo.dev(), nullptr);
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    const auto t2 = clk::now();
+    uo.finish();
+    sync_and_raise(c);
+    out->iterations = r.iterations;
+    out->converged = r.converged ? 1 : 0;
+    out->setup_seconds = std::chrono::duration<double>(t1 - t0).count();
+    out->solve_seconds = std::chrono::duration<double>(t2 - t1).count();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// internal.hpp -- device-side objects behind the opaque C-ABI handles and the
+// host-callable entry points shared between translation units.
+#pragma once
+
+#include <memory>
+
+#include "common.cuh"
+
+namespace rdg {
+
+// ---------------------------------------------------------------- CSR on device
+// Layout in HBM: row_ptr int32[rows+1], col int32[nnz], val fp64[nnz]
+// (Eigen RowMajor<int> storage contract, types.hpp:14).  `lat` records the
+// lattice box when the pattern was verified to be a monotone box stencil
+// (SURVEY.md Appendix A); the structured smoother keys off it.
+struct Lattice {
+  int lx = 0, ly = 0, lz = 0;  // box sides; lx*ly*lz == rows
+  bool ok = false;
+};
+
+struct DCsr {
+  int rows = 0, cols = 0;
+  int64_t nnz = 0;
+  DBuf<int> rp, ci;
+  DBuf<double> v;
+  Lattice lat;
+  // generic (sync-free) Gauss-Seidel readiness flags, epoch-stamped so they
+  // never need clearing between sweeps
+  mutable DBuf<unsigned> gs_flags;
+  mutable unsigned gs_epoch = 0;
+};
+
+// ---------------------------------------------------------------- scan
+// Exclusive prefix sum of n int32 counts into int32 offsets[n+1]; returns the
+// total (throws RD_EINVAL if it exceeds INT32_MAX, the reference's index type).
+int64_t exclusive_scan(Ctx& c, const int* counts, int* offsets, int64_t n);
+
+// ---------------------------------------------------------------- linalg.cu
+void spmv(Ctx& c, const DCsr& A, const double* x, double* y);
+// y = A x and *dot_out = p . y (deterministic), both on device
+void spmv_dot(Ctx& c, const DCsr& A, const double* x, double* y, double* dot_out);
+// res = r - A z
+void residual(Ctx& c, const DCsr& A, const double* r, const double* z, double* res);
+// z += P zc
+void prolong_add(Ctx& c, const DCsr& P, const double* zc, double* z);
+void dot(Ctx& c, int64_t n, const double* a, const double* b, double* out_dev);
+DCsr transpose(Ctx& c, const DCsr& A);
+DCsr spgemm(Ctx& c, const DCsr& A, const DCsr& B);  // Eigen conservative product order
+DCsr prune_zeros(Ctx& c, const DCsr& A);
+DCsr csr_copy(Ctx& c, const DCsr& A);
+bool pattern_symmetric(Ctx& c, const DCsr& A);
+// detect a monotone (15-point Kuhn or sub-) stencil on a box; fills A.lat
+void detect_lattice(Ctx& c, DCsr& A);
+
+// ---------------------------------------------------------------- smoother.cu
+// one forward (fwd=true) or backward Gauss-Seidel pass: xout from xin (xin may be
+// nullptr = zero vector).  Optionally accumulates dot(r, xout) into dot_out.
+void gs_pass(Ctx& c, const DCsr& A, const double* f, const double* xin, double* xout, bool fwd,
+             double* dot_out = nullptr, const double* dot_with = nullptr);
+
+// ---------------------------------------------------------------- amg.cu
+struct Level {
+  DCsr A, P, Pt;
+  DBuf<uint8_t> flags;
+  bool has_p = false;
+  // work vectors
+  DBuf<double> r, z, t, res;
+};
+
+struct Hierarchy {
+  std::vector<Level> levels;
+  int smoothing_steps = 1;
+  int nc = 0;              // coarsest dimension
+  DBuf<double> Lc;         // coarsest LLT factor (row-major, lower)
+};
+
+std::vector<uint8_t> coarsen(Ctx& c, const DCsr& A, DBuf<uint8_t>& flags_dev, DCsr& P);
+DCsr galerkin(Ctx& c, const DCsr& A, const DCsr& P, const DCsr& Pt);
+void build_hierarchy(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h);
+// z = V(r) on device; if dot_out, also writes r.z (deterministic)
+void vcycle(Ctx& c, Hierarchy& h, const double* r, double* z, double* dot_out);
+void dense_llt(Ctx& c, const DCsr& A, DBuf<double>& L);  // throws RD_ENOTSPD
+
+// ---------------------------------------------------------------- pcg.cu
+struct PcgResultDev {
+  int iterations = 0;
+  bool converged = false;
+};
+// x (device, n) receives the solution; hist_dev (device, >= max_iter) may be null.
+PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, double tol, int max_iter, double* x,
+                        double* hist_dev);
+
+// ---------------------------------------------------------------- assembly.cu
+struct DMesh {
+  int nv = 0, nt = 0, lattice_n = -1;
+  DBuf<double> xyz;
+  DBuf<int> tets;
+  DBuf<uint8_t> boundary;
+};
+
+struct DSystem {
+  double rho = 1.0;
+  DCsr K, M, A;
+  DBuf<double> f;
+  DBuf<int> v2d, d2v;
+  int n_dofs = 0;
+  int nv = 0;
+};
+
+void build_structured_cube(Ctx& c, int n, DMesh& m);
+void build_system(Ctx& c, const DMesh& m, double rho, int target_kind, uint64_t seed, DSystem& s);
+
+}  // namespace rdg
+
+// opaque handles
+struct rd_ctx {
+  rdg::Ctx c;
+};
+struct rd_csr {
+  rd_ctx* ctx = nullptr;
+  std::unique_ptr<rdg::DCsr> owned;  // null for borrowed views
+  rdg::DCsr* a = nullptr;
+};
+struct rd_mesh {
+  rd_ctx* ctx = nullptr;
+  rdg::DMesh m;
+};
+struct rd_system {
+  rd_ctx* ctx = nullptr;
+  rdg::DSystem s;
+  rd_csr views[3];
+};
+struct rd_amg {
+  rd_ctx* ctx = nullptr;
+  rdg::Hierarchy h;
+  std::vector<rd_csr> views;  // 3 per level
+};

@@ -1,0 +1,102 @@
+// smoother.cu -- exact lexicographic Gauss-Seidel passes (amg.cpp:67-88) on sm_100a.
+//
+// The reference relaxes rows strictly in order i = 0..n-1 (forward) and then
+// n-1..0 (backward); row i reads new values for already-visited columns and
+// old values for the rest, summing s = f_i - sum_k a_ik x_k in column order
+// and dividing by the diagonal last.  Both kernels here reproduce that
+// arithmetic bit for bit: same operands, same order, IEEE division, no FMA.
+//
+//  * gs_syncfree_kernel (generic CSR): one thread per row, blocks take rows in
+//    ticket order; a row spins on epoch-stamped readiness flags of its
+//    already-visited neighbours (acquire/release at gpu scope).  Correct for
+//    any matrix, latency bound by the dependency depth.
+//  * the structured lattice kernel (smoother_lattice.cu) handles matrices whose
+//    pattern was verified to be the 15-point Kuhn stencil on a box.
+#include "internal.hpp"
+
+namespace rdg {
+
+void gs_pass_lattice(Ctx& c, const DCsr& A, const double* f, const double* xin, double* xout, bool fwd,
+                     double* dot_out, const double* dot_with);
+void gs_pass_generic(Ctx& c, const DCsr& A, const double* f, const double* xin, double* xout, bool fwd,
+                     double* dot_out, const double* dot_with);
+
+namespace {
+
+constexpr int kGsNT = 128;
+
+__global__ void __launch_bounds__(kGsNT) gs_syncfree_kernel(int n, const int* __restrict__ rp,
+                                                            const int* __restrict__ ci,
+                                                            const double* __restrict__ val,
+                                                            const double* __restrict__ f,
+                                                            const double* __restrict__ xin, double* xout,
+                                                            unsigned* flags, unsigned epoch, int* ticket,
+                                                            int* err, int fwd) {
+  __shared__ int blk;
+  if (threadIdx.x == 0) blk = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int t = blk * kGsNT + threadIdx.x;
+  if (t >= n) return;
+  const int i = fwd ? t : n - 1 - t;
+  double s = f[i];
+  double d = 0.0;
+  const int e = rp[i + 1];
+  for (int k = rp[i]; k < e; ++k) {
+    const int j = ci[k];
+    const double a = val[k];
+    if (j == i) {
+      d = a;
+      continue;
+    }
+    double xj;
+    if (fwd ? (j < i) : (j > i)) {
+      while (ld_acquire_u32(flags + j) != epoch) {
+      }
+      xj = ld_relaxed_f64(xout + j);
+    } else {
+      xj = xin ? __ldg(xin + j) : 0.0;
+    }
+    s = __dsub_rn(s, __dmul_rn(a, xj));
+  }
+  if (d == 0.0) atomicCAS(err, 0, RD_EZERODIAG);
+  xout[i] = __ddiv_rn(s, d);
+  st_release_u32(flags + i, epoch);
+}
+
+}  // namespace
+
+void gs_pass(Ctx& c, const DCsr& A, const double* f, const double* xin, double* xout, bool fwd, double* dot_out,
+             const double* dot_with) {
+  if (A.rows == 0) {
+    if (dot_out) RDG_CUDA(cudaMemsetAsync(dot_out, 0, sizeof(double), c.stream));
+    return;
+  }
+  if (A.lat.ok)
+    gs_pass_lattice(c, A, f, xin, xout, fwd, dot_out, dot_with);
+  else
+    gs_pass_generic(c, A, f, xin, xout, fwd, dot_out, dot_with);
+}
+
+void gs_pass_generic(Ctx& c, const DCsr& A, const double* f, const double* xin, double* xout, bool fwd,
+                     double* dot_out, const double* dot_with) {
+  const int n = A.rows;
+  if (!A.gs_flags.p) {
+    A.gs_flags.alloc(n, c.stream);
+    RDG_CUDA(cudaMemsetAsync(A.gs_flags.p, 0, sizeof(unsigned) * n, c.stream));
+    A.gs_epoch = 0;
+  }
+  if (++A.gs_epoch == 0) {  // wrapped: clear and restart at 1
+    RDG_CUDA(cudaMemsetAsync(A.gs_flags.p, 0, sizeof(unsigned) * n, c.stream));
+    A.gs_epoch = 1;
+  }
+  int* ticket = reinterpret_cast<int*>(c.d_counter + 32);
+  RDG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), c.stream));
+  gs_syncfree_kernel<<<div_up(n, kGsNT), kGsNT, 0, c.stream>>>(n, A.rp.p, A.ci.p, A.v.p, f, xin, xout,
+                                                               A.gs_flags.p, A.gs_epoch, ticket, c.d_err,
+                                                               fwd ? 1 : 0);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+  if (dot_out) dot(c, n, dot_with, xout, dot_out);
+}
+
+}  // namespace rdg

@@ -1,0 +1,494 @@
+"""Host-side mirror of the reference rd:: API over the rd_gpu C-ABI (include/rd_gpu.h).
+
+Names, argument meaning and error behaviour follow the reference library
+(/root/reference/proj/include/rd/*.hpp); every call runs the sm_100a kernels in
+``_build/librd_gpu.so``.  There is no CPU fallback: importing this module on a
+machine without the built library raises, and every compute call without a
+CUDA device raises :class:`RdCudaError`.
+
+Error mapping: RD_EINVAL -> ValueError (std::invalid_argument),
+RD_ENOTSPD / RD_EZERODIAG / RD_EDEGENERATE -> RuntimeError subclasses
+(std::runtime_error), CUDA failures -> RdCudaError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_build", "librd_gpu.so")
+
+RD_OK, RD_EINVAL, RD_ERUNTIME, RD_ENOTSPD, RD_EZERODIAG, RD_ECUDA, RD_ENCCL, RD_EDEGENERATE = range(8)
+
+TARGETS = {"smooth": 0, "box": 1, "nonzero_bc": 2, "ball": 3, "sine_random": 4, "zero": 5, "one": 6,
+           "quadratic": 7}
+
+
+class RdError(RuntimeError):
+    pass
+
+
+class RdInvalidArgument(RdError, ValueError):
+    pass
+
+
+class RdNotSpdError(RdError):
+    pass
+
+
+class RdZeroDiagonalError(RdError):
+    pass
+
+
+class RdDegenerateTetError(RdError):
+    pass
+
+
+class RdCudaError(RdError):
+    pass
+
+
+_EXC = {RD_EINVAL: RdInvalidArgument, RD_ENOTSPD: RdNotSpdError, RD_EZERODIAG: RdZeroDiagonalError,
+        RD_EDEGENERATE: RdDegenerateTetError, RD_ECUDA: RdCudaError}
+
+_P = C.c_void_p
+_I = C.c_int
+_D = C.c_double
+_lib = None
+
+
+def library_path() -> str:
+    return LIB_PATH
+
+
+def lib():
+    """Load librd_gpu.so; raise if it was not built (no silent fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"rd_gpu CUDA library missing at {LIB_PATH}: run __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    sig = {
+        "rd_gpu_version": (C.c_char_p, []),
+        "rd_gpu_ctx_create": (_I, [_I, _P, C.POINTER(_P)]),
+        "rd_gpu_ctx_destroy": (None, [_P]),
+        "rd_gpu_last_error": (C.c_char_p, [_P]),
+        "rd_gpu_ctx_stream": (_P, [_P]),
+        "rd_gpu_synchronize": (_I, [_P]),
+        "rd_gpu_launch_count": (C.c_int64, [_P]),
+        "rd_gpu_copy": (_I, [_P, _P, _P, C.c_size_t]),
+        "rd_gpu_build_structured_cube": (_I, [_P, _I, C.POINTER(_P)]),
+        "rd_gpu_mesh_create": (_I, [_P, _I, _P, _I, _P, _P, C.POINTER(_P)]),
+        "rd_gpu_mesh_free": (None, [_P]),
+        "rd_gpu_mesh_info": (_I, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
+        "rd_gpu_mesh_download": (_I, [_P, _P, _P, _P]),
+        "rd_gpu_build_system": (_I, [_P, _P, _D, _P, C.POINTER(_P)]),
+        "rd_gpu_system_free": (None, [_P]),
+        "rd_gpu_system_n_dofs": (_I, [_P]),
+        "rd_gpu_system_matrix": (_P, [_P, _I]),
+        "rd_gpu_system_load": (_P, [_P]),
+        "rd_gpu_system_dofmap": (_I, [_P, _P, _P]),
+        "rd_gpu_csr_create": (_I, [_P, _I, _I, C.c_int64, _P, _P, _P, C.POINTER(_P)]),
+        "rd_gpu_csr_free": (None, [_P]),
+        "rd_gpu_csr_info": (_I, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(C.c_int64)]),
+        "rd_gpu_csr_download": (_I, [_P, _P, _P, _P]),
+        "rd_gpu_spmv": (_I, [_P, _P, _P, _P]),
+        "rd_gpu_dot": (_I, [_P, _I, _P, _P, _P]),
+        "rd_gpu_coarsen_redblack": (_I, [_P, _P, _P, C.POINTER(_P)]),
+        "rd_gpu_galerkin_coarse": (_I, [_P, _P, _P, C.POINTER(_P)]),
+        "rd_gpu_sgs_sweep": (_I, [_P, _P, _P, _P, _P]),
+        "rd_gpu_amg_setup": (_I, [_P, _P, _I, _I, C.POINTER(_P)]),
+        "rd_gpu_amg_free": (None, [_P]),
+        "rd_gpu_amg_num_levels": (_I, [_P]),
+        "rd_gpu_amg_level_matrix": (_P, [_P, _I, _I]),
+        "rd_gpu_amg_level_flags": (_I, [_P, _I, _P]),
+        "rd_gpu_amg_level_structured": (_I, [_P, _I]),
+        "rd_gpu_amg_apply": (_I, [_P, _P, _P]),
+        "rd_gpu_pcg": (_I, [_P, _P, _P, _P, _D, _I, _P, _P, _P]),
+        "rd_gpu_solve_system_amg": (_I, [_P, _P, _P, _D, _P, _P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+class _PcgReport(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int)]
+
+
+class _SolveOutcome(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("setup_seconds", C.c_double),
+                ("solve_seconds", C.c_double)]
+
+
+class _Target(C.Structure):
+    _fields_ = [("kind", C.c_int), ("seed", C.c_uint64)]
+
+
+def _ptr(x):
+    """Raw pointer of a numpy array (host), a torch tensor (data_ptr) or an int."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return C.c_void_p(x.ctypes.data)
+    if hasattr(x, "data_ptr"):
+        return C.c_void_p(x.data_ptr())
+    if isinstance(x, int):
+        return C.c_void_p(x)
+    raise TypeError(f"unsupported buffer type {type(x)!r}")
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """rd_ctx: one device, one stream."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        h = _P()
+        rc = lib().rd_gpu_ctx_create(int(device), C.c_void_p(stream) if stream else None, C.byref(h))
+        if rc != RD_OK:
+            raise _EXC.get(rc, RdError)(lib().rd_gpu_last_error(None).decode())
+        self.h = h
+        self.device = device
+
+    def check(self, rc):
+        if rc != RD_OK:
+            raise _EXC.get(rc, RdError)(lib().rd_gpu_last_error(self.h).decode())
+
+    @property
+    def stream(self) -> int:
+        return lib().rd_gpu_ctx_stream(self.h) or 0
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().rd_gpu_launch_count(self.h))
+
+    def synchronize(self):
+        self.check(lib().rd_gpu_synchronize(self.h))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().rd_gpu_ctx_destroy(self.h)
+            self.h = None
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# ------------------------------------------------------------------ CSR
+class Csr:
+    """SpMat (types.hpp:14): int32 row_ptr/col_idx, fp64 values, resident in HBM."""
+
+    def __init__(self, h, ctx: Context, owner=None, owned=True):
+        self.h = h
+        self.ctx = ctx
+        self._owner = owner  # keeps a borrowed view's parent alive
+        self._owned = owned
+        r, c, z = _I(), _I(), C.c_int64()
+        lib().rd_gpu_csr_info(h, C.byref(r), C.byref(c), C.byref(z))
+        self.rows, self.cols, self.nnz = r.value, c.value, z.value
+
+    @staticmethod
+    def from_arrays(rows, cols, rp, ci, v, ctx: Context | None = None) -> "Csr":
+        ctx = ctx or default_context()
+        rp = np.ascontiguousarray(rp, np.int32)
+        ci = np.ascontiguousarray(ci, np.int32)
+        v = np.ascontiguousarray(v, np.float64)
+        h = _P()
+        ctx.check(lib().rd_gpu_csr_create(ctx.h, int(rows), int(cols), int(ci.size), _ptr(rp),
+                                          _ptr(ci) if ci.size else None, _ptr(v) if v.size else None, C.byref(h)))
+        return Csr(h, ctx)
+
+    @staticmethod
+    def from_scipy_like(A, ctx: Context | None = None) -> "Csr":
+        return Csr.from_arrays(A.rows, A.cols, A.rp, A.ci, A.v, ctx)
+
+    def download(self):
+        rp = np.zeros(self.rows + 1, np.int32)
+        ci = np.zeros(max(self.nnz, 1), np.int32)
+        v = np.zeros(max(self.nnz, 1), np.float64)
+        self.ctx.check(lib().rd_gpu_csr_download(self.h, _ptr(rp), _ptr(ci), _ptr(v)))
+        return rp, ci[: self.nnz], v[: self.nnz]
+
+    def dense(self):
+        rp, ci, v = self.download()
+        D = np.zeros((self.rows, self.cols))
+        for r in range(self.rows):
+            D[r, ci[rp[r]:rp[r + 1]]] = v[rp[r]:rp[r + 1]]
+        return D
+
+    def __del__(self):
+        if getattr(self, "h", None) and self._owned:
+            lib().rd_gpu_csr_free(self.h)
+        self.h = None
+
+
+def from_triplets(rows, cols, trips, ctx: Context | None = None) -> Csr:
+    """linalg.cpp:11-17 semantics (duplicates summed in insertion order, zeros pruned), staged on
+    the host only to build the input matrix of a test; every compute call then runs on the device."""
+    acc: dict = {}
+    order = []
+    for (i, j, val) in trips:
+        if not (0 <= i < rows and 0 <= j < cols):
+            raise ValueError("from_triplets: index out of range")
+        if (i, j) not in acc:
+            acc[(i, j)] = val
+            order.append((i, j))
+        else:
+            acc[(i, j)] = acc[(i, j)] + val
+    keys = sorted(k for k in order if acc[k] != 0.0)
+    rp = np.zeros(rows + 1, np.int32)
+    for (i, _) in keys:
+        rp[i + 1] += 1
+    rp = np.cumsum(rp).astype(np.int32)
+    ci = np.array([k[1] for k in keys], np.int32)
+    v = np.array([acc[k] for k in keys], np.float64)
+    return Csr.from_arrays(rows, cols, rp, ci, v, ctx)
+
+
+# ------------------------------------------------------------------ mesh / system
+class TetMesh:
+    """mesh.hpp:13-24, resident in HBM."""
+
+    def __init__(self, h, ctx: Context):
+        self.h = h
+        self.ctx = ctx
+        nv, nt, ln = _I(), _I(), _I()
+        lib().rd_gpu_mesh_info(h, C.byref(nv), C.byref(nt), C.byref(ln))
+        self.n_vertices, self.n_tets, self.lattice_n = nv.value, nt.value, ln.value
+
+    def download(self):
+        xyz = np.zeros((max(self.n_vertices, 1), 3))
+        tets = np.zeros((max(self.n_tets, 1), 4), np.int32)
+        b = np.zeros(max(self.n_vertices, 1), np.uint8)
+        self.ctx.check(lib().rd_gpu_mesh_download(self.h, _ptr(xyz), _ptr(tets), _ptr(b)))
+        return xyz[: self.n_vertices], tets[: self.n_tets], b[: self.n_vertices]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().rd_gpu_mesh_free(self.h)
+            self.h = None
+
+
+def build_structured_cube(n: int, ctx: Context | None = None) -> TetMesh:
+    """mesh.hpp:36 / mesh.cpp:29-65 on the device."""
+    ctx = ctx or default_context()
+    h = _P()
+    ctx.check(lib().rd_gpu_build_structured_cube(ctx.h, int(n), C.byref(h)))
+    return TetMesh(h, ctx)
+
+
+def mesh_from_arrays(xyz, tets, boundary, ctx: Context | None = None) -> TetMesh:
+    """Upload a host rd::TetMesh."""
+    ctx = ctx or default_context()
+    xyz = np.ascontiguousarray(xyz, np.float64)
+    tets = np.ascontiguousarray(tets, np.int32)
+    boundary = np.ascontiguousarray(boundary, np.uint8)
+    h = _P()
+    ctx.check(lib().rd_gpu_mesh_create(ctx.h, xyz.shape[0], _ptr(xyz), tets.shape[0], _ptr(tets), _ptr(boundary),
+                                       C.byref(h)))
+    return TetMesh(h, ctx)
+
+
+class FemSystem:
+    """assembly.hpp:24-31: K, M, A = rho*K + M, f and the dof map, resident in HBM."""
+
+    def __init__(self, h, ctx: Context, mesh: TetMesh, rho: float):
+        self.h = h
+        self.ctx = ctx
+        self.mesh = mesh
+        self.rho = rho
+        self.n_dofs = lib().rd_gpu_system_n_dofs(h)
+        self.K = Csr(lib().rd_gpu_system_matrix(h, 0), ctx, owner=self, owned=False)
+        self.M = Csr(lib().rd_gpu_system_matrix(h, 1), ctx, owner=self, owned=False)
+        self.A = Csr(lib().rd_gpu_system_matrix(h, 2), ctx, owner=self, owned=False)
+
+    @property
+    def f_ptr(self) -> int:
+        """Device pointer of the load vector."""
+        return lib().rd_gpu_system_load(self.h) or 0
+
+    def f(self) -> np.ndarray:
+        """Download the load vector."""
+        out = np.zeros(max(self.n_dofs, 1))
+        if self.n_dofs:
+            self.ctx.check(lib().rd_gpu_copy(self.ctx.h, _ptr(out), C.c_void_p(self.f_ptr), 8 * self.n_dofs))
+        return out[: self.n_dofs]
+
+    def dofmap(self):
+        v2d = np.zeros(max(self.mesh.n_vertices, 1), np.int32)
+        d2v = np.zeros(max(self.n_dofs, 1), np.int32)
+        self.ctx.check(lib().rd_gpu_system_dofmap(self.h, _ptr(v2d), _ptr(d2v)))
+        return v2d[: self.mesh.n_vertices], d2v[: self.n_dofs]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().rd_gpu_system_free(self.h)
+            self.h = None
+
+
+def build_system(mesh: TetMesh, rho: float, target: str = "smooth", seed: int = 0) -> FemSystem:
+    """assembly.hpp:48 / assembly.cpp:225-238 on the device."""
+    ctx = mesh.ctx
+    t = _Target(TARGETS[target], int(seed))
+    h = _P()
+    ctx.check(lib().rd_gpu_build_system(ctx.h, mesh.h, float(rho), C.byref(t), C.byref(h)))
+    return FemSystem(h, ctx, mesh, rho)
+
+
+# ------------------------------------------------------------------ kernels
+def spmv(A: Csr, x) -> np.ndarray:
+    """linalg.hpp:30 -- y = A x."""
+    x = np.ascontiguousarray(x, np.float64)
+    if x.size != A.cols:
+        raise RdInvalidArgument("spmv: dimension mismatch")
+    y = np.zeros(max(A.rows, 1))
+    A.ctx.check(lib().rd_gpu_spmv(A.ctx.h, A.h, _ptr(x), _ptr(y)))
+    return y[: A.rows]
+
+
+def dot(a, b, ctx: Context | None = None) -> float:
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    out = np.zeros(1)
+    ctx.check(lib().rd_gpu_dot(ctx.h, a.size, _ptr(a), _ptr(b), _ptr(out)))
+    return float(out[0])
+
+
+def coarsen_redblack(A: Csr):
+    """amg.hpp:29 -- (coarse flags, P)."""
+    flags = np.zeros(max(A.rows, 1), np.uint8)
+    h = _P()
+    A.ctx.check(lib().rd_gpu_coarsen_redblack(A.ctx.h, A.h, _ptr(flags), C.byref(h)))
+    return flags[: A.rows], Csr(h, A.ctx)
+
+
+def galerkin_coarse(A: Csr, P: Csr) -> Csr:
+    """amg.hpp:31 -- prune(P^T A P)."""
+    if A.cols != P.rows:
+        raise RdInvalidArgument("galerkin_coarse: dims")
+    h = _P()
+    A.ctx.check(lib().rd_gpu_galerkin_coarse(A.ctx.h, A.h, P.h, C.byref(h)))
+    return Csr(h, A.ctx)
+
+
+def sgs_sweep(A: Csr, f, u) -> np.ndarray:
+    """amg.hpp:34 -- one forward then one backward Gauss-Seidel pass."""
+    f = np.ascontiguousarray(f, np.float64)
+    u = np.ascontiguousarray(u, np.float64)
+    out = np.zeros(max(A.rows, 1))
+    A.ctx.check(lib().rd_gpu_sgs_sweep(A.ctx.h, A.h, _ptr(f), _ptr(u), _ptr(out)))
+    return out[: A.rows]
+
+
+class AmgHierarchy:
+    """amg.hpp:13-24 (levels of A, P, Pt, coarse flags; coarsest LLT) built on the device."""
+
+    def __init__(self, A: Csr, coarsest_threshold: int = 64, smoothing_steps: int = 1):
+        self.ctx = A.ctx
+        h = _P()
+        self.ctx.check(lib().rd_gpu_amg_setup(self.ctx.h, A.h, int(coarsest_threshold), int(smoothing_steps),
+                                              C.byref(h)))
+        self.h = h
+        self.n = A.rows
+
+    @property
+    def num_levels(self) -> int:
+        return lib().rd_gpu_amg_num_levels(self.h)
+
+    def level(self, l: int, which: str = "A") -> Csr | None:
+        p = lib().rd_gpu_amg_level_matrix(self.h, int(l), {"A": 0, "P": 1, "Pt": 2}[which])
+        return Csr(p, self.ctx, owner=self, owned=False) if p else None
+
+    def flags(self, l: int):
+        A = self.level(l)
+        f = np.zeros(max(A.rows, 1), np.uint8)
+        rc = lib().rd_gpu_amg_level_flags(self.h, int(l), _ptr(f))
+        if rc != RD_OK:
+            return None
+        return f[: A.rows]
+
+    def structured(self, l: int) -> bool:
+        return lib().rd_gpu_amg_level_structured(self.h, int(l)) == 1
+
+    def apply(self, r, z=None):
+        """amg.hpp:39 amg_apply: one V-cycle, zero initial guess.  Host arrays in -> host array out;
+        device buffers (torch tensors / pointers) are used in place and left stream-ordered."""
+        if isinstance(r, np.ndarray) or not hasattr(r, "data_ptr"):
+            r = np.ascontiguousarray(r, np.float64)
+            if r.size != self.n:
+                raise RdInvalidArgument("amg_apply: dimension mismatch")
+            out = np.zeros(max(self.n, 1))
+            self.ctx.check(lib().rd_gpu_amg_apply(self.h, _ptr(r), _ptr(out)))
+            return out[: self.n]
+        self.ctx.check(lib().rd_gpu_amg_apply(self.h, _ptr(r), _ptr(z)))
+        return z
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().rd_gpu_amg_free(self.h)
+            self.h = None
+
+
+def build_amg(A: Csr, coarsest_threshold: int = 64, smoothing_steps: int = 1) -> AmgHierarchy:
+    return AmgHierarchy(A, coarsest_threshold, smoothing_steps)
+
+
+@dataclass
+class PcgResult:
+    x: np.ndarray
+    iterations: int
+    converged: bool
+    residual_history: np.ndarray
+
+
+def pcg(A: Csr, precond="amg", f=None, tol: float = 1e-8, max_iter: int = 500,
+        hierarchy: AmgHierarchy | None = None) -> PcgResult:
+    """linalg.hpp:46-49 with amg_precond(h) (or the identity)."""
+    f = np.ascontiguousarray(f, np.float64)
+    if precond == "amg" and hierarchy is None:
+        hierarchy = build_amg(A)
+    if precond not in ("amg", "identity"):
+        raise RdInvalidArgument(f"unsupported preconditioner {precond!r} on the device path")
+    x = np.zeros(max(A.rows, 1))
+    hist = np.zeros(max(max_iter, 1))
+    rep = _PcgReport()
+    A.ctx.check(lib().rd_gpu_pcg(A.ctx.h, A.h, hierarchy.h if precond == "amg" else None, _ptr(f), float(tol),
+                                 int(max_iter), _ptr(x), C.byref(rep), _ptr(hist)))
+    return PcgResult(x[: A.rows], rep.iterations, bool(rep.converged), hist[: rep.iterations].copy())
+
+
+@dataclass
+class SolveOutcome:
+    u: np.ndarray
+    iterations: int
+    converged: bool
+    setup_seconds: float
+    solve_seconds: float
+
+
+def solve_system_amg(A: Csr, f, tol: float = 1e-8, u=None) -> SolveOutcome:
+    """bench.hpp:56 solve_system(mesh, sys, PrecondKind::amg, p, tol)."""
+    host = u is None
+    if host:
+        u = np.zeros(max(A.rows, 1))
+    if isinstance(f, np.ndarray):
+        f = np.ascontiguousarray(f, np.float64)
+    out = _SolveOutcome()
+    A.ctx.check(lib().rd_gpu_solve_system_amg(A.ctx.h, A.h, _ptr(f), float(tol), _ptr(u), C.byref(out)))
+    return SolveOutcome(u[: A.rows] if host else u, out.iterations, bool(out.converged), out.setup_seconds,
+                        out.solve_seconds)

@@ -1,0 +1,311 @@
+"""Device parity: every sm_100a kernel called through the C-ABI against the CPU oracle.
+
+Bars (BASELINE.json north star):
+  * mesh, dof map, CSR patterns, C/F splittings, P, Galerkin operators: bit-exact;
+  * fp64 values on integer/indicator paths (K, M, A, SpMV, GS sweeps, ball/box loads): bit-exact;
+  * loads of sin targets: CUDA sin vs glibc sin -> <= 4 ulp (tolerance 1e-15 relative);
+  * PCG: iteration counts equal, solutions within 1e-10 relative (dot products are
+    reduced in a different -- deterministic -- order than Eigen's SSE2 dot).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rd():
+    from paper_2102_03515_b200 import rd as _rd
+
+    _rd.default_context()
+    return _rd
+
+
+def assert_csr_equal(dev, ref, what=""):
+    rp, ci, v = dev.download()
+    assert dev.rows == ref.rows and dev.cols == ref.cols, what
+    assert np.array_equal(rp, ref.rp), f"{what}: row_ptr"
+    assert np.array_equal(ci, ref.ci), f"{what}: col_idx"
+    assert np.array_equal(v, ref.v), f"{what}: values differ (max {np.abs(v - ref.v).max() if v.size else 0})"
+
+
+def to_dev(rd, A):
+    return rd.Csr.from_arrays(A.rows, A.cols, A.rp, A.ci, A.v)
+
+
+# ------------------------------------------------------------------ mesh / assembly
+@pytest.mark.parametrize("n", [1, 2, 4, 7, 8])
+def test_mesh_bit_exact(rd, O, n):
+    dm = rd.build_structured_cube(n)
+    om = O.build_structured_cube(n)
+    xyz, tets, b = dm.download()
+    assert np.array_equal(xyz, om.xyz) and np.array_equal(tets, om.tets) and np.array_equal(b, om.boundary)
+
+
+def test_mesh_rejects_nonpositive(rd):
+    with pytest.raises(ValueError):
+        rd.build_structured_cube(0)
+
+
+@pytest.mark.parametrize("target", ["smooth", "ball", "box", "sine_random", "quadratic", "one", "zero", "nonzero_bc"])
+@pytest.mark.parametrize("n", [3, 8])
+def test_build_system_parity(rd, O, n, target):
+    rho = 1.0 / (n * n)
+    ds = rd.build_system(rd.build_structured_cube(n), rho, target)
+    os_ = O.build_system(O.build_structured_cube(n), rho, target)
+    assert_csr_equal(ds.K, os_.K, "K")
+    assert_csr_equal(ds.M, os_.M, "M")
+    assert_csr_equal(ds.A, os_.A, "A")
+    v2d, d2v = ds.dofmap()
+    assert np.array_equal(v2d, os_.vertex_to_dof) and np.array_equal(d2v, os_.dof_to_vertex)
+    f = ds.f()
+    if target in ("smooth", "sine_random", "nonzero_bc"):
+        # CUDA sin vs glibc sin: ulp-level only
+        assert np.abs(f - os_.f).max() <= 1e-15 * np.abs(os_.f).max() + 1e-300
+    else:
+        assert np.array_equal(f, os_.f), np.abs(f - os_.f).max()
+
+
+def test_build_system_c2_pattern_n32(rd, O):
+    ds = rd.build_system(rd.build_structured_cube(32), 2.0 ** -10, "ball")
+    os_ = O.build_system(O.build_structured_cube(32), 2.0 ** -10, "ball")
+    assert_csr_equal(ds.A, os_.A, "A")
+    assert np.array_equal(ds.f(), os_.f)
+
+
+def test_build_system_rejects_rho(rd):
+    with pytest.raises(ValueError):
+        rd.build_system(rd.build_structured_cube(2), 0.0, "smooth")
+
+
+def test_reference_tet_assembly(rd, O):  # test_assembly.cpp:41-62 on a hand-built mesh
+    xyz = [[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [2, 2, 2]]
+    tets = [[0, 1, 2, 3]]
+    bnd = [0, 0, 0, 0, 1]
+    ds = rd.build_system(rd.mesh_from_arrays(xyz, tets, bnd), 1.0, "one")
+    K = ds.K.dense()
+    assert K[0, 0] == pytest.approx(0.5, rel=1e-14) and K[1, 1] == pytest.approx(1 / 6, rel=1e-14)
+    M = ds.M.dense()
+    assert M[0, 0] == pytest.approx(1 / 60, rel=1e-14) and M[0, 1] == pytest.approx(1 / 120, rel=1e-14)
+
+
+# ------------------------------------------------------------------ SpMV
+@pytest.mark.parametrize("n", [4, 16, 33])
+def test_spmv_bit_exact(rd, O, n):
+    os_ = O.build_system(O.build_structured_cube(n), 1e-3, "smooth")
+    A = to_dev(rd, os_.A)
+    x = O.pseudo_random_vec(A.rows, 7)
+    assert np.array_equal(rd.spmv(A, x), O.spmv(os_.A, x))
+
+
+def test_spmv_hand_cases(rd, O):  # test_linalg.cpp:47-71
+    I3 = rd.from_triplets(3, 3, [(0, 0, 1.0), (1, 1, 1.0), (2, 2, 1.0)])
+    x = np.array([3.0, -1.0, 2.0])
+    assert np.array_equal(rd.spmv(I3, x), x)
+    A = rd.from_triplets(2, 2, [(0, 0, 2.0), (0, 1, 1.0), (1, 0, 1.0), (1, 1, 2.0)])
+    assert list(rd.spmv(A, np.ones(2))) == [3.0, 3.0]
+    with pytest.raises(ValueError):
+        rd.spmv(A, np.ones(5))
+
+
+def test_spmv_irregular_rows(rd, O):  # rows longer than one staging chunk
+    rng = np.random.default_rng(0)
+    n = 300
+    trips = []
+    for i in range(n):
+        k = 1 + (i * 37) % 700 if i % 50 == 0 else 1 + i % 9
+        cols = rng.choice(n, size=min(k, n), replace=False)
+        trips += [(i, int(c), float(rng.standard_normal())) for c in cols]
+    Ao = O.from_triplets(n, n, trips)
+    A = to_dev(rd, Ao)
+    x = rng.standard_normal(n)
+    assert np.array_equal(rd.spmv(A, x), O.spmv(Ao, x))
+
+
+# ------------------------------------------------------------------ coarsening / Galerkin
+def test_coarsen_hand_cases(rd):  # test_amg.cpp:36-60
+    t = []
+    for i in range(5):
+        t.append((i, i, 2.0))
+        if i + 1 < 5:
+            t += [(i, i + 1, -1.0), (i + 1, i, -1.0)]
+    flags, P = rd.coarsen_redblack(rd.from_triplets(5, 5, t))
+    assert list(flags) == [1, 0, 1, 0, 1]
+    D = P.dense()
+    assert D[1, 0] == 0.5 and D[1, 1] == 0.5 and D[4, 2] == 1.0
+    flags, P = rd.coarsen_redblack(rd.from_triplets(3, 3, [(0, 0, 1.0), (1, 1, 2.0), (2, 2, 3.0)]))
+    assert list(flags) == [1, 1, 1] and np.array_equal(P.dense(), np.eye(3))
+
+
+@pytest.mark.parametrize("n", [4, 8, 16])
+def test_coarsen_galerkin_bit_exact(rd, O, n):
+    os_ = O.build_system(O.build_structured_cube(n), 1e-2, "smooth")
+    A = to_dev(rd, os_.A)
+    flags, P = rd.coarsen_redblack(A)
+    oflags, oP = O.coarsen_redblack(os_.A)
+    assert np.array_equal(flags, oflags)
+    assert_csr_equal(P, oP, "P")
+    assert_csr_equal(rd.galerkin_coarse(A, P), O.galerkin_coarse(os_.A, oP), "Ac")
+
+
+def test_galerkin_hand_case(rd):  # test_amg.cpp:83-99
+    A = rd.from_triplets(2, 2, [(0, 0, 2.0), (0, 1, -1.0), (1, 0, -1.0), (1, 1, 2.0)])
+    P = rd.from_triplets(2, 1, [(0, 0, 1.0), (1, 0, 0.5)])
+    assert rd.galerkin_coarse(A, P).dense()[0, 0] == pytest.approx(1.5, rel=1e-14)
+
+
+def test_coarsen_nonsymmetric_pattern(rd, O):
+    rng = np.random.default_rng(3)
+    n = 60
+    trips = [(i, i, 4.0) for i in range(n)]
+    for _ in range(150):
+        i, j = rng.integers(0, n, 2)
+        if i != j:
+            trips.append((int(i), int(j), -0.1))
+    Ao = O.from_triplets(n, n, trips)
+    flags, P = rd.coarsen_redblack(to_dev(rd, Ao))
+    of, oP = O.coarsen_redblack(Ao)
+    assert np.array_equal(flags, of)
+    assert_csr_equal(P, oP, "P")
+
+
+# ------------------------------------------------------------------ Gauss-Seidel
+def test_sgs_hand_cases(rd):  # test_amg.cpp:109-126
+    A = rd.from_triplets(2, 2, [(0, 0, 2.0), (0, 1, 1.0), (1, 0, 1.0), (1, 1, 2.0)])
+    u = rd.sgs_sweep(A, np.ones(2), np.zeros(2))
+    assert u[0] == pytest.approx(0.375, rel=1e-15) and u[1] == pytest.approx(0.25, rel=1e-15)
+    D = rd.from_triplets(2, 2, [(0, 0, 2.0), (1, 1, 4.0)])
+    u = rd.sgs_sweep(D, np.array([2.0, 2.0]), np.zeros(2))
+    assert u[0] == 1.0 and u[1] == 0.5
+
+
+def test_sgs_zero_diagonal_raises(rd):  # amg.cpp:82
+    A = rd.from_triplets(2, 2, [(0, 1, 1.0), (1, 0, 1.0), (1, 1, 2.0)])
+    with pytest.raises(rd.RdZeroDiagonalError):
+        rd.sgs_sweep(A, np.ones(2), np.zeros(2))
+
+
+@pytest.mark.parametrize("n", [3, 8, 17, 32])
+def test_sgs_bit_exact(rd, O, n):
+    os_ = O.build_system(O.build_structured_cube(n), 2.0 ** -8, "smooth")
+    A = to_dev(rd, os_.A)
+    f = O.pseudo_random_vec(A.rows, 1)
+    u = O.pseudo_random_vec(A.rows, 2)
+    assert np.array_equal(rd.sgs_sweep(A, f, u), O.sgs_sweep(os_.A, f, u))
+
+
+def test_sgs_random_sparse_bit_exact(rd, O):
+    rng = np.random.default_rng(5)
+    n = 500
+    trips = [(i, i, 10.0 + rng.random()) for i in range(n)]
+    for _ in range(3000):
+        i, j = rng.integers(0, n, 2)
+        if i != j:
+            trips.append((int(i), int(j), float(rng.standard_normal())))
+    Ao = O.from_triplets(n, n, trips)
+    f, u = rng.standard_normal(n), rng.standard_normal(n)
+    assert np.array_equal(rd.sgs_sweep(to_dev(rd, Ao), f, u), O.sgs_sweep(Ao, f, u))
+
+
+# ------------------------------------------------------------------ hierarchy / V-cycle
+@pytest.mark.parametrize("n,thr", [(4, 16), (6, 8), (16, 64), (32, 64)])
+def test_hierarchy_bit_exact(rd, O, n, thr):
+    os_ = O.build_system(O.build_structured_cube(n), 1.0 / (n * n), "ball")
+    oh = O.build_amg(os_.A, thr)
+    dh = rd.build_amg(to_dev(rd, os_.A), thr)
+    assert dh.num_levels == oh.num_levels
+    for l in range(oh.num_levels):
+        assert_csr_equal(dh.level(l), oh.level(l), f"A_{l}")
+        if l + 1 < oh.num_levels:
+            assert np.array_equal(dh.flags(l), oh.flags(l))
+            assert_csr_equal(dh.level(l, "P"), oh.level(l, "P"), f"P_{l}")
+            assert_csr_equal(dh.level(l, "Pt"), oh.level(l, "Pt"), f"Pt_{l}")
+
+
+@pytest.mark.parametrize("n,thr", [(3, 1000), (4, 16), (16, 64), (32, 64)])
+def test_amg_apply_bit_exact(rd, O, n, thr):
+    os_ = O.build_system(O.build_structured_cube(n), 1e-4, "smooth")
+    oh = O.build_amg(os_.A, thr)
+    dh = rd.build_amg(to_dev(rd, os_.A), thr)
+    r = O.pseudo_random_vec(os_.A.rows, 9)
+    assert np.array_equal(dh.apply(r), oh.apply(r))
+
+
+def test_vcycle_symmetric_positive(rd, O):  # test_amg.cpp:139-151
+    os_ = O.build_system(O.build_structured_cube(4), 1e-2, "smooth")
+    h = rd.build_amg(to_dev(rd, os_.A), 16)
+    for s in range(3):
+        r1, r2 = O.pseudo_random_vec(os_.A.rows, 10 + s), O.pseudo_random_vec(os_.A.rows, 20 + s)
+        assert r2 @ h.apply(r1) == pytest.approx(r1 @ h.apply(r2), rel=1e-11)
+
+
+def test_empty_hierarchy(rd):  # test_amg.cpp:204-210
+    A = rd.Csr.from_arrays(0, 0, np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0))
+    h = rd.build_amg(A)
+    assert h.num_levels == 1
+
+
+# ------------------------------------------------------------------ PCG / solve_system
+def test_pcg_hand_cases(rd, O):  # test_linalg.cpp:96-139
+    A1 = rd.from_triplets(1, 1, [(0, 0, 2.0)])
+    r = rd.pcg(A1, "identity", np.array([4.0]), 1e-12, 10)
+    assert r.converged and r.iterations == 1 and r.x[0] == pytest.approx(2.0, rel=1e-14)
+    t = []
+    for i in range(40):
+        t.append((i, i, 4.0 + 0.01 * i))
+        if i + 1 < 40:
+            t += [(i, i + 1, -1.0), (i + 1, i, -1.0)]
+        if i + 3 < 40:
+            t += [(i, i + 3, -0.5), (i + 3, i, -0.5)]
+    B = rd.from_triplets(40, 40, t)
+    r = rd.pcg(B, "identity", np.ones(40), 1e-14, 2)
+    assert not r.converged and r.iterations == 2
+    r = rd.pcg(B, "identity", np.zeros(40), 1e-10, 10)
+    assert r.converged and r.iterations == 0 and np.linalg.norm(r.x) == 0.0
+    with pytest.raises(rd.RdNotSpdError):
+        rd.pcg(rd.from_triplets(2, 2, [(0, 0, 1.0), (1, 1, -1.0)]), "identity", np.ones(2), 1e-10, 10)
+
+
+@pytest.mark.parametrize("n,rho,target", [(8, 1.0, "smooth"), (8, 1e-12, "smooth"), (16, 2.0 ** -8, "ball"),
+                                          (32, 2.0 ** -10, "smooth"), (32, 1e-2, "sine_random"),
+                                          (32, 2.0 ** -10, "box")])
+def test_solve_system_parity(rd, O, n, rho, target):
+    ds = rd.build_system(rd.build_structured_cube(n), rho, target)
+    os_ = O.build_system(O.build_structured_cube(n), rho, target)
+    out = rd.solve_system_amg(ds.A, ds.f(), 1e-8)
+    ref = O.solve_system_amg(os_, 1e-8)
+    assert out.converged and ref.converged
+    assert out.iterations == ref.iterations
+    assert np.abs(out.u - ref.u).max() <= 1e-10 * np.abs(ref.u).max()
+
+
+@pytest.mark.parametrize("rho", [1.0, 1e-2, 1e-4, 1e-6, 2.0 ** -12])
+def test_c3_rho_sweep_n64(rd, O, rho):  # BASELINE config 3 at full size
+    O.set_num_threads(8)
+    ds = rd.build_system(rd.build_structured_cube(64), rho, "sine_random")
+    os_ = O.build_system(O.build_structured_cube(64), rho, "sine_random")
+    assert_csr_equal(ds.A, os_.A, "A")
+    out = rd.solve_system_amg(ds.A, ds.f(), 1e-8)
+    ref = O.solve_system_amg(os_, 1e-8)
+    assert abs(out.iterations - ref.iterations) <= 0, (out.iterations, ref.iterations)
+    assert np.abs(out.u - ref.u).max() <= 1e-10 * np.abs(ref.u).max()
+
+
+def test_pcg_history_matches(rd, O):
+    os_ = O.build_system(O.build_structured_cube(16), 1e-3, "smooth")
+    A = to_dev(rd, os_.A)
+    r = rd.pcg(A, "amg", os_.f, 1e-10, 100)
+    ro = O.pcg(os_.A, "amg", os_.f, 1e-10, 100)
+    assert r.iterations == ro.iterations
+    assert np.allclose(r.residual_history, ro.residual_history, rtol=1e-9, atol=0)
+
+
+def test_degenerate_meshes(rd):  # test_bench.cpp:185-195: n=1 has no dofs
+    ds = rd.build_system(rd.build_structured_cube(1), 1.0, "smooth")
+    assert ds.n_dofs == 0
+    out = rd.solve_system_amg(ds.A, np.zeros(0), 1e-8)
+    assert out.converged and out.iterations == 0
+    ds = rd.build_system(rd.build_structured_cube(2), 1.0, "smooth")
+    assert ds.n_dofs == 1
+    out = rd.solve_system_amg(ds.A, ds.f(), 1e-8)
+    assert out.converged
