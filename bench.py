@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native AMG-PCG solve path (BASELINE.json configs[1] = C2).
+
+Workload (C2): unit cube, n = 128 cells per side (127^3 = 2,048,383 interior dofs,
+30.3M nnz), rho = h^2 = 2^-14, ball target (64-point rule), fp64 AMG-PCG to
+rtol 1e-8 from a zero initial guess.  Synthetic and seeded: the mesh is generated,
+not loaded.
+
+One *step* = one pass of the whole hot path over that input:
+    build_system (device assembly of rho*K + M and f)  ->  build_amg (device setup)
+    ->  pcg with the AMG V-cycle (device-resident).
+`value` = DOF * PCG iterations / step time (inputs resident in HBM: the device
+mesh is built before the timed region), aggregated over ranks.  `e2e` = the same
+metric through the C-ABI with HOST buffers: the pinned host TetMesh is uploaded
+(rd_gpu_mesh_create), assembled, solved, and u read back, every step.
+
+--impl reference times the CPU oracle port (oracle/, the reference cannot be built
+here: no Eigen) on the host cores for the same config and metric.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DEFAULT = 128
+RHO_EXP = -14  # rho = h^2 = 2^-14 at n = 128
+TARGET = "ball"
+TOL = 1e-8
+METRIC = "AMG-PCG DOF*iters/s (C2: n=128, 2.05M dofs, fp64, rho=h^2, rtol 1e-8)"
+UNIT = "DOF*iters/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=N_DEFAULT)
+    p.add_argument("--target", default=TARGET)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--profile", action="store_true", help="short run for ncu: 1 step, no extras")
+    return p.parse_args()
+
+
+def rho_for(n):
+    return 1.0 / (n * n)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_profile_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_2102_03515_b200 import rd
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ctx = rd.Context(local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    n = args.n
+    rho = rho_for(n)
+    mesh = rd.build_structured_cube(n, ctx)
+    ctx.synchronize()
+    u_dev = None
+
+    def step():
+        nonlocal u_dev
+        s = rd.build_system(mesh, rho, args.target)
+        if u_dev is None:
+            u_dev = torch.empty(s.n_dofs, dtype=torch.float64, device=dev)
+        out = rd.solve_system_amg(s.A, s.f_ptr, TOL, u=u_dev)
+        return s.n_dofs, out
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+
+    # ---------------- timed region: K steps, inputs resident in HBM
+    clocks = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    l0 = ctx.launch_count
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    its, ndofs, setup_s, solve_s = [], 0, [], []
+    for _ in range(args.steps):
+        ndofs, out = step()
+        its.append(out.iterations)
+        setup_s.append(out.setup_seconds)
+        solve_s.append(out.solve_seconds)
+        assert out.converged
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launch_count - l0
+    elapsed_ms = e0.elapsed_time(e1)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    work = torch.tensor([float(ndofs) * sum(its)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(work, op=torch.distributed.ReduceOp.SUM)
+    elapsed_ms = float(t.item())
+    value = float(work.item()) / (elapsed_ms / 1e3)
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated Kuhn lattice, ball target, seeded)",
+        "config": {"workload": f"C2: build_system + build_amg + pcg, n={n} ({ndofs} dofs), rho=2^{-2 * int(np.log2(n))}"
+                               f" (h^2), {args.target} target, rtol {TOL}",
+                   "n": n, "n_dofs": ndofs, "rho": rho, "target": args.target, "tol": TOL,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs exceed L2 (device mesh 255 MB, A 364 MB > 126 MB L2); no flush"},
+        "iterations": its[0],
+        "phases_ms": {"setup_host_clock": 1e3 * statistics.mean(setup_s), "pcg_host_clock": 1e3 * statistics.mean(solve_s)},
+        "pcg_dof_iters_per_s": float(ndofs) * statistics.mean(its) / statistics.mean(solve_s),
+        "clocks": clk,
+        "gpu_launches": launches,
+    }
+    if args.profile:
+        return result
+
+    # ---------------- dominant kernels, timed live with events on the library stream
+    s = rd.build_system(mesh, rho, args.target)
+    h = rd.build_amg(s.A)
+    N, Z = s.n_dofs, s.A.nnz
+    x = torch.rand(N, dtype=torch.float64, device=dev)
+    y = torch.empty(N, dtype=torch.float64, device=dev)
+    ctx.synchronize()
+    R = 20
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(R):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / R
+
+    gs_ms = timed(lambda: h.level_sweep(0, True, s.f_ptr, x, y))
+    spmv_ms = timed(lambda: rd.lib().rd_gpu_spmv(ctx.h, s.A.h, rd._ptr(x), rd._ptr(y)))
+    structured = h.structured(0)
+    gs_bytes = (8 * Z + 4 * (N + 1) + 24 * N) if structured else (12 * Z + 28 * N + 4)
+    spmv_bytes = 12 * Z + 20 * N + 4
+    peak, peak_kind = peaks()
+    traffic = load_profile_traffic()
+    gs_gbs = gs_bytes / (gs_ms * 1e-3) / 1e9
+    its0 = its[0]
+    # level-0 sweeps per step: 4 per V-cycle, V-cycles = iterations + 1
+    share = (4 * (its0 + 1) * gs_ms) / (elapsed_ms / args.steps)
+    result["roofline"] = {
+        "kernel": "gs_sweep level 0 (" + ("structured lattice kernel" if structured else "generic sync-free kernel") + ")",
+        "bound": "hbm", "achieved": gs_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+        "frac": gs_gbs / peak, "traffic": traffic.get("gs_sweep"),
+        "bytes_per_launch": gs_bytes, "launch_ms": gs_ms, "share_of_step_est": share,
+    }
+    result["kernels"] = {
+        "spmv": {"bytes_per_launch": spmv_bytes, "launch_ms": spmv_ms,
+                 "achieved_gbs": spmv_bytes / (spmv_ms * 1e-3) / 1e9,
+                 "frac": spmv_bytes / (spmv_ms * 1e-3) / 1e9 / peak, "traffic": traffic.get("spmv")},
+        "gs_sweep_level0": {"bytes_per_launch": gs_bytes, "launch_ms": gs_ms, "achieved_gbs": gs_gbs,
+                            "frac": gs_gbs / peak},
+        "levels": h.num_levels,
+        "structured_levels": [bool(h.structured(l)) for l in range(h.num_levels - 1)],
+    }
+    del h, s
+
+    # ---------------- e2e through the C-ABI with host buffers
+    if not args.no_e2e:
+        xyz, tets, bnd = mesh.download()
+        pxyz = torch.from_numpy(xyz).pin_memory()
+        ptets = torch.from_numpy(tets).pin_memory()
+        pbnd = torch.from_numpy(bnd).pin_memory()
+        u_host = torch.empty(ndofs, dtype=torch.float64).pin_memory()
+
+        def e2e_step():
+            m = rd.mesh_from_arrays(pxyz.numpy(), ptets.numpy(), pbnd.numpy(), ctx)
+            s2 = rd.build_system(m, rho, args.target)
+            out = rd.solve_system_amg(s2.A, s2.f_ptr, TOL, u=u_host)
+            return out.iterations
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        e2e_its = [e2e_step() for _ in range(args.steps)]
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        e2e_work = torch.tensor([float(ndofs) * sum(e2e_its)], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX)
+            torch.distributed.all_reduce(e2e_work, op=torch.distributed.ReduceOp.SUM)
+        result["e2e"] = {"value": float(e2e_work.item()) / (float(e2e_ms.item()) / 1e3), "unit": UNIT,
+                         "ms_per_step": float(e2e_ms.item()) / args.steps,
+                         "h2d_bytes_per_step": int(xyz.nbytes + tets.nbytes + bnd.nbytes),
+                         "d2h_bytes_per_step": int(8 * ndofs),
+                         "path": "rd_gpu_mesh_create(pinned host TetMesh) -> rd_gpu_build_system -> "
+                                 "rd_gpu_solve_system_amg(u -> pinned host)"}
+
+    # ---------------- CPU baseline (rank 0, N = 1): the oracle port on the host cores
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(n, args.target)
+    return result
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(n, target):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+
+    O.build()
+    cores = host_threads()
+    O.set_num_threads(cores)
+    r = O.pipeline(n, rho_for(n), target, 0, TOL)
+    return {"value": r["n_dofs"] * r["iterations"] / r["total_s"], "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"one full C2 step on the CPU oracle (n={n}: build_system + build_amg + pcg, "
+                      f"{r['iterations']} iterations), {r['total_s']:.1f} s; SGS/setup serial as in the reference",
+            "phases_s": {"build": r["build_s"], "setup": r["setup_s"], "solve": r["solve_s"]}}
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+
+    O.build()
+    cores = host_threads()
+    O.set_num_threads(cores)
+    n = args.n
+    for _ in range(args.warmup):  # CPU warm-up on a small case (threads, page cache)
+        O.pipeline(16, rho_for(16), args.target, 0, TOL)
+    t0 = time.perf_counter()
+    runs = [O.pipeline(n, rho_for(n), args.target, 0, TOL) for _ in range(args.steps)]
+    el = time.perf_counter() - t0
+    work = sum(r["n_dofs"] * r["iterations"] for r in runs)
+    value = work / el
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated Kuhn lattice, ball target, seeded)",
+        "config": {"workload": f"C2: build_system + build_amg + pcg, n={n}, rho=h^2, {args.target} target, rtol {TOL}",
+                   "n": n, "n_dofs": runs[0]["n_dofs"], "rho": rho_for(n), "target": args.target, "tol": TOL},
+        "iterations": runs[0]["iterations"],
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} full C2 steps (reference rdsolve not buildable here: no Eigen; "
+                                   f"the oracle/ C++ port with -O3 -ffp-contract=off, {cores} threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "phases_s": {k: statistics.mean(r[k] for r in runs) for k in ("build_s", "setup_s", "solve_s")},
+    }
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+
+        backend = "nccl" if (args.impl == "ours" and torch.cuda.is_available()) else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group(backend=backend)
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+    else:
+        res = run_ours(args, rank, world, local_rank)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch
+
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

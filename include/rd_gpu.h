@@ -140,6 +140,11 @@ int rd_gpu_amg_level_flags(const rd_amg* h, int level, uint8_t* flags);
 int rd_gpu_amg_level_structured(const rd_amg* h, int level);
 /* replaces rd::amg_apply(h, r) / amg_precond(h)          amg.hpp:39-42, amg.cpp:119-145 */
 int rd_gpu_amg_apply(rd_amg* h, const double* r, double* z);
+/* one Gauss-Seidel pass (forward != 0: i ascending) on level l's matrix with the
+ * kernel the V-cycle uses there; DEVICE pointers, stream-ordered (xin may be NULL =
+ * zero vector).  Half of rd::sgs_sweep (amg.cpp:67-88); used to time the smoother. */
+int rd_gpu_amg_level_sweep(rd_amg* h, int level, int forward, const double* f, const double* xin,
+                           double* xout);
 
 /* ------------------------------------------------------------ PCG */
 typedef struct {

@@ -91,6 +91,8 @@ def lib():
         "or_amg_apply": (_I, [_P, _I, _pd, _pd]),
         "or_pcg": (_I, [_P, _I, _P, _pd, _D, _I, _pd, C.POINTER(_I), C.POINTER(_I), _pd]),
         "or_solve_system_amg": (_I, [_P, _D, _pd, C.POINTER(_I), C.POINTER(_I), C.POINTER(_D), C.POINTER(_D)]),
+        "or_pipeline": (_I, [_I, _D, _I, C.c_uint64, _D, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I),
+                             C.POINTER(_D), C.POINTER(_D), C.POINTER(_D)]),
         "or_l2_error_manufactured": (_I, [_P, _P, _pd, _D, C.POINTER(_D)]),
         "or_h1_semi_error_manufactured": (_I, [_P, _P, _pd, _D, C.POINTER(_D)]),
     }
@@ -429,6 +431,16 @@ def solve_system_amg(sys: FemSystem, tol: float = 1e-8) -> SolveOutcome:
     ts, tv = _D(), _D()
     _check(lib().or_solve_system_amg(sys._h.h, float(tol), u, C.byref(it), C.byref(conv), C.byref(ts), C.byref(tv)))
     return SolveOutcome(u[: sys.n_dofs], it.value, bool(conv.value), ts.value, tv.value)
+
+
+def pipeline(n: int, rho: float, target: str = "ball", seed: int = 0, tol: float = 1e-8) -> dict:
+    """Mesh + build_system, build_amg, pcg on the CPU, timed in C++ (bench.cpp:193-224)."""
+    it, conv, nd = _I(), _I(), _I()
+    tb, ts, tv = _D(), _D(), _D()
+    _check(lib().or_pipeline(int(n), float(rho), TARGETS[target], int(seed), float(tol), C.byref(it), C.byref(conv),
+                             C.byref(nd), C.byref(tb), C.byref(ts), C.byref(tv)))
+    return {"iterations": it.value, "converged": bool(conv.value), "n_dofs": nd.value, "build_s": tb.value,
+            "setup_s": ts.value, "solve_s": tv.value, "total_s": tb.value + ts.value + tv.value}
 
 
 def l2_error_manufactured(mesh: Mesh, sys: FemSystem, coeffs, rho_exact: float) -> float:

@@ -1391,6 +1391,32 @@ int or_solve_system_amg(const or_system* s, double tol, double* u, int* iteratio
   });
 }
 
+// The whole BASELINE step on the CPU, timed in C++ like bench.cpp:193-224:
+// build_structured_cube + build_system [t_build], build_amg [t_setup], pcg [t_solve].
+int or_pipeline(int n, double rho, int kind, uint64_t seed, double tol, int* iterations, int* converged,
+                int* n_dofs, double* t_build, double* t_setup, double* t_solve) {
+  return guard([&] {
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    const Mesh m = build_structured_cube(n);
+    const Target t = make_target(kind, kind == OR_TARGET_SINE_RANDOM ? n : 0, seed);
+    const System s = build_system(m, rho, t);
+    const auto t1 = clk::now();
+    const Amg h = build_amg(s.A, 64, 1);
+    const auto t2 = clk::now();
+    const Csr& A = s.A;
+    const PcgOut o = pcg([&A](const Vec& v) { return spmv(A, v); }, [&h](const Vec& r) { return amg_apply(h, r); },
+                         s.f, tol, 500);
+    const auto t3 = clk::now();
+    *iterations = o.iterations;
+    *converged = o.converged ? 1 : 0;
+    *n_dofs = s.dm.n_dofs();
+    *t_build = std::chrono::duration<double>(t1 - t0).count();
+    *t_setup = std::chrono::duration<double>(t2 - t1).count();
+    *t_solve = std::chrono::duration<double>(t3 - t2).count();
+  });
+}
+
 int or_l2_error_manufactured(const or_mesh* m, const or_system* s, const double* coeffs, double rho, double* out) {
   return guard([&] { *out = l2_error(m->m, s->s.dm, coeffs, manufactured_exact(rho)); });
 }

@@ -101,6 +101,10 @@ int or_pcg(const or_csr* a, int precond, const or_amg* h, const double* f,
 int or_solve_system_amg(const or_system* s, double tol, double* u, int* iterations,
                         int* converged, double* setup_seconds, double* solve_seconds);
 
+/* the whole BASELINE step on the CPU (mesh + build_system, build_amg, pcg), timed in C++ */
+int or_pipeline(int n, double rho, int target_kind, uint64_t seed, double tol, int* iterations,
+                int* converged, int* n_dofs, double* t_build, double* t_setup, double* t_solve);
+
 /* assembly.cpp:265-310 error norms against the closed form (manufactured_exact) */
 int or_l2_error_manufactured(const or_mesh* m, const or_system* s, const double* coeffs,
                              double rho_exact, double* out);

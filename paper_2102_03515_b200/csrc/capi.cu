@@ -438,6 +438,15 @@ int rd_gpu_amg_apply(rd_amg* h, const double* r, double* z) {
   });
 }
 
+int rd_gpu_amg_level_sweep(rd_amg* h, int level, int forward, const double* f, const double* xin, double* xout) {
+  return guard(h->ctx, [&] {
+    require(level >= 0 && level < (int)h->h.levels.size(), "amg_level_sweep: bad level");
+    require(is_device_ptr(f) && is_device_ptr(xout) && (!xin || is_device_ptr(xin)),
+            "amg_level_sweep: device pointers required");
+    gs_pass(h->ctx->c, h->h.levels[level].A, f, xin, xout, forward != 0);
+  });
+}
+
 // ------------------------------------------------------------ PCG / solve_system
 int rd_gpu_pcg(rd_ctx* ctx, const rd_csr* a, rd_amg* amg, const double* f, double tol, int max_iter, double* x,
                rd_pcg_report* rep, double* hist) {

@@ -28,6 +28,9 @@ struct DCsr {
   // never need clearing between sweeps
   mutable DBuf<unsigned> gs_flags;
   mutable unsigned gs_epoch = 0;
+  // structured smoother: per-tile progress words (epoch << 32 | steps done)
+  mutable DBuf<unsigned long long> lat_progress;
+  mutable unsigned lat_epoch = 0;
 };
 
 // ---------------------------------------------------------------- scan

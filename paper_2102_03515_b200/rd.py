@@ -108,6 +108,7 @@ def lib():
         "rd_gpu_amg_level_flags": (_I, [_P, _I, _P]),
         "rd_gpu_amg_level_structured": (_I, [_P, _I]),
         "rd_gpu_amg_apply": (_I, [_P, _P, _P]),
+        "rd_gpu_amg_level_sweep": (_I, [_P, _I, _I, _P, _P, _P]),
         "rd_gpu_pcg": (_I, [_P, _P, _P, _P, _D, _I, _P, _P, _P]),
         "rd_gpu_solve_system_amg": (_I, [_P, _P, _P, _D, _P, _P]),
     }
@@ -437,6 +438,11 @@ class AmgHierarchy:
             return out[: self.n]
         self.ctx.check(lib().rd_gpu_amg_apply(self.h, _ptr(r), _ptr(z)))
         return z
+
+    def level_sweep(self, l: int, forward: bool, f, xin, xout):
+        """One GS pass on level l with the V-cycle's kernel (device buffers, stream-ordered)."""
+        self.ctx.check(lib().rd_gpu_amg_level_sweep(self.h, int(l), 1 if forward else 0, _ptr(f), _ptr(xin),
+                                                    _ptr(xout)))
 
     def __del__(self):
         if getattr(self, "h", None):

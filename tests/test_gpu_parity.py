@@ -194,6 +194,25 @@ def test_sgs_bit_exact(rd, O, n):
     assert np.array_equal(rd.sgs_sweep(A, f, u), O.sgs_sweep(os_.A, f, u))
 
 
+@pytest.mark.parametrize("n,target", [(65, "smooth"), (128, "ball")])
+def test_sgs_bit_exact_large(rd, O, n, target):
+    """The structured lattice kernel at the BASELINE sizes (many tiles, halo traffic)."""
+    O.set_num_threads(8)
+    ds = rd.build_system(rd.build_structured_cube(n), 1.0 / (n * n), target)
+    A = ds.A
+    rp, ci, v = A.download()
+    Ao = O.Csr(A.rows, A.cols, rp, ci, v)
+    f = O.pseudo_random_vec(A.rows, 3)
+    u = O.pseudo_random_vec(A.rows, 4)
+    assert np.array_equal(rd.sgs_sweep(A, f, u), O.sgs_sweep(Ao, f, u))
+
+
+def test_structured_levels_detected(rd, O):
+    os_ = O.build_system(O.build_structured_cube(32), 2.0 ** -10, "smooth")
+    h = rd.build_amg(to_dev(rd, os_.A))
+    assert [h.structured(l) for l in range(h.num_levels - 1)] == [True] * (h.num_levels - 1)
+
+
 def test_sgs_random_sparse_bit_exact(rd, O):
     rng = np.random.default_rng(5)
     n = 500
