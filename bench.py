@@ -218,6 +218,15 @@ def run_ours(args, rank, world, local_rank):
         return a.elapsed_time(b) / R
 
     gs_ms = timed(lambda: h.level_sweep(0, True, s.f_ptr, x, y))
+    level_sweeps = []
+    for l in range(h.num_levels - 1):
+        Al = h.level(l)
+        xl = torch.rand(Al.rows, dtype=torch.float64, device=dev)
+        fl = torch.rand(Al.rows, dtype=torch.float64, device=dev)
+        yl = torch.empty(Al.rows, dtype=torch.float64, device=dev)
+        fw = timed(lambda: h.level_sweep(l, True, fl, xl, yl))
+        bw = timed(lambda: h.level_sweep(l, False, fl, xl, yl))
+        level_sweeps.append({"level": l, "rows": Al.rows, "nnz": Al.nnz, "fwd_ms": fw, "bwd_ms": bw})
     spmv_ms = timed(lambda: rd.lib().rd_gpu_spmv(ctx.h, s.A.h, rd._ptr(x), rd._ptr(y)))
     structured = h.structured(0)
     gs_bytes = (8 * Z + 4 * (N + 1) + 24 * N) if structured else (12 * Z + 28 * N + 4)
@@ -241,6 +250,7 @@ def run_ours(args, rank, world, local_rank):
         "gs_sweep_level0": {"bytes_per_launch": gs_bytes, "launch_ms": gs_ms, "achieved_gbs": gs_gbs,
                             "frac": gs_gbs / peak},
         "levels": h.num_levels,
+        "level_sweeps": level_sweeps,
         "structured_levels": [bool(h.structured(l)) for l in range(h.num_levels - 1)],
     }
     del h, s

@@ -28,8 +28,8 @@ struct DCsr {
   // never need clearing between sweeps
   mutable DBuf<unsigned> gs_flags;
   mutable unsigned gs_epoch = 0;
-  // structured smoother: per-tile progress words (epoch << 32 | steps done)
-  mutable DBuf<unsigned long long> lat_progress;
+  // structured smoother: tagged halo cells {value, sweep tag} (2 words per row)
+  mutable DBuf<unsigned long long> lat_xh;
   mutable unsigned lat_epoch = 0;
 };
 

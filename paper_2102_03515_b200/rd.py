@@ -174,9 +174,12 @@ class Context:
         self.check(lib().rd_gpu_synchronize(self.h))
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().rd_gpu_ctx_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().rd_gpu_ctx_destroy(self.h)
+        except Exception:
+            pass
+        self.h = None
 
 
 _default_ctx: Context | None = None
@@ -232,8 +235,11 @@ class Csr:
         return D
 
     def __del__(self):
-        if getattr(self, "h", None) and self._owned:
-            lib().rd_gpu_csr_free(self.h)
+        try:
+            if getattr(self, "h", None) and self._owned:
+                lib().rd_gpu_csr_free(self.h)
+        except Exception:
+            pass
         self.h = None
 
 
@@ -279,9 +285,12 @@ class TetMesh:
         return xyz[: self.n_vertices], tets[: self.n_tets], b[: self.n_vertices]
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().rd_gpu_mesh_free(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().rd_gpu_mesh_free(self.h)
+        except Exception:
+            pass
+        self.h = None
 
 
 def build_structured_cube(n: int, ctx: Context | None = None) -> TetMesh:
@@ -336,9 +345,12 @@ class FemSystem:
         return v2d[: self.mesh.n_vertices], d2v[: self.n_dofs]
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().rd_gpu_system_free(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().rd_gpu_system_free(self.h)
+        except Exception:
+            pass
+        self.h = None
 
 
 def build_system(mesh: TetMesh, rho: float, target: str = "smooth", seed: int = 0) -> FemSystem:
@@ -445,9 +457,12 @@ class AmgHierarchy:
                                                     _ptr(xout)))
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().rd_gpu_amg_free(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().rd_gpu_amg_free(self.h)
+        except Exception:
+            pass
+        self.h = None
 
 
 def build_amg(A: Csr, coarsest_threshold: int = 64, smoothing_steps: int = 1) -> AmgHierarchy:

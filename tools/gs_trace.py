@@ -1,0 +1,45 @@
+"""Dump per-tile step timestamps of one lattice sweep per level (RD_GS_TRACE)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+path = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/trace.txt"
+if os.path.exists(path):
+    os.remove(path)
+os.environ["RD_GS_TRACE"] = path
+from paper_2102_03515_b200 import rd  # noqa: E402
+
+n = 128
+s = rd.build_system(rd.build_structured_cube(n), 1.0 / n ** 2, "ball")
+h = rd.build_amg(s.A)
+import torch  # noqa: E402
+
+for l in range(h.num_levels - 1):
+    A = h.level(l)
+    x = torch.rand(A.rows, dtype=torch.float64, device="cuda")
+    f = torch.rand(A.rows, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+    for _ in range(2):
+        h.level_sweep(l, True, f, x, y)
+h.ctx.synchronize()
+# analyse
+lines = open(path).read().splitlines()
+i = 0
+while i < len(lines):
+    hdr = lines[i].split()
+    L, nty, ntz, ns = int(hdr[1]), int(hdr[3]), int(hdr[5]), int(hdr[7])
+    T = np.array([[int(v) for v in lines[i + 1 + t].split()] for t in range(nty * ntz)], dtype=np.int64)
+    i += 1 + nty * ntz
+    t0 = T[:, 0].min()
+    start = (T[:, 0] - t0) / 1e3
+    steps = (T[:, 2:] - t0) / 1e3
+    end = steps[:, -1]
+    dt = np.diff(steps, axis=1)
+    print(f"L={L} tiles={nty}x{ntz} ns={ns}: span {end.max():.1f} us; start max {start.max():.1f}; "
+          f"median step {np.median(dt):.3f} us; p90 step {np.percentile(dt, 90):.3f}; "
+          f"tile0 steps {np.median(dt[0]):.3f}; last tile start->first step {steps[-1,0]-start[-1]:.1f}")
+    if nty * ntz > 1:
+        # lag of each tile's step 0 vs its first-row step, along the diagonal
+        print("   first-step time per tile (y fastest):", np.round(steps[:, 0], 1)[: min(24, nty * ntz)])
