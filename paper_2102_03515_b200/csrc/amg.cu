@@ -284,7 +284,10 @@ void build_hierarchy(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h) 
     }
     lv.t.alloc(n, c.stream);
     lv.res.alloc(n, c.stream);
-    if (lv.has_p) detect_lattice(c, lv.A);
+    if (lv.has_p) {
+      detect_lattice(c, lv.A);
+      lattice_prepare(c, lv.A);
+    }
   }
 }
 

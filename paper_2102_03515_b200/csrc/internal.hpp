@@ -28,7 +28,9 @@ struct DCsr {
   // never need clearing between sweeps
   mutable DBuf<unsigned> gs_flags;
   mutable unsigned gs_epoch = 0;
-  // structured smoother: tagged halo cells {value, sweep tag} (2 words per row)
+  // structured smoother: step-major packed values (fwd, bwd) and tagged halo
+  // cells {value, sweep tag} (2 words per row), built by lattice_prepare
+  mutable DBuf<double> lat_pack[2];
   mutable DBuf<unsigned long long> lat_xh;
   mutable unsigned lat_epoch = 0;
 };
@@ -60,6 +62,8 @@ void detect_lattice(Ctx& c, DCsr& A);
 // nullptr = zero vector).  Optionally accumulates dot(r, xout) into dot_out.
 void gs_pass(Ctx& c, const DCsr& A, const double* f, const double* xin, double* xout, bool fwd,
              double* dot_out = nullptr, const double* dot_with = nullptr);
+// setup-time layout for the structured smoother (no-op unless A.lat.ok)
+void lattice_prepare(Ctx& c, const DCsr& A);
 
 // ---------------------------------------------------------------- amg.cu
 struct Level {
