@@ -35,15 +35,16 @@ __global__ void __launch_bounds__(kMisNT) mis_kernel(int n, const int* __restric
   for (int k = grp[i]; k < grp[i + 1]; ++k) {
     const int j = gci[k];
     if (j >= i) continue;
+    // the state word is the whole message: relaxed loads suffice (no L1 invalidation)
     int sj;
-    while ((sj = ld_acquire_s32(state + j)) == kUndecided) {
+    while ((sj = ld_relaxed_s32(state + j)) == kUndecided) {
     }
     if (sj == kCoarse) {
       st = kFine;
       break;
     }
   }
-  st_release_s32(state + i, st);
+  st_relaxed_s32(state + i, st);
 }
 
 // guard (amg.cpp:22-29): count fine rows without a coarse neighbour
@@ -222,10 +223,7 @@ std::vector<uint8_t> coarsen(Ctx& c, const DCsr& A, DBuf<uint8_t>& flags, DCsr& 
   p_fill_kernel<<<div_up(n, 256), 256, 0, c.stream>>>(n, A.rp.p, A.ci.p, state.p, cidx.p, P.rp.p, P.ci.p, P.v.p);
   RDG_LAUNCH_CHECK();
   ++c.launches;
-  std::vector<uint8_t> h(n);
-  RDG_CUDA(cudaMemcpyAsync(h.data(), flags.p, n, cudaMemcpyDeviceToHost, c.stream));
-  RDG_CUDA(cudaStreamSynchronize(c.stream));
-  return h;
+  return {};  // flags stay on the device (rd_gpu_coarsen_redblack downloads them)
 }
 
 DCsr galerkin(Ctx& c, const DCsr& A, const DCsr& P, const DCsr& Pt) {

@@ -248,7 +248,7 @@ __device__ __forceinline__ bool local_geom(const double* v0, const double* v1, c
     return __dmul_rn(J[0][a], __dsub_rn(__dmul_rn(J[1][b], J[2][c]), __dmul_rn(J[1][c], J[2][b])));
   };
   const double det = __dadd_rn(__dsub_rn(det3(0, 1, 2), det3(1, 0, 2)), det3(2, 0, 1));
-  G.vol = __ddiv_rn(fabs(det), 6.0);
+  G.vol = div_tail(fabs(det), 6.0, div_recip(6.0));  // == __ddiv_rn(|det|, 6.0)
   if (!(G.vol > 0.0)) return false;
   auto cof = [&](int i, int j) {
     const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
@@ -256,7 +256,7 @@ __device__ __forceinline__ bool local_geom(const double* v0, const double* v1, c
   };
   const double c0[3] = {cof(0, 0), cof(1, 0), cof(2, 0)};
   const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(c0[0], J[0][0]), __dmul_rn(c0[1], J[1][0])), __dmul_rn(c0[2], J[2][0]));
-  const double invdet = __ddiv_rn(1.0, d2);
+  const double invdet = div_tail(1.0, d2, div_recip(d2));  // == __ddiv_rn(1.0, d2)
   G.g[1][0] = __dmul_rn(c0[0], invdet);
   G.g[1][1] = __dmul_rn(c0[1], invdet);
   G.g[1][2] = __dmul_rn(c0[2], invdet);
@@ -321,6 +321,90 @@ __global__ void values_kernel(int nd, const int* __restrict__ d2v, const int* __
   }
 }
 
+// Same arithmetic, four threads per row: the incident tets' element terms (the
+// expensive local_geom) are computed in parallel, staged in shared memory in
+// ascending tet order, then every slot is accumulated sequentially in that order
+// (val = 0.0; val += term; slot += val), so the sums are bit-identical to the
+// one-thread-per-row loop above.  Rows with more than kQuadMaxTets incident tets
+// use values_kernel.
+constexpr int kQuadRows = 16;  // rows per 64-thread block
+constexpr int kQuadMaxTets = 32;
+struct QuadContrib {
+  int slot[kQuadRows][kQuadMaxTets * 4];
+  double k[kQuadRows][kQuadMaxTets * 4];
+  double m[kQuadRows][kQuadMaxTets * 4];
+};
+
+__global__ void __launch_bounds__(64) values_quad_kernel(int nd, const int* __restrict__ d2v,
+                                                        const int* __restrict__ v2d, const int* __restrict__ vto,
+                                                        const int* __restrict__ vt, const int* __restrict__ tets,
+                                                        const double* __restrict__ xyz, const int* __restrict__ rp,
+                                                        const int* __restrict__ ci, double* Kf, double* Mf,
+                                                        int* err) {
+  extern __shared__ __align__(16) unsigned char qsm[];
+  QuadContrib& Q = *reinterpret_cast<QuadContrib*>(qsm);
+  const int lr = threadIdx.x >> 2, q = threadIdx.x & 3;
+  const int r = blockIdx.x * kQuadRows + lr;
+  const bool valid = r < nd;
+  int v = 0, kb = 0, deg = 0, rb = 0, re = 0;
+  if (valid) {
+    v = d2v[r];
+    kb = vto[v];
+    deg = vto[v + 1] - kb;
+    rb = rp[r];
+    re = rp[r + 1];
+  }
+  if (deg > kQuadMaxTets) {
+    atomicExch(err, -1);  // host falls back to values_kernel
+    deg = 0;
+  }
+  for (int kk = q; kk < deg; kk += 4) {
+    const int4 t4 = reinterpret_cast<const int4*>(tets)[vt[kb + kk]];
+    const int tv[4] = {t4.x, t4.y, t4.z, t4.w};
+    Geom G;
+    const bool ok = local_geom(xyz + 3 * (int64_t)tv[0], xyz + 3 * (int64_t)tv[1], xyz + 3 * (int64_t)tv[2],
+                               xyz + 3 * (int64_t)tv[3], G);
+    if (!ok) atomicExch(err, RD_EDEGENERATE);
+    int iv = 0;
+    while (iv < 3 && tv[iv] != v) ++iv;
+#pragma unroll
+    for (int jv = 0; jv < 4; ++jv) {
+      const int c = v2d[tv[jv]];
+      int slot = -1;
+      double valK = 0.0, valM = 0.0;
+      if (c >= 0 && ok) {
+        valK = __dadd_rn(0.0, __dmul_rn(__dmul_rn(1.0, G.vol), dot3(G.g[iv], G.g[jv])));
+        valM = __dadd_rn(0.0, __dmul_rn(__dmul_rn(1.0, G.vol), iv == jv ? 0.1 : 0.05));
+        int lo = rb, hi = re;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (ci[mid] < c)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        slot = lo - rb;
+      }
+      Q.slot[lr][kk * 4 + jv] = slot;
+      Q.k[lr][kk * 4 + jv] = valK;
+      Q.m[lr][kk * 4 + jv] = valM;
+    }
+  }
+  __syncthreads();
+  if (!valid) return;
+  // thread q owns slots q, q+4, ...: accumulate in (tet ascending, jv) order
+  for (int sl = q; sl < re - rb; sl += 4) {
+    double ak = 0.0, am = 0.0;
+    for (int e = 0; e < deg * 4; ++e)
+      if (Q.slot[lr][e] == sl) {
+        ak = __dadd_rn(ak, Q.k[lr][e]);
+        am = __dadd_rn(am, Q.m[lr][e]);
+      }
+    Kf[rb + sl] = ak;
+    Mf[rb + sl] = am;
+  }
+}
+
 // counts of the pruned K, pruned M, and their union (A)
 __global__ void split_count_kernel(int nd, const int* __restrict__ rp, const double* __restrict__ Kf,
                                    const double* __restrict__ Mf, int* kc, int* mc, int* ac) {
@@ -363,6 +447,48 @@ __global__ void split_fill_kernel(int nd, double rho, const int* __restrict__ rp
       av[ao++] = k && m ? __dadd_rn(__dmul_rn(rho, kq), mq) : (k ? __dadd_rn(__dmul_rn(rho, kq), 0.0) : __dadd_rn(0.0, mq));
     }
   }
+}
+
+// One thread per full-pattern entry (coalesced): rank among the row's kept
+// entries, then the same K / M / A values as split_fill_kernel.
+__global__ void split_fill_entry_kernel(int64_t zf, int nd, double rho, const int* __restrict__ rp,
+                                        const int* __restrict__ ci, const double* __restrict__ Kf,
+                                        const double* __restrict__ Mf, const int* __restrict__ krp, int* kci,
+                                        double* kv, const int* __restrict__ mrp, int* mci, double* mv,
+                                        const int* __restrict__ arp, int* aci, double* av) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= zf) return;
+  int lo = 0, hi = nd;  // row r: rp[r] <= q < rp[r+1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (rp[mid] <= q)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const int r = lo;
+  const double kq = Kf[q], mq = Mf[q];
+  const bool k = kq != 0.0, m = mq != 0.0;
+  if (!k && !m) return;
+  int kr = 0, mr = 0, ar = 0;
+  for (int e = rp[r]; e < q; ++e) {
+    const bool ke = Kf[e] != 0.0, me = Mf[e] != 0.0;
+    kr += ke;
+    mr += me;
+    ar += (ke || me);
+  }
+  const int c = ci[q];
+  if (k) {
+    kci[krp[r] + kr] = c;
+    kv[krp[r] + kr] = kq;
+  }
+  if (m) {
+    mci[mrp[r] + mr] = c;
+    mv[mrp[r] + mr] = mq;
+  }
+  aci[arp[r] + ar] = c;
+  // Eigen union sum: both -> rho*K + M, K only -> rho*K + 0, M only -> 0 + M
+  av[arp[r] + ar] = k && m ? __dadd_rn(__dmul_rn(rho, kq), mq) : (k ? __dadd_rn(__dmul_rn(rho, kq), 0.0) : __dadd_rn(0.0, mq));
 }
 
 // ---------------------------------------------------------------- targets (target.cpp + BASELINE)
@@ -463,7 +589,7 @@ __global__ void load_tet_kernel(int nt, const int* __restrict__ tets, const doub
   const double x1 = __dsub_rn(__dmul_rn(a[2], b[0]), __dmul_rn(a[0], b[2]));
   const double x2 = __dsub_rn(__dmul_rn(a[0], b[1]), __dmul_rn(a[1], b[0]));
   const double dt = __dadd_rn(__dadd_rn(__dmul_rn(x0, d[0]), __dmul_rn(x1, d[1])), __dmul_rn(x2, d[2]));
-  tvol[t] = __ddiv_rn(fabs(dt), 6.0);
+  tvol[t] = div_tail(fabs(dt), 6.0, div_recip(6.0));  // == __ddiv_rn(|dt|, 6.0)
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int q = 0; q < NQ; ++q) {
     const double* lam = NQ == 14 ? c_rules.p14[q] : c_rules.p64[q];
@@ -575,8 +701,20 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
     pattern_kernel<true><<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p,
                                                                 nullptr, frp.p, fci.p, err.p);
     RDG_LAUNCH_CHECK();
-    values_kernel<<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p, m.xyz.p,
-                                                         frp.p, fci.p, Kf.p, Mf.p, err.p);
+    static bool qattr = false;
+    if (!qattr) {
+      RDG_CUDA(cudaFuncSetAttribute(values_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sizeof(QuadContrib)));
+      qattr = true;
+    }
+    values_quad_kernel<<<div_up(nd, kQuadRows), 64, sizeof(QuadContrib), c.stream>>>(
+        nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p, m.xyz.p, frp.p, fci.p, Kf.p, Mf.p, err.p);
+    RDG_LAUNCH_CHECK();
+    if (read_flag(c, err.p) == -1) {  // some vertex has more incident tets than the quad kernel stages
+      RDG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.stream));
+      values_kernel<<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p, m.xyz.p,
+                                                           frp.p, fci.p, Kf.p, Mf.p, err.p);
+    }
     RDG_LAUNCH_CHECK();
     c.launches += 2;
   }
@@ -600,9 +738,9 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
     X.v.alloc(X.nnz, c.stream);
   }
   if (nd) {
-    split_fill_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, rho, frp.p, fci.p, Kf.p, Mf.p, s.K.rp.p, s.K.ci.p,
-                                                             s.K.v.p, s.M.rp.p, s.M.ci.p, s.M.v.p, s.A.rp.p,
-                                                             s.A.ci.p, s.A.v.p);
+    split_fill_entry_kernel<<<div_up(zf, 256), 256, 0, c.stream>>>(zf, nd, rho, frp.p, fci.p, Kf.p, Mf.p, s.K.rp.p,
+                                                                   s.K.ci.p, s.K.v.p, s.M.rp.p, s.M.ci.p, s.M.v.p,
+                                                                   s.A.rp.p, s.A.ci.p, s.A.v.p);
     RDG_LAUNCH_CHECK();
     ++c.launches;
   }

@@ -331,8 +331,8 @@ int rd_gpu_coarsen_redblack(rd_ctx* ctx, const rd_csr* a, uint8_t* flags, rd_csr
     P->ctx = ctx;
     P->owned = std::make_unique<DCsr>();
     DBuf<uint8_t> fl;
-    const std::vector<uint8_t> h = coarsen(c, *a->a, fl, *P->owned);
-    if (flags && !h.empty()) std::memcpy(flags, h.data(), h.size());
+    coarsen(c, *a->a, fl, *P->owned);
+    if (flags && a->a->rows) RDG_CUDA(cudaMemcpyAsync(flags, fl.p, a->a->rows, cudaMemcpyDefault, c.stream));
     RDG_CUDA(cudaStreamSynchronize(c.stream));
     P->a = P->owned.get();
     *p_out = P.release();

@@ -62,7 +62,8 @@ __global__ void scan_tile_sums(const int* __restrict__ in, int64_t n, long long*
   }
 }
 
-__global__ void scan_block_offsets(long long* __restrict__ bsum, int nb, long long* __restrict__ total) {
+__global__ void scan_block_offsets(long long* __restrict__ bsum, int nb, long long* __restrict__ total,
+                                   int* __restrict__ out_last) {
   // single block: exclusive scan of nb block sums in place
   __shared__ long long sh[32];
   long long carry = 0;
@@ -74,7 +75,10 @@ __global__ void scan_block_offsets(long long* __restrict__ bsum, int nb, long lo
     carry += sh[(blockDim.x >> 5) - 1];  // block total left by the scan
     __syncthreads();
   }
-  if (threadIdx.x == 0) *total = carry;
+  if (threadIdx.x == 0) {
+    *total = carry;
+    *out_last = carry > 0x7fffffffLL ? 0x7fffffff : (int)carry;  // offsets[n]
+  }
 }
 
 __global__ void scan_tiles(const int* __restrict__ in, int64_t n, const long long* __restrict__ boff,
@@ -109,18 +113,16 @@ int64_t exclusive_scan(Ctx& c, const int* counts, int* offsets, int64_t n) {
   DBuf<long long> bsum(nb + 1, c.stream);
   scan_tile_sums<<<nb, kScanNT, 0, c.stream>>>(counts, n, bsum.p);
   RDG_LAUNCH_CHECK();
-  scan_block_offsets<<<1, 1024, 0, c.stream>>>(bsum.p, nb, bsum.p + nb);
+  scan_block_offsets<<<1, 1024, 0, c.stream>>>(bsum.p, nb, bsum.p + nb, offsets + n);
   RDG_LAUNCH_CHECK();
   scan_tiles<<<nb, kScanNT, 0, c.stream>>>(counts, n, bsum.p, offsets);
   RDG_LAUNCH_CHECK();
   c.launches += 3;
-  long long total = 0;
-  RDG_CUDA(cudaMemcpyAsync(&total, bsum.p + nb, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
+  long long* hp = reinterpret_cast<long long*>(c.h_pinned + 8);  // pinned: a true async readback
+  RDG_CUDA(cudaMemcpyAsync(hp, bsum.p + nb, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
   RDG_CUDA(cudaStreamSynchronize(c.stream));
+  const long long total = *hp;
   if (total > 0x7fffffffLL) throw Error(RD_EINVAL, "index overflow: more than INT32_MAX entries (SpMat<int>)");
-  const int t32 = static_cast<int>(total);
-  RDG_CUDA(cudaMemcpyAsync(offsets + n, &t32, sizeof(int), cudaMemcpyHostToDevice, c.stream));
-  RDG_CUDA(cudaStreamSynchronize(c.stream));
   return total;
 }
 

@@ -58,6 +58,17 @@ _P = C.c_void_p
 _I = C.c_int
 _D = C.c_double
 _lib = None
+_closing = False  # set at interpreter exit: handles are then leaked to the process teardown
+
+
+def _at_exit():
+    global _closing
+    _closing = True
+
+
+import atexit  # noqa: E402
+
+atexit.register(_at_exit)
 
 
 def library_path() -> str:
@@ -175,7 +186,7 @@ class Context:
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
+            if getattr(self, "h", None) and not _closing:
                 lib().rd_gpu_ctx_destroy(self.h)
         except Exception:
             pass
@@ -236,7 +247,7 @@ class Csr:
 
     def __del__(self):
         try:
-            if getattr(self, "h", None) and self._owned:
+            if getattr(self, "h", None) and self._owned and not _closing:
                 lib().rd_gpu_csr_free(self.h)
         except Exception:
             pass
@@ -286,7 +297,7 @@ class TetMesh:
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
+            if getattr(self, "h", None) and not _closing:
                 lib().rd_gpu_mesh_free(self.h)
         except Exception:
             pass
@@ -346,7 +357,7 @@ class FemSystem:
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
+            if getattr(self, "h", None) and not _closing:
                 lib().rd_gpu_system_free(self.h)
         except Exception:
             pass
@@ -458,7 +469,7 @@ class AmgHierarchy:
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
+            if getattr(self, "h", None) and not _closing:
                 lib().rd_gpu_amg_free(self.h)
         except Exception:
             pass
