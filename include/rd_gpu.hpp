@@ -1,0 +1,274 @@
+// rd_gpu.hpp -- header-only C++17 layer over the rd_gpu C-ABI (rd_gpu.h) that
+// mirrors the reference rd:: API (/root/reference/proj/include/rd/*.hpp): same
+// function names, argument meaning and exception types.  This is what a
+// maintainer of the reference includes to route the AMG-PCG path to the B200
+// (INTEGRATION.md); status codes are rethrown as the exceptions the reference
+// throws: RD_EINVAL -> std::invalid_argument, everything else ->
+// std::runtime_error (subclass rd_gpu::Error keeps the code).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "rd_gpu.h"
+
+namespace rd_gpu {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void check(int rc, const rd_ctx* ctx) {
+  if (rc == RD_OK) return;
+  const std::string msg = rd_gpu_last_error(ctx);
+  if (rc == RD_EINVAL) throw std::invalid_argument(msg);
+  throw Error(rc, msg);
+}
+
+// ------------------------------------------------------------------ context
+class Context {
+ public:
+  explicit Context(int device = 0, void* stream = nullptr) { check(rd_gpu_ctx_create(device, stream, &h_), nullptr); }
+  ~Context() { rd_gpu_ctx_destroy(h_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  rd_ctx* get() const { return h_; }
+  void synchronize() { check(rd_gpu_synchronize(h_), h_); }
+  int64_t launch_count() const { return rd_gpu_launch_count(h_); }
+
+ private:
+  rd_ctx* h_ = nullptr;
+};
+
+inline Context& default_context() {
+  static Context ctx(0);
+  return ctx;
+}
+
+// host CSR view, the storage contract of rd::SpMat (types.hpp:14)
+struct HostCsr {
+  int rows = 0, cols = 0;
+  std::vector<int32_t> row_ptr{0}, col_idx;
+  std::vector<double> values;
+};
+
+// ------------------------------------------------------------------ matrices
+class DeviceMatrix {
+ public:
+  DeviceMatrix() = default;
+  DeviceMatrix(Context& ctx, int rows, int cols, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* v)
+      : ctx_(&ctx) {
+    rd_csr* h = nullptr;
+    check(rd_gpu_csr_create(ctx.get(), rows, cols, nnz, rp, ci, v, &h), ctx.get());
+    h_ = std::shared_ptr<rd_csr>(h, rd_gpu_csr_free);
+  }
+  explicit DeviceMatrix(Context& ctx, const HostCsr& a)
+      : DeviceMatrix(ctx, a.rows, a.cols, (int64_t)a.col_idx.size(), a.row_ptr.data(), a.col_idx.data(),
+                     a.values.data()) {}
+  // borrowed view (system / hierarchy keeps it alive through `owner`)
+  DeviceMatrix(Context& ctx, const rd_csr* view, std::shared_ptr<void> owner)
+      : ctx_(&ctx), view_(view), owner_(std::move(owner)) {}
+
+  const rd_csr* get() const { return h_ ? h_.get() : view_; }
+  int rows() const { int r; rd_gpu_csr_info(get(), &r, nullptr, nullptr); return r; }
+  int cols() const { int c; rd_gpu_csr_info(get(), nullptr, &c, nullptr); return c; }
+  int64_t nonZeros() const { int64_t z; rd_gpu_csr_info(get(), nullptr, nullptr, &z); return z; }
+  HostCsr download() const {
+    HostCsr a;
+    a.rows = rows();
+    a.cols = cols();
+    a.row_ptr.resize(a.rows + 1);
+    a.col_idx.resize(nonZeros());
+    a.values.resize(nonZeros());
+    check(rd_gpu_csr_download(get(), a.row_ptr.data(), a.col_idx.data(), a.values.data()), ctx_->get());
+    return a;
+  }
+  Context& context() const { return *ctx_; }
+
+ private:
+  Context* ctx_ = nullptr;
+  std::shared_ptr<rd_csr> h_;
+  const rd_csr* view_ = nullptr;
+  std::shared_ptr<void> owner_;
+};
+
+// ------------------------------------------------------------------ mesh / system
+class TetMesh {
+ public:
+  TetMesh(Context& ctx, rd_mesh* h) : ctx_(&ctx), h_(h, rd_gpu_mesh_free) {}
+  const rd_mesh* get() const { return h_.get(); }
+  int n_vertices() const { int v; rd_gpu_mesh_info(get(), &v, nullptr, nullptr); return v; }
+  int n_tets() const { int t; rd_gpu_mesh_info(get(), nullptr, &t, nullptr); return t; }
+  Context& context() const { return *ctx_; }
+
+ private:
+  Context* ctx_;
+  std::shared_ptr<rd_mesh> h_;
+};
+
+// mesh.hpp:36
+inline TetMesh build_structured_cube(int n, Context& ctx = default_context()) {
+  rd_mesh* h = nullptr;
+  check(rd_gpu_build_structured_cube(ctx.get(), n, &h), ctx.get());
+  return TetMesh(ctx, h);
+}
+
+enum class Target { smooth = RD_TARGET_SMOOTH, box = RD_TARGET_BOX, nonzero_bc = RD_TARGET_NONZERO_BC,
+                    ball = RD_TARGET_BALL, sine_random = RD_TARGET_SINE_RANDOM };
+
+// assembly.hpp:24-31 FemSystem, resident in HBM
+class FemSystem {
+ public:
+  FemSystem(Context& ctx, rd_system* h, double rho) : ctx_(&ctx), h_(h, rd_gpu_system_free), rho(rho) {
+    K = DeviceMatrix(ctx, rd_gpu_system_matrix(h, 0), h_);
+    M = DeviceMatrix(ctx, rd_gpu_system_matrix(h, 1), h_);
+    A = DeviceMatrix(ctx, rd_gpu_system_matrix(h, 2), h_);
+  }
+  int n_dofs() const { return rd_gpu_system_n_dofs(h_.get()); }
+  const double* f_device() const { return rd_gpu_system_load(h_.get()); }
+  std::vector<double> f() const {
+    std::vector<double> out(n_dofs());
+    if (!out.empty()) check(rd_gpu_copy(ctx_->get(), out.data(), f_device(), 8 * out.size()), ctx_->get());
+    return out;
+  }
+
+ private:
+  Context* ctx_;
+  std::shared_ptr<rd_system> h_;
+
+ public:
+  double rho;
+  DeviceMatrix K, M, A;
+};
+
+// assembly.hpp:48
+inline FemSystem build_system(const TetMesh& mesh, double rho, Target target, uint64_t seed = 0) {
+  rd_system* h = nullptr;
+  const rd_target t{static_cast<int>(target), seed};
+  check(rd_gpu_build_system(mesh.context().get(), mesh.get(), rho, &t, &h), mesh.context().get());
+  return FemSystem(mesh.context(), h, rho);
+}
+
+// ------------------------------------------------------------------ linalg / amg
+// linalg.hpp:30
+inline std::vector<double> spmv(const DeviceMatrix& A, const std::vector<double>& x) {
+  if ((int)x.size() != A.cols()) throw std::invalid_argument("spmv: dimension mismatch");
+  std::vector<double> y(A.rows());
+  check(rd_gpu_spmv(A.context().get(), A.get(), x.data(), y.data()), A.context().get());
+  return y;
+}
+
+// amg.hpp:29
+inline std::pair<std::vector<uint8_t>, DeviceMatrix> coarsen_redblack(const DeviceMatrix& A) {
+  std::vector<uint8_t> flags(A.rows());
+  rd_csr* P = nullptr;
+  check(rd_gpu_coarsen_redblack(A.context().get(), A.get(), flags.data(), &P), A.context().get());
+  std::shared_ptr<rd_csr> own(P, rd_gpu_csr_free);
+  return {std::move(flags), DeviceMatrix(A.context(), P, own)};
+}
+
+// amg.hpp:31
+inline DeviceMatrix galerkin_coarse(const DeviceMatrix& A, const DeviceMatrix& P) {
+  rd_csr* c = nullptr;
+  check(rd_gpu_galerkin_coarse(A.context().get(), A.get(), P.get(), &c), A.context().get());
+  std::shared_ptr<rd_csr> own(c, rd_gpu_csr_free);
+  return DeviceMatrix(A.context(), c, own);
+}
+
+// amg.hpp:34
+inline std::vector<double> sgs_sweep(const DeviceMatrix& A, const std::vector<double>& f, const std::vector<double>& u) {
+  std::vector<double> out(A.rows());
+  check(rd_gpu_sgs_sweep(A.context().get(), A.get(), f.data(), u.data(), out.data()), A.context().get());
+  return out;
+}
+
+// amg.hpp:13-24, 36-42
+class AmgHierarchy {
+ public:
+  AmgHierarchy(const DeviceMatrix& A, int coarsest_threshold = 64, int smoothing_steps = 1) : ctx_(&A.context()) {
+    rd_amg* h = nullptr;
+    check(rd_gpu_amg_setup(ctx_->get(), A.get(), coarsest_threshold, smoothing_steps, &h), ctx_->get());
+    h_ = std::shared_ptr<rd_amg>(h, rd_gpu_amg_free);
+  }
+  int num_levels() const { return rd_gpu_amg_num_levels(h_.get()); }
+  DeviceMatrix level(int l, int which = 0) const { return DeviceMatrix(*ctx_, rd_gpu_amg_level_matrix(h_.get(), l, which), h_); }
+  std::vector<uint8_t> coarse_flag(int l) const {
+    std::vector<uint8_t> f(level(l).rows());
+    check(rd_gpu_amg_level_flags(h_.get(), l, f.data()), ctx_->get());
+    return f;
+  }
+  rd_amg* get() const { return h_.get(); }
+  Context& context() const { return *ctx_; }
+
+ private:
+  Context* ctx_;
+  std::shared_ptr<rd_amg> h_;
+};
+
+inline AmgHierarchy build_amg(const DeviceMatrix& A, int coarsest_threshold = 64, int smoothing_steps = 1) {
+  return AmgHierarchy(A, coarsest_threshold, smoothing_steps);
+}
+
+inline std::vector<double> amg_apply(const AmgHierarchy& h, const std::vector<double>& r) {
+  std::vector<double> z(r.size());
+  if (r.empty()) return z;
+  check(rd_gpu_amg_apply(h.get(), r.data(), z.data()), h.context().get());
+  return z;
+}
+
+// linalg.hpp:13-24
+struct PcgReport {
+  int iterations = 0;
+  bool converged = false;
+  std::vector<double> residual_history;
+};
+struct PcgResult {
+  std::vector<double> x;
+  PcgReport report;
+};
+
+// linalg.hpp:46-49 with apply_P = amg_precond(h) (h == nullptr: identity)
+inline PcgResult pcg(const DeviceMatrix& A, const AmgHierarchy* h, const std::vector<double>& f, double tol = 1e-8,
+                     int max_iter = 500) {
+  PcgResult out;
+  out.x.resize(f.size());
+  std::vector<double> hist(max_iter > 0 ? max_iter : 1);
+  rd_pcg_report rep{};
+  check(rd_gpu_pcg(A.context().get(), A.get(), h ? h->get() : nullptr, f.data(), tol, max_iter, out.x.data(), &rep,
+                   hist.data()),
+        A.context().get());
+  out.report.iterations = rep.iterations;
+  out.report.converged = rep.converged != 0;
+  out.report.residual_history.assign(hist.begin(), hist.begin() + rep.iterations);
+  return out;
+}
+
+// bench.hpp:48-57 SolveOutcome / solve_system(..., PrecondKind::amg, ...)
+struct SolveOutcome {
+  std::vector<double> u;
+  int iterations = 0;
+  bool converged = false;
+  double setup_seconds = 0.0;
+  double solve_seconds = 0.0;
+};
+
+inline SolveOutcome solve_system_amg(const DeviceMatrix& A, const double* f, double tol) {
+  SolveOutcome out;
+  out.u.resize(A.rows());
+  rd_solve_outcome o{};
+  check(rd_gpu_solve_system_amg(A.context().get(), A.get(), f, tol, out.u.data(), &o), A.context().get());
+  out.iterations = o.iterations;
+  out.converged = o.converged != 0;
+  out.setup_seconds = o.setup_seconds;
+  out.solve_seconds = o.solve_seconds;
+  return out;
+}
+
+inline SolveOutcome solve_system_amg(const FemSystem& sys, double tol) { return solve_system_amg(sys.A, sys.f_device(), tol); }
+
+}  // namespace rd_gpu

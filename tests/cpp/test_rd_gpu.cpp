@@ -1,0 +1,138 @@
+// C++ drop-in test: the reference's own hot-path test cases (test_amg.cpp,
+// test_linalg.cpp, test_assembly.cpp, test_bench.cpp) written against the
+// rd_gpu:: C++ layer (include/rd_gpu.hpp) exactly as a maintainer of the
+// reference would call it.  Prints one line per case; exit code = failures.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "rd_gpu.hpp"
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                      \
+  do {                                                                   \
+    if (cond) {                                                          \
+      ++g_pass;                                                          \
+    } else {                                                             \
+      ++g_fail;                                                          \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+    }                                                                    \
+  } while (0)
+
+using namespace rd_gpu;
+
+static DeviceMatrix from_dense(Context& ctx, int n, const std::vector<double>& d) {
+  HostCsr a;
+  a.rows = a.cols = n;
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < n; ++j)
+      if (d[i * n + j] != 0.0) {
+        a.col_idx.push_back(j);
+        a.values.push_back(d[i * n + j]);
+      }
+    a.row_ptr.push_back((int)a.col_idx.size());
+  }
+  return DeviceMatrix(ctx, a);
+}
+
+int main() {
+  Context& ctx = default_context();
+  {  // test_amg.cpp:36-52 red-black coarsening of a path graph
+    std::vector<double> d(25, 0.0);
+    for (int i = 0; i < 5; ++i) {
+      d[i * 5 + i] = 2.0;
+      if (i + 1 < 5) d[i * 5 + i + 1] = d[(i + 1) * 5 + i] = -1.0;
+    }
+    auto fp = coarsen_redblack(from_dense(ctx, 5, d));
+    CHECK(fp.first == std::vector<uint8_t>({1, 0, 1, 0, 1}));
+    const HostCsr P = fp.second.download();
+    CHECK(P.cols == 3 && P.values[1] == 0.5 && P.values[2] == 0.5);
+  }
+  {  // test_amg.cpp:83-90 galerkin hand case
+    auto A = from_dense(ctx, 2, {2.0, -1.0, -1.0, 2.0});
+    HostCsr p;
+    p.rows = 2;
+    p.cols = 1;
+    p.row_ptr = {0, 1, 2};
+    p.col_idx = {0, 0};
+    p.values = {1.0, 0.5};
+    const HostCsr Ac = galerkin_coarse(A, DeviceMatrix(ctx, p)).download();
+    CHECK(Ac.rows == 1 && std::fabs(Ac.values[0] - 1.5) < 1e-14);
+  }
+  {  // test_amg.cpp:109-117 SGS hand sweep
+    auto A = from_dense(ctx, 2, {2.0, 1.0, 1.0, 2.0});
+    auto u = sgs_sweep(A, {1.0, 1.0}, {0.0, 0.0});
+    CHECK(std::fabs(u[0] - 0.375) < 1e-15 && std::fabs(u[1] - 0.25) < 1e-15);
+  }
+  {  // amg.cpp:82 zero diagonal -> std::runtime_error
+    auto A = from_dense(ctx, 2, {0.0, 1.0, 1.0, 2.0});
+    bool threw = false;
+    try {
+      sgs_sweep(A, {1.0, 1.0}, {0.0, 0.0});
+    } catch (const std::runtime_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  {  // test_linalg.cpp:47-71 spmv hand case + dimension mismatch -> invalid_argument
+    auto A = from_dense(ctx, 2, {2.0, 1.0, 1.0, 2.0});
+    auto y = spmv(A, {1.0, 1.0});
+    CHECK(y[0] == 3.0 && y[1] == 3.0);
+    bool threw = false;
+    try {
+      spmv(A, {1.0, 1.0, 1.0});
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  {  // test_linalg.cpp:96-104, 126-139 pcg cases
+    auto A1 = from_dense(ctx, 1, {2.0});
+    auto r = pcg(A1, nullptr, {4.0}, 1e-12, 10);
+    CHECK(r.report.converged && r.report.iterations == 1 && std::fabs(r.x[0] - 2.0) < 1e-14);
+    auto B = from_dense(ctx, 2, {1.0, 0.0, 0.0, -1.0});
+    bool threw = false;
+    try {
+      pcg(B, nullptr, {1.0, 1.0}, 1e-10, 10);
+    } catch (const std::runtime_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  {  // test_mesh.cpp:55-66 / test_assembly.cpp:96-100
+    auto mesh = build_structured_cube(4, ctx);
+    CHECK(mesh.n_vertices() == 125 && mesh.n_tets() == 384);
+    auto sys = build_system(mesh, 1e-2, Target::smooth);
+    CHECK(sys.n_dofs() == 27);
+    bool threw = false;
+    try {
+      build_system(mesh, 0.0, Target::smooth);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  {  // test_amg.cpp:187-202 rho-robust counts at n = 8 (AMG-PCG through the device)
+    auto mesh = build_structured_cube(8, ctx);
+    auto iters = [&](double rho) {
+      auto sys = build_system(mesh, rho, Target::smooth);
+      AmgHierarchy h(sys.A);
+      auto r = pcg(sys.A, &h, sys.f(), 1e-8, 200);
+      CHECK(r.report.converged);
+      return r.report.iterations;
+    };
+    const int a = iters(1.0), b = iters(1e-12);
+    CHECK(a <= 30 && b <= 30 && b <= a + 2);
+  }
+  {  // BASELINE C1: n = 32, rho = h^2, smooth target, solve_system(amg)
+    auto mesh = build_structured_cube(32, ctx);
+    auto sys = build_system(mesh, 1.0 / 1024.0, Target::smooth);
+    auto out = solve_system_amg(sys, 1e-8);
+    CHECK(out.converged);
+    std::printf("C1 n=32: %d iterations, setup %.3f ms, solve %.3f ms\n", out.iterations, 1e3 * out.setup_seconds,
+                1e3 * out.solve_seconds);
+  }
+  std::printf("%d passed, %d failed\n", g_pass, g_fail);
+  return g_fail;
+}

@@ -59,3 +59,11 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".hpp", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert "pyoracle" not in txt and "rd_oracle.h" not in txt and "liboracle" not in txt, f
+
+
+def test_cpp_layer_builds():
+    """include/rd_gpu.hpp (the rd:: mirror a reference maintainer includes) compiles and links."""
+    import subprocess
+
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_2102_03515_b200"), "cpptest"], check=True)
+    assert os.path.exists(os.path.join(ROOT, "tests", "cpp", "test_rd_gpu"))
