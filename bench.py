@@ -276,6 +276,13 @@ def run_ours(args, rank, world, local_rank):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
+        if os.environ.get("RD_BENCH_VERBOSE"):
+            for _ in range(2):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                e2e_step()
+                torch.cuda.synchronize()
+                print(f"e2e step {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr, flush=True)
         e2e_its = [e2e_step() for _ in range(args.steps)]
         b.record(stream)
         torch.cuda.synchronize()
@@ -357,10 +364,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 and args.impl == "reference":
+        # the CPU reference arm runs on rank 0 alone; the other ranks exit without work
+        if rank != 0:
+            return
+    if world > 1 and args.impl == "ours":
         import torch
 
-        backend = "nccl" if (args.impl == "ours" and torch.cuda.is_available()) else "gloo"
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group(backend=backend)
@@ -370,7 +381,7 @@ def main():
         res = run_ours(args, rank, world, local_rank)
     if rank == 0 and res is not None:
         print(json.dumps(res), flush=True)
-    if world > 1:
+    if world > 1 and args.impl == "ours":
         import torch
 
         torch.distributed.destroy_process_group()

@@ -333,9 +333,16 @@ class FemSystem:
         self.mesh = mesh
         self.rho = rho
         self.n_dofs = lib().rd_gpu_system_n_dofs(h)
-        self.K = Csr(lib().rd_gpu_system_matrix(h, 0), ctx, owner=self, owned=False)
-        self.M = Csr(lib().rd_gpu_system_matrix(h, 1), ctx, owner=self, owned=False)
-        self.A = Csr(lib().rd_gpu_system_matrix(h, 2), ctx, owner=self, owned=False)
+
+    # K, M, A are views created on access: each holds the system alive, and the
+    # system holds no reference back (no cycle, so the device memory is released
+    # as soon as the last user drops it, not at the next cyclic GC).
+    def _view(self, which: int) -> Csr:
+        return Csr(lib().rd_gpu_system_matrix(self.h, which), self.ctx, owner=self, owned=False)
+
+    K = property(lambda self: self._view(0))
+    M = property(lambda self: self._view(1))
+    A = property(lambda self: self._view(2))
 
     @property
     def f_ptr(self) -> int:
