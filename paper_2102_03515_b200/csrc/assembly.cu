@@ -17,6 +17,7 @@
 // 4x-redundant row loop with a quarter of the quadrature work.
 #include <algorithm>
 #include <cmath>
+#include <utility>
 
 #include "internal.hpp"
 
@@ -33,6 +34,10 @@ struct Rules {
   double w14[14];
   double p64[64][4];
   double w64[64];
+  // element accumulators when the target is identically 1 on the tet: the
+  // integration loop below with u = 1 (w*1 = w), summed in the same order
+  double in14[4];
+  double in64[4];
 };
 __constant__ Rules c_rules;
 
@@ -89,6 +94,20 @@ Rules make_rules() {
   for (int k = 0; k < 64; ++k) {
     colmean(cells[k], r.p64[k]);
     r.w64[k] = 1.0 / 64.0;
+  }
+  // (x86-64 host code: no FMA contraction without -mfma)
+  for (int k = 0; k < 4; ++k) {
+    volatile double a14 = 0.0, a64 = 0.0;
+    for (int q = 0; q < 14; ++q) {
+      const volatile double prod = r.w14[q] * r.p14[q][k];
+      a14 = a14 + prod;
+    }
+    for (int q = 0; q < 64; ++q) {
+      const volatile double prod = r.w64[q] * r.p64[q][k];
+      a64 = a64 + prod;
+    }
+    r.in14[k] = a14;
+    r.in64[k] = a64;
   }
   return r;
 }
@@ -422,35 +441,8 @@ __global__ void split_count_kernel(int nd, const int* __restrict__ rp, const dou
   ac[r] = u;
 }
 
-__global__ void split_fill_kernel(int nd, double rho, const int* __restrict__ rp, const int* __restrict__ ci,
-                                  const double* __restrict__ Kf, const double* __restrict__ Mf,
-                                  const int* __restrict__ krp, int* kci, double* kv, const int* __restrict__ mrp,
-                                  int* mci, double* mv, const int* __restrict__ arp, int* aci, double* av) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= nd) return;
-  int ko = krp[r], mo = mrp[r], ao = arp[r];
-  for (int q = rp[r]; q < rp[r + 1]; ++q) {
-    const double kq = Kf[q], mq = Mf[q];
-    const bool k = kq != 0.0, m = mq != 0.0;
-    const int c = ci[q];
-    if (k) {
-      kci[ko] = c;
-      kv[ko++] = kq;
-    }
-    if (m) {
-      mci[mo] = c;
-      mv[mo++] = mq;
-    }
-    if (k || m) {
-      aci[ao] = c;
-      // Eigen union sum: both -> rho*K + M, K only -> rho*K + 0, M only -> 0 + M
-      av[ao++] = k && m ? __dadd_rn(__dmul_rn(rho, kq), mq) : (k ? __dadd_rn(__dmul_rn(rho, kq), 0.0) : __dadd_rn(0.0, mq));
-    }
-  }
-}
-
 // One thread per full-pattern entry (coalesced): rank among the row's kept
-// entries, then the same K / M / A values as split_fill_kernel.
+// entries, then K / M / A values as below (Eigen's union sum for A).
 __global__ void split_fill_entry_kernel(int64_t zf, int nd, double rho, const int* __restrict__ rp,
                                         const int* __restrict__ ci, const double* __restrict__ Kf,
                                         const double* __restrict__ Mf, const int* __restrict__ krp, int* kci,
@@ -489,6 +481,196 @@ __global__ void split_fill_entry_kernel(int64_t zf, int nd, double rho, const in
   aci[arp[r] + ar] = c;
   // Eigen union sum: both -> rho*K + M, K only -> rho*K + 0, M only -> 0 + M
   av[arp[r] + ar] = k && m ? __dadd_rn(__dmul_rn(rho, kq), mq) : (k ? __dadd_rn(__dmul_rn(rho, kq), 0.0) : __dadd_rn(0.0, mq));
+}
+
+// ---------------------------------------------------------------- Kuhn-lattice assembly
+// When the tets are exactly the build_structured_cube enumeration (mesh.cpp:29-65;
+// checked on the device for uploaded meshes), every interior vertex sees the same
+// 24 incident tets in the same ascending-id order and the same 15-point column
+// pattern, so the adjacency CSR, the column search and the slot search of the
+// generic path are compile-time constants.  Geometry still comes from the
+// vertex coordinates, operation for operation as local_geom; each row sums its
+// slots in ascending tet order exactly as the row loop of assembly.cpp:97-126.
+struct LatRowTet {
+  int o;        // corner of v in the cell: bits x | y<<1 | z<<2 (cell origin = v - o)
+  int p;        // Kuhn permutation (tet id = cell * 6 + p)
+  int iv;       // local index of v in the tet
+  int slot[4];  // stencil slot of local vertex jv
+  int dv[4];    // offset code of local vertex jv relative to v: (dx+1) + 3(dy+1) + 9(dz+1)
+};
+struct LatTab {
+  int sten[15];  // offset codes, sorted by vertex id (dz, dy, dx lexicographic)
+  LatRowTet t[24];
+};
+
+constexpr int kKuhnPerm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+
+constexpr LatTab make_lat_tab() {
+  LatTab T{};
+  int ns = 0;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        // edge directions of the Kuhn split are the 0/1 vectors: both signs all same
+        const bool nonneg = dx >= 0 && dy >= 0 && dz >= 0, nonpos = dx <= 0 && dy <= 0 && dz <= 0;
+        if (nonneg || nonpos) T.sten[ns++] = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
+      }
+  int nt = 0;
+  for (int o = 7; o >= 0; --o) {  // ascending cell id = descending corner code
+    const int ov[3] = {o & 1, (o >> 1) & 1, (o >> 2) & 1};
+    for (int p = 0; p < 6; ++p) {
+      int q[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {1, 1, 1}};
+      q[1][kKuhnPerm[p][0]] = 1;
+      q[2][kKuhnPerm[p][0]] = 1;
+      q[2][kKuhnPerm[p][1]] = 1;
+      int iv = -1;
+      for (int a = 0; a < 4; ++a)
+        if (q[a][0] == ov[0] && q[a][1] == ov[1] && q[a][2] == ov[2]) iv = a;
+      if (iv < 0) continue;
+      LatRowTet& e = T.t[nt++];
+      e.o = o;
+      e.p = p;
+      e.iv = iv;
+      for (int a = 0; a < 4; ++a) {
+        const int code = (q[a][0] - ov[0] + 1) + 3 * (q[a][1] - ov[1] + 1) + 9 * (q[a][2] - ov[2] + 1);
+        e.dv[a] = code;
+        for (int k = 0; k < 15; ++k)
+          if (T.sten[k] == code) e.slot[a] = k;
+      }
+    }
+  }
+  return T;
+}
+constexpr LatTab kLatTab = make_lat_tab();
+static_assert(kLatTab.t[23].o == 0 && kLatTab.t[23].p == 5, "24 incident tets per lattice vertex");
+__constant__ LatTab c_lat_tab = kLatTab;  // runtime-indexed copy
+
+__device__ __forceinline__ int lat_code_off(int code, int nv) {
+  return (code % 3 - 1) + (code / 3 % 3 - 1) * nv + (code / 9 - 1) * nv * nv;
+}
+
+template <int E>
+__device__ __forceinline__ void lat_row_tet(int v, int nv, const double* __restrict__ xyz, double* K, double* M,
+                                            bool& ok) {
+  constexpr LatRowTet T = kLatTab.t[E];
+  const int t0 = v + lat_code_off(T.dv[0], nv), t1 = v + lat_code_off(T.dv[1], nv),
+            t2 = v + lat_code_off(T.dv[2], nv), t3 = v + lat_code_off(T.dv[3], nv);
+  Geom G;
+  ok &= local_geom(xyz + 3 * (int64_t)t0, xyz + 3 * (int64_t)t1, xyz + 3 * (int64_t)t2, xyz + 3 * (int64_t)t3, G);
+  const double vm = __dmul_rn(1.0, G.vol);
+#pragma unroll
+  for (int jv = 0; jv < 4; ++jv) {
+    const int sl = T.slot[jv];
+    K[sl] = __dadd_rn(K[sl], __dadd_rn(0.0, __dmul_rn(vm, dot3(G.g[T.iv], G.g[jv]))));
+    M[sl] = __dadd_rn(M[sl], __dadd_rn(0.0, __dmul_rn(vm, T.iv == jv ? 0.1 : 0.05)));
+  }
+}
+
+template <int... E>
+__device__ __forceinline__ void lat_row_all(std::integer_sequence<int, E...>, int v, int nv, const double* xyz,
+                                            double* K, double* M, bool& ok) {
+  (lat_row_tet<E>(v, nv, xyz, K, M, ok), ...);
+}
+
+// Row r: 15 K and M slots (slot-major, padded [15][nd]), the interior-column
+// mask, and the pruned counts of K, M and A = K u M.
+constexpr int kLatNT = 128;
+__global__ void __launch_bounds__(kLatNT) lat_values_kernel(int nd, int n, const int* __restrict__ d2v,
+                                                           const int* __restrict__ v2d,
+                                                           const double* __restrict__ xyz, double* Kp, double* Mp,
+                                                           unsigned short* mask, int* kc, int* mc, int* ac,
+                                                           int* err) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nd) return;
+  const int nv = n + 1;
+  const int v = d2v[r];
+  const int i = v % nv, j = v / nv % nv, k = v / (nv * nv);
+  if (i == 0 || j == 0 || k == 0 || i == n || j == n || k == n) {  // dof on the cube's surface: generic path
+    atomicExch(err, -1);
+    return;
+  }
+  double K[15], M[15];
+#pragma unroll
+  for (int s = 0; s < 15; ++s) K[s] = M[s] = 0.0;
+  bool ok = true;
+  lat_row_all(std::make_integer_sequence<int, 24>{}, v, nv, xyz, K, M, ok);
+  if (!ok) atomicExch(err, RD_EDEGENERATE);
+  unsigned m = 0;
+  int a = 0, b = 0, u = 0;
+#pragma unroll
+  for (int s = 0; s < 15; ++s) {
+    if (v2d[v + lat_code_off(c_lat_tab.sten[s], nv)] < 0) continue;
+    m |= 1u << s;
+    const bool kk = K[s] != 0.0, mm = M[s] != 0.0;
+    a += kk;
+    b += mm;
+    u += (kk || mm);
+    Kp[(int64_t)s * nd + r] = K[s];
+    Mp[(int64_t)s * nd + r] = M[s];
+  }
+  mask[r] = (unsigned short)m;
+  kc[r] = a;
+  mc[r] = b;
+  ac[r] = u;
+}
+
+// Compacted K, M and A rows from the padded slots (split_fill_entry_kernel's
+// values; rows are contiguous, so a warp's stores cover one contiguous range).
+__global__ void __launch_bounds__(kLatNT) lat_split_kernel(int nd, int n, double rho, const int* __restrict__ d2v,
+                                                          const int* __restrict__ v2d,
+                                                          const double* __restrict__ Kp,
+                                                          const double* __restrict__ Mp,
+                                                          const unsigned short* __restrict__ mask,
+                                                          const int* __restrict__ krp, int* kci, double* kv,
+                                                          const int* __restrict__ mrp, int* mci, double* mv,
+                                                          const int* __restrict__ arp, int* aci, double* av) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nd) return;
+  const int nv = n + 1;
+  const int v = d2v[r];
+  const unsigned m = mask[r];
+  int ko = krp[r], mo = mrp[r], ao = arp[r];
+#pragma unroll
+  for (int s = 0; s < 15; ++s) {
+    if (!(m >> s & 1u)) continue;
+    const int c = v2d[v + lat_code_off(c_lat_tab.sten[s], nv)];
+    const double kq = Kp[(int64_t)s * nd + r], mq = Mp[(int64_t)s * nd + r];
+    const bool k = kq != 0.0, mm = mq != 0.0;
+    if (k) {
+      kci[ko] = c;
+      kv[ko++] = kq;
+    }
+    if (mm) {
+      mci[mo] = c;
+      mv[mo++] = mq;
+    }
+    if (k || mm) {
+      aci[ao] = c;
+      av[ao++] = k && mm ? __dadd_rn(__dmul_rn(rho, kq), mq)
+                         : (k ? __dadd_rn(__dmul_rn(rho, kq), 0.0) : __dadd_rn(0.0, mq));
+    }
+  }
+}
+
+// Does the tet array equal the build_structured_cube enumeration for n?
+__global__ void lattice_tets_check_kernel(int n, const int* __restrict__ tets, int* bad) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * n * n * 6) return;
+  const int nv = n + 1;
+  const int p = (int)(t % 6);
+  const int64_t cell = t / 6;
+  int c[3] = {(int)(cell % n), (int)((cell / n) % n), (int)(cell / ((int64_t)n * n))};
+  const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  int4 e;
+  e.x = (c[2] * nv + c[1]) * nv + c[0];
+  c[perms[p][0]] += 1;
+  e.y = (c[2] * nv + c[1]) * nv + c[0];
+  c[perms[p][1]] += 1;
+  e.z = (c[2] * nv + c[1]) * nv + c[0];
+  c[perms[p][2]] += 1;
+  e.w = (c[2] * nv + c[1]) * nv + c[0];
+  const int4 g = reinterpret_cast<const int4*>(tets)[t];
+  if (g.x != e.x || g.y != e.y || g.z != e.z || g.w != e.w) *bad = 1;
 }
 
 // ---------------------------------------------------------------- targets (target.cpp + BASELINE)
@@ -564,6 +746,53 @@ __global__ void random_nodal_kernel(int n, uint64_t seed, double* nodal) {
   nodal[v] = __dsub_rn(__dmul_rn(2.0, __dmul_rn((double)(z >> 11), 0x1.0p-53)), 1.0);
 }
 
+// +1: the tet lies strictly inside the support of an indicator target, -1:
+// strictly outside, 0: straddles (or the target is not an indicator).
+__device__ __forceinline__ int support_class(int kind, const double (&V)[4][3]) {
+  constexpr double eps = 1e-9;
+  if (kind == RD_TARGET_BALL) {
+    constexpr double rin = (0.25 - eps) * (0.25 - eps), rout = (0.25 + eps) * (0.25 + eps);
+    bool all_in = true;
+    double lo[3], hi[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) lo[c] = hi[c] = V[0][c];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double dx = V[k][0] - 0.5, dy = V[k][1] - 0.5, dz = V[k][2] - 0.5;
+      all_in &= dx * dx + dy * dy + dz * dz < rin;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        lo[c] = fmin(lo[c], V[k][c]);
+        hi[c] = fmax(hi[c], V[k][c]);
+      }
+    }
+    if (all_in) return 1;
+    double d2 = 0.0;  // squared distance from the centre to the bounding box
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double e = fmax(fmax(lo[c] - 0.5, 0.5 - hi[c]), 0.0);
+      d2 += e * e;
+    }
+    return d2 > rout ? -1 : 0;
+  }
+  if (kind == RD_TARGET_BOX) {
+    bool all_in = true, out = false;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double lo = V[0][c], hi = V[0][c];
+#pragma unroll
+      for (int k = 1; k < 4; ++k) {
+        lo = fmin(lo, V[k][c]);
+        hi = fmax(hi, V[k][c]);
+      }
+      all_in &= lo > 0.25 + eps && hi < 0.75 - eps;
+      out |= hi < 0.25 - eps || lo > 0.75 + eps;
+    }
+    return all_in ? 1 : (out ? -1 : 0);
+  }
+  return 0;
+}
+
 // per tet: vol (mesh.cpp:188-191 cross-product formula) and acc[iv] =
 // sum_q (w_q u(x_q)) lambda_q,iv for all four iv (assembly.cpp:152-171)
 template <int NQ>
@@ -591,6 +820,18 @@ __global__ void load_tet_kernel(int nt, const int* __restrict__ tets, const doub
   const double dt = __dadd_rn(__dadd_rn(__dmul_rn(x0, d[0]), __dmul_rn(x1, d[1])), __dmul_rn(x2, d[2]));
   tvol[t] = div_tail(fabs(dt), 6.0, div_recip(6.0));  // == __ddiv_rn(|dt|, 6.0)
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  // Indicator targets: a tet whose closed hull is (with a 1e-9 margin, far above
+  // the rounding of a quadrature point) entirely outside the support integrates
+  // u = 0 at every point (acc stays +0.0), entirely inside integrates u = 1
+  // (the rule's constant accumulators): skip the loop, same bits.
+  const int cls = support_class(kind, V);
+  if (cls != 0) {
+    const double* in = NQ == 14 ? c_rules.in14 : c_rules.in64;
+    const bool inside = cls > 0;
+    reinterpret_cast<double4*>(tacc)[t] = inside ? make_double4(in[0], in[1], in[2], in[3])
+                                                 : make_double4(0.0, 0.0, 0.0, 0.0);
+    return;
+  }
   for (int q = 0; q < NQ; ++q) {
     const double* lam = NQ == 14 ? c_rules.p14[q] : c_rules.p64[q];
     const double w = NQ == 14 ? c_rules.w14[q] : c_rules.w64[q];
@@ -625,6 +866,31 @@ __global__ void load_gather_kernel(int nd, const int* __restrict__ d2v, const in
   f[r] = s;
 }
 
+// load_gather_kernel on the lattice: the 24 incident tets by formula
+template <int E>
+__device__ __forceinline__ void lat_load_tet(int ci, int cj, int ck, int n, const double* __restrict__ tacc,
+                                             const double* __restrict__ tvol, double& s) {
+  constexpr LatRowTet T = kLatTab.t[E];
+  const int64_t cell = ((int64_t)(ck - (T.o >> 2 & 1)) * n + (cj - (T.o >> 1 & 1))) * n + (ci - (T.o & 1));
+  const int64_t t = cell * 6 + T.p;
+  s = __dadd_rn(s, __dmul_rn(tvol[t], tacc[4 * t + T.iv]));
+}
+template <int... E>
+__device__ __forceinline__ void lat_load_all(std::integer_sequence<int, E...>, int i, int j, int k, int n,
+                                             const double* tacc, const double* tvol, double& s) {
+  (lat_load_tet<E>(i, j, k, n, tacc, tvol, s), ...);
+}
+__global__ void lat_load_gather_kernel(int nd, int n, const int* __restrict__ d2v, const double* __restrict__ tacc,
+                                       const double* __restrict__ tvol, double* f) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nd) return;
+  const int nv = n + 1;
+  const int v = d2v[r];
+  double s = 0.0;
+  lat_load_all(std::make_integer_sequence<int, 24>{}, v % nv, v / nv % nv, v / (nv * nv), n, tacc, tvol, s);
+  f[r] = s;
+}
+
 int read_flag(Ctx& c, const int* d) {
   int h = 0;
   RDG_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -633,6 +899,19 @@ int read_flag(Ctx& c, const int* d) {
 }
 
 }  // namespace
+
+void detect_cube_lattice(Ctx& c, DMesh& m) {
+  m.lattice_n = -1;
+  if (m.nt < 6 || m.nt % 6) return;
+  const int n = (int)std::llround(std::cbrt((double)(m.nt / 6)));
+  if ((int64_t)6 * n * n * n != m.nt || (int64_t)(n + 1) * (n + 1) * (n + 1) != m.nv) return;
+  DBuf<int> bad(1, c.stream);
+  RDG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
+  lattice_tets_check_kernel<<<div_up(m.nt, 256), 256, 0, c.stream>>>(n, m.tets.p, bad.p);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+  if (read_flag(c, bad.p) == 0) m.lattice_n = n;
+}
 
 void build_structured_cube(Ctx& c, int n, DMesh& m) {
   if (n < 1) throw Error(RD_EINVAL, "build_structured_cube: n must be >= 1");
@@ -673,82 +952,117 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
   dofmap_kernel<<<div_up(nv, 256), 256, 0, c.stream>>>(nv, m.boundary.p, off.p, s.v2d.p, s.d2v.p);
   RDG_LAUNCH_CHECK();
   c.launches += 2;
-  // ---- vertex -> tet CSR, ascending tets (assembly.cpp:14-31)
-  DBuf<int> vcnt(nv + 1, c.stream), vto(nv + 1, c.stream), vt(std::max<int64_t>((int64_t)nt * 4, 1), c.stream);
-  RDG_CUDA(cudaMemsetAsync(vcnt.p, 0, sizeof(int) * (nv + 1), c.stream));
-  vt_count_kernel<<<div_up((int64_t)nt * 4, 256), 256, 0, c.stream>>>(nt, m.tets.p, vcnt.p);
-  RDG_LAUNCH_CHECK();
-  exclusive_scan(c, vcnt.p, vto.p, nv);
-  RDG_CUDA(cudaMemcpyAsync(vcnt.p, vto.p, sizeof(int) * nv, cudaMemcpyDeviceToDevice, c.stream));
-  vt_fill_kernel<<<div_up((int64_t)nt * 4, 256), 256, 0, c.stream>>>(nt, m.tets.p, vcnt.p, vt.p);
-  RDG_LAUNCH_CHECK();
-  sort_segments_kernel<<<div_up(nv, 256), 256, 0, c.stream>>>(nv, vto.p, vt.p);
-  RDG_LAUNCH_CHECK();
-  c.launches += 3;
-  // ---- pattern
-  DBuf<int> rcnt(std::max(nd, 1), c.stream), frp(nd + 1, c.stream);
-  if (nd) {
-    pattern_kernel<false><<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p,
-                                                                 rcnt.p, nullptr, nullptr, err.p);
-    RDG_LAUNCH_CHECK();
-    ++c.launches;
-  }
-  if (read_flag(c, err.p)) throw Error(RD_EINVAL, "assembly: row has more than 128 columns");
-  const int64_t zf = exclusive_scan(c, rcnt.p, frp.p, nd);
-  DBuf<int> fci(std::max<int64_t>(zf, 1), c.stream);
-  DBuf<double> Kf(std::max<int64_t>(zf, 1), c.stream), Mf(std::max<int64_t>(zf, 1), c.stream);
-  if (nd) {
-    pattern_kernel<true><<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p,
-                                                                nullptr, frp.p, fci.p, err.p);
-    RDG_LAUNCH_CHECK();
-    static bool qattr = false;
-    if (!qattr) {
-      RDG_CUDA(cudaFuncSetAttribute(values_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)sizeof(QuadContrib)));
-      qattr = true;
-    }
-    values_quad_kernel<<<div_up(nd, kQuadRows), 64, sizeof(QuadContrib), c.stream>>>(
-        nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p, m.xyz.p, frp.p, fci.p, Kf.p, Mf.p, err.p);
-    RDG_LAUNCH_CHECK();
-    if (read_flag(c, err.p) == -1) {  // some vertex has more incident tets than the quad kernel stages
-      RDG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.stream));
-      values_kernel<<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p, m.xyz.p,
-                                                           frp.p, fci.p, Kf.p, Mf.p, err.p);
-    }
-    RDG_LAUNCH_CHECK();
-    c.launches += 2;
-  }
-  if (read_flag(c, err.p)) throw Error(RD_EDEGENERATE, "assembly: degenerate tet");
-  // ---- prune K, M; A = rho*K + M (assembly.cpp:129,234)
-  DBuf<int> kc(std::max(nd, 1), c.stream), mc(std::max(nd, 1), c.stream), ac(std::max(nd, 1), c.stream);
-  if (nd) {
-    split_count_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, frp.p, Kf.p, Mf.p, kc.p, mc.p, ac.p);
-    RDG_LAUNCH_CHECK();
-    ++c.launches;
-  }
   DCsr* mats[3] = {&s.K, &s.M, &s.A};
-  int* cnts[3] = {kc.p, mc.p, ac.p};
-  for (int w = 0; w < 3; ++w) {
-    DCsr& X = *mats[w];
-    X = DCsr{};
-    X.rows = X.cols = nd;
-    X.rp.alloc(nd + 1, c.stream);
-    X.nnz = exclusive_scan(c, cnts[w], X.rp.p, nd);
-    X.ci.alloc(X.nnz, c.stream);
-    X.v.alloc(X.nnz, c.stream);
-  }
-  if (nd) {
-    split_fill_entry_kernel<<<div_up(zf, 256), 256, 0, c.stream>>>(zf, nd, rho, frp.p, fci.p, Kf.p, Mf.p, s.K.rp.p,
-                                                                   s.K.ci.p, s.K.v.p, s.M.rp.p, s.M.ci.p, s.M.v.p,
-                                                                   s.A.rp.p, s.A.ci.p, s.A.v.p);
+  auto alloc_split = [&](int* const* cnts) {
+    for (int w = 0; w < 3; ++w) {
+      DCsr& X = *mats[w];
+      X = DCsr{};
+      X.rows = X.cols = nd;
+      X.rp.alloc(nd + 1, c.stream);
+      X.nnz = exclusive_scan(c, cnts[w], X.rp.p, nd);
+      X.ci.alloc(X.nnz, c.stream);
+      X.v.alloc(X.nnz, c.stream);
+    }
+  };
+  // ---- Kuhn-lattice fast path (same sums, adjacency by formula)
+  const int n = m.lattice_n;
+  bool lattice = n >= 2 && (int64_t)nt == 6LL * n * n * n && (int64_t)nv == (int64_t)(n + 1) * (n + 1) * (n + 1) && nd > 0;
+  if (lattice) {
+    DBuf<double> Kp((size_t)15 * nd, c.stream), Mp((size_t)15 * nd, c.stream);
+    DBuf<unsigned short> mask(nd, c.stream);
+    DBuf<int> kc(nd, c.stream), mc(nd, c.stream), ac(nd, c.stream);
+    lat_values_kernel<<<div_up(nd, kLatNT), kLatNT, 0, c.stream>>>(nd, n, s.d2v.p, s.v2d.p, m.xyz.p, Kp.p, Mp.p,
+                                                                  mask.p, kc.p, mc.p, ac.p, err.p);
     RDG_LAUNCH_CHECK();
     ++c.launches;
+    const int e = read_flag(c, err.p);
+    if (e == RD_EDEGENERATE) throw Error(RD_EDEGENERATE, "assembly: degenerate tet");
+    if (e == 0) {
+      int* cnts[3] = {kc.p, mc.p, ac.p};
+      alloc_split(cnts);
+      lat_split_kernel<<<div_up(nd, kLatNT), kLatNT, 0, c.stream>>>(
+          nd, n, rho, s.d2v.p, s.v2d.p, Kp.p, Mp.p, mask.p, s.K.rp.p, s.K.ci.p, s.K.v.p, s.M.rp.p, s.M.ci.p,
+          s.M.v.p, s.A.rp.p, s.A.ci.p, s.A.v.p);
+      RDG_LAUNCH_CHECK();
+      ++c.launches;
+    } else {  // a dof on the cube's surface (custom boundary flags): generic path
+      RDG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.stream));
+      lattice = false;
+    }
+  }
+  // ---- vertex -> tet CSR, ascending tets (assembly.cpp:14-31)
+  DBuf<int> vto, vt;
+  if (!lattice) {
+    DBuf<int> vcnt(nv + 1, c.stream);
+    vto.alloc(nv + 1, c.stream);
+    vt.alloc(std::max<int64_t>((int64_t)nt * 4, 1), c.stream);
+    RDG_CUDA(cudaMemsetAsync(vcnt.p, 0, sizeof(int) * (nv + 1), c.stream));
+    vt_count_kernel<<<div_up((int64_t)nt * 4, 256), 256, 0, c.stream>>>(nt, m.tets.p, vcnt.p);
+    RDG_LAUNCH_CHECK();
+    exclusive_scan(c, vcnt.p, vto.p, nv);
+    RDG_CUDA(cudaMemcpyAsync(vcnt.p, vto.p, sizeof(int) * nv, cudaMemcpyDeviceToDevice, c.stream));
+    vt_fill_kernel<<<div_up((int64_t)nt * 4, 256), 256, 0, c.stream>>>(nt, m.tets.p, vcnt.p, vt.p);
+    RDG_LAUNCH_CHECK();
+    sort_segments_kernel<<<div_up(nv, 256), 256, 0, c.stream>>>(nv, vto.p, vt.p);
+    RDG_LAUNCH_CHECK();
+    c.launches += 3;
+  }
+  if (!lattice) {
+    // ---- pattern
+    DBuf<int> rcnt(std::max(nd, 1), c.stream), frp(nd + 1, c.stream);
+    if (nd) {
+      pattern_kernel<false><<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p,
+                                                                   rcnt.p, nullptr, nullptr, err.p);
+      RDG_LAUNCH_CHECK();
+      ++c.launches;
+    }
+    if (read_flag(c, err.p)) throw Error(RD_EINVAL, "assembly: row has more than 128 columns");
+    const int64_t zf = exclusive_scan(c, rcnt.p, frp.p, nd);
+    DBuf<int> fci(std::max<int64_t>(zf, 1), c.stream);
+    DBuf<double> Kf(std::max<int64_t>(zf, 1), c.stream), Mf(std::max<int64_t>(zf, 1), c.stream);
+    if (nd) {
+      pattern_kernel<true><<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p,
+                                                                  nullptr, frp.p, fci.p, err.p);
+      RDG_LAUNCH_CHECK();
+      static bool qattr = false;
+      if (!qattr) {
+        RDG_CUDA(cudaFuncSetAttribute(values_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(QuadContrib)));
+        qattr = true;
+      }
+      values_quad_kernel<<<div_up(nd, kQuadRows), 64, sizeof(QuadContrib), c.stream>>>(
+          nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p, m.xyz.p, frp.p, fci.p, Kf.p, Mf.p, err.p);
+      RDG_LAUNCH_CHECK();
+      if (read_flag(c, err.p) == -1) {  // some vertex has more incident tets than the quad kernel stages
+        RDG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.stream));
+        values_kernel<<<div_up(nd, 128), 128, 0, c.stream>>>(nd, s.d2v.p, s.v2d.p, vto.p, vt.p, m.tets.p, m.xyz.p,
+                                                             frp.p, fci.p, Kf.p, Mf.p, err.p);
+      }
+      RDG_LAUNCH_CHECK();
+      c.launches += 2;
+    }
+    if (read_flag(c, err.p)) throw Error(RD_EDEGENERATE, "assembly: degenerate tet");
+    // ---- prune K, M; A = rho*K + M (assembly.cpp:129,234)
+    DBuf<int> kc(std::max(nd, 1), c.stream), mc(std::max(nd, 1), c.stream), ac(std::max(nd, 1), c.stream);
+    if (nd) {
+      split_count_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, frp.p, Kf.p, Mf.p, kc.p, mc.p, ac.p);
+      RDG_LAUNCH_CHECK();
+      ++c.launches;
+    }
+    int* cnts[3] = {kc.p, mc.p, ac.p};
+    alloc_split(cnts);
+    if (nd) {
+      split_fill_entry_kernel<<<div_up(zf, 256), 256, 0, c.stream>>>(zf, nd, rho, frp.p, fci.p, Kf.p, Mf.p, s.K.rp.p,
+                                                                     s.K.ci.p, s.K.v.p, s.M.rp.p, s.M.ci.p, s.M.v.p,
+                                                                     s.A.rp.p, s.A.ci.p, s.A.v.p);
+      RDG_LAUNCH_CHECK();
+      ++c.launches;
+    }
   }
   // ---- load vector (assembly.cpp:140-174)
   s.f.alloc(std::max(nd, 1), c.stream);
   if (nd) {
     DBuf<double> nodal;
-    const int n = m.lattice_n;
     if (kind == RD_TARGET_SINE_RANDOM) {
       nodal.alloc(nv, c.stream);
       random_nodal_kernel<<<div_up(nv, 256), 256, 0, c.stream>>>(n, seed, nodal.p);
@@ -764,8 +1078,11 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
       load_tet_kernel<14><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, kind, nodal.p, n, tacc.p,
                                                                  tvol.p);
     RDG_LAUNCH_CHECK();
-    load_gather_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, s.d2v.p, vto.p, vt.p, m.tets.p, tacc.p, tvol.p,
-                                                              s.f.p);
+    if (lattice)
+      lat_load_gather_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, n, s.d2v.p, tacc.p, tvol.p, s.f.p);
+    else
+      load_gather_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, s.d2v.p, vto.p, vt.p, m.tets.p, tacc.p,
+                                                                tvol.p, s.f.p);
     RDG_LAUNCH_CHECK();
     c.launches += 2;
   }

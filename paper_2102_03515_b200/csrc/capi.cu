@@ -179,7 +179,7 @@ int rd_gpu_mesh_create(rd_ctx* ctx, int nv, const double* xyz, int nt, const int
     if (nv) RDG_CUDA(cudaMemcpyAsync(m->m.xyz.p, xyz, sizeof(double) * 3 * nv, k, c.stream));
     if (nt) RDG_CUDA(cudaMemcpyAsync(m->m.tets.p, tets, sizeof(int) * 4 * nt, k, c.stream));
     if (nv) RDG_CUDA(cudaMemcpyAsync(m->m.boundary.p, bnd, nv, k, c.stream));
-    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    detect_cube_lattice(c, m->m);  // synchronises
     *out = m.release();
   });
 }

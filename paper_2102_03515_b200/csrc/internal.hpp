@@ -115,6 +115,8 @@ struct DSystem {
 };
 
 void build_structured_cube(Ctx& c, int n, DMesh& m);
+// sets m.lattice_n when the tets are exactly the build_structured_cube enumeration
+void detect_cube_lattice(Ctx& c, DMesh& m);
 void build_system(Ctx& c, const DMesh& m, double rho, int target_kind, uint64_t seed, DSystem& s);
 
 }  // namespace rdg

@@ -73,6 +73,59 @@ def test_build_system_c2_pattern_n32(rd, O):
     assert np.array_equal(ds.f(), os_.f)
 
 
+def _sys_equal(ds, os_, exact_f=True):
+    assert_csr_equal(ds.K, os_.K, "K")
+    assert_csr_equal(ds.M, os_.M, "M")
+    assert_csr_equal(ds.A, os_.A, "A")
+    f = ds.f()
+    if exact_f:
+        assert np.array_equal(f, os_.f), np.abs(f - os_.f).max()
+    else:
+        assert np.abs(f - os_.f).max() <= 1e-15 * np.abs(os_.f).max() + 1e-300
+
+
+@pytest.mark.parametrize("target", ["ball", "smooth"])
+def test_uploaded_mesh_lattice_and_generic_paths(rd, O, target):
+    """The Kuhn-lattice assembly (adjacency by formula) and the generic one
+    (vertex->tet CSR, searched pattern) against the oracle on the same arrays."""
+    n, rho = 8, 1.0 / 64
+    exact = target == "ball"
+    xyz, tets, b = rd.build_structured_cube(n).download()
+    # (a) the cube as host arrays: detected as a lattice
+    dm = rd.mesh_from_arrays(xyz, tets, b)
+    assert dm.lattice_n == n
+    _sys_equal(rd.build_system(dm, rho, target), O.build_system(O.mesh_from_arrays(xyz, tets, b), rho, target), exact)
+    # (b) jittered interior coordinates: still a lattice, non-uniform geometry
+    rng = np.random.default_rng(5)
+    xj = xyz.copy()
+    xj[b == 0] += rng.uniform(-0.2, 0.2, size=(int((b == 0).sum()), 3)) / n
+    dm = rd.mesh_from_arrays(xj, tets, b)
+    assert dm.lattice_n == n
+    _sys_equal(rd.build_system(dm, rho, target), O.build_system(O.mesh_from_arrays(xj, tets, b), rho, target), exact)
+    # (c) shuffled tet order: not the enumeration -> generic path
+    perm = rng.permutation(tets.shape[0])
+    ts = np.ascontiguousarray(tets[perm])
+    dm = rd.mesh_from_arrays(xyz, ts, b)
+    assert dm.lattice_n == -1
+    _sys_equal(rd.build_system(dm, rho, target), O.build_system(O.mesh_from_arrays(xyz, ts, b), rho, target), exact)
+    # (d) a surface vertex flagged interior: lattice mesh, generic fallback
+    bb = b.copy()
+    bb[(n + 1) * (n + 1) * (n // 2) + (n + 1) * (n // 2)] = 0  # x = 0 face, centre
+    dm = rd.mesh_from_arrays(xyz, tets, bb)
+    assert dm.lattice_n == n
+    _sys_equal(rd.build_system(dm, rho, target), O.build_system(O.mesh_from_arrays(xyz, tets, bb), rho, target), exact)
+
+
+@pytest.mark.parametrize("n", [30, 32])
+def test_indicator_support_culling(rd, O, n):
+    """Box and ball loads skip the quadrature loop on tets strictly inside or
+    outside the support; the box faces lie on lattice planes when 4 | n."""
+    for target in ("box", "ball"):
+        ds = rd.build_system(rd.build_structured_cube(n), 1.0 / (n * n), target)
+        os_ = O.build_system(O.build_structured_cube(n), 1.0 / (n * n), target)
+        assert np.array_equal(ds.f(), os_.f), target
+
+
 def test_build_system_rejects_rho(rd):
     with pytest.raises(ValueError):
         rd.build_system(rd.build_structured_cube(2), 0.0, "smooth")
