@@ -174,6 +174,118 @@ __global__ void __launch_bounds__(kCoarseNT) llt_solve_kernel(int n, const doubl
   for (int i = threadIdx.x; i < n; i += kCoarseNT) x[i] = sh[i];
 }
 
+// ---------------------------------------------------------------- lattice levels
+// On a verified 15-point in-box lattice stencil the greedy MIS is the set of
+// all-even points (every odd point p sees p - e_S, S = its odd axes, as a lower
+// neighbour; every even point's lower neighbours are odd), and every F point has
+// a C neighbour, so the guard never fires.
+__global__ void lat_flags_kernel(int n, int L, int* state) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int x = i % L, y = i / L % L, z = i / (L * L);
+  state[i] = ((x | y | z) & 1) ? kFine : kCoarse;
+}
+
+// Galerkin product on lattice levels.  Eigen's ordered product gives entry
+// (i, j) of A*B as the in-order sum over ascending k of A_ik * B_kj (first
+// term assigned); here each row accumulates into a dense 3x3x3 window of coarse
+// columns around its own position, in exactly that order, instead of searching
+// a first-touch list.  Terms of absent entries are never added; a window slot
+// that only ever receives exact zeros differs at most in the sign of zero, and
+// every zero is pruned from A_c.  A column outside the window (not a lattice
+// coarsening) raises the flag and the generic product runs instead.
+constexpr int kGalNT = 128;
+
+__global__ void __launch_bounds__(kGalNT) lat_ap_kernel(int nf, int L, int Lc, const int* __restrict__ arp,
+                                                        const int* __restrict__ aci, const double* __restrict__ av,
+                                                        const int* __restrict__ prp, const int* __restrict__ pci,
+                                                        const double* __restrict__ pv, double* ap, int* err) {
+  __shared__ double W[27][kGalNT];
+  const int t = threadIdx.x;
+  const int k = blockIdx.x * kGalNT + t;
+  if (k >= nf) return;
+#pragma unroll
+  for (int s = 0; s < 27; ++s) W[s][t] = 0.0;
+  const int x = k % L, y = k / L % L, z = k / (L * L);
+  const int bx = (x - 1) >> 1, by = (y - 1) >> 1, bz = (z - 1) >> 1;
+  bool bad = false;
+  for (int ka = arp[k]; ka < arp[k + 1]; ++ka) {
+    const int m = aci[ka];
+    const double a = av[ka];
+    for (int kb = prp[m]; kb < prp[m + 1]; ++kb) {
+      const int J = pci[kb];
+      const int dx = J % Lc - bx, dy = J / Lc % Lc - by, dz = J / (Lc * Lc) - bz;
+      if ((unsigned)dx > 2u || (unsigned)dy > 2u || (unsigned)dz > 2u) {
+        bad = true;
+        continue;
+      }
+      double& w = W[dz * 9 + dy * 3 + dx][t];
+      w = __dadd_rn(w, __dmul_rn(pv[kb], a));
+    }
+  }
+  if (bad) atomicExch(err, 1);
+#pragma unroll
+  for (int s = 0; s < 27; ++s) ap[(size_t)s * nf + k] = W[s][t];
+}
+
+__global__ void __launch_bounds__(kGalNT) lat_ptap_kernel(int nc, int Lc, int nf, int L,
+                                                          const int* __restrict__ trp, const int* __restrict__ tci,
+                                                          const double* __restrict__ tv,
+                                                          const double* __restrict__ ap, double* out, int* cnt,
+                                                          int* err) {
+  __shared__ double W[27][kGalNT];
+  const int t = threadIdx.x;
+  const int I = blockIdx.x * kGalNT + t;
+  if (I >= nc) return;
+#pragma unroll
+  for (int s = 0; s < 27; ++s) W[s][t] = 0.0;
+  const int cx = I % Lc - 1, cy = I / Lc % Lc - 1, cz = I / (Lc * Lc) - 1;  // window origin
+  bool bad = false;
+  for (int kt = trp[I]; kt < trp[I + 1]; ++kt) {
+    const int k = tci[kt];
+    const double pw = tv[kt];
+    const int x = k % L, y = k / L % L, z = k / (L * L);
+    const int ox = ((x - 1) >> 1) - cx, oy = ((y - 1) >> 1) - cy, oz = ((z - 1) >> 1) - cz;
+#pragma unroll 3
+    for (int s = 0; s < 27; ++s) {
+      const double v = ap[(size_t)s * nf + k];
+      if (v == 0.0) continue;
+      const int dx = ox + s % 3, dy = oy + s / 3 % 3, dz = oz + s / 9;
+      if ((unsigned)dx > 2u || (unsigned)dy > 2u || (unsigned)dz > 2u) {
+        bad = true;
+        continue;
+      }
+      double& w = W[dz * 9 + dy * 3 + dx][t];
+      w = __dadd_rn(w, __dmul_rn(v, pw));
+    }
+  }
+  if (bad) atomicExch(err, 1);
+  int c = 0;
+#pragma unroll
+  for (int s = 0; s < 27; ++s) {
+    const double w = W[s][t];
+    c += w != 0.0;
+    out[(size_t)s * nc + I] = w;
+  }
+  cnt[I] = c;
+}
+
+__global__ void lat_compact_kernel(int nc, int Lc, const double* __restrict__ out, const int* __restrict__ rp,
+                                   int* ci, double* v) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= nc) return;
+  const int cx = I % Lc - 1, cy = I / Lc % Lc - 1, cz = I / (Lc * Lc) - 1;
+  int o = rp[I];
+#pragma unroll
+  for (int s = 0; s < 27; ++s) {
+    const double w = out[(size_t)s * nc + I];
+    if (w != 0.0) {
+      ci[o] = ((cz + s / 9) * Lc + (cy + s / 3 % 3)) * Lc + (cx + s % 3);
+      v[o++] = w;
+    }
+  }
+}
+
 int read_int(Ctx& c, const int* d) {
   int h = 0;
   RDG_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -196,19 +308,25 @@ std::vector<uint8_t> coarsen(Ctx& c, const DCsr& A, DBuf<uint8_t>& flags, DCsr& 
   DBuf<int> state(n, c.stream), tmp(n + 1, c.stream), cidx(n + 1, c.stream), scratch(4, c.stream);
   RDG_CUDA(cudaMemsetAsync(state.p, 0, sizeof(int) * n, c.stream));
   RDG_CUDA(cudaMemsetAsync(scratch.p, 0, sizeof(int) * 4, c.stream));
-  DCsr At;
-  const bool sym = pattern_symmetric(c, A);
-  if (!sym) At = transpose(c, A);
-  const DCsr& G = sym ? A : At;
-  mis_kernel<<<div_up(n, kMisNT), kMisNT, 0, c.stream>>>(n, G.rp.p, G.ci.p, state.p, scratch.p);
-  RDG_LAUNCH_CHECK();
-  guard_count_kernel<<<div_up(n, 256), 256, 0, c.stream>>>(n, A.rp.p, A.ci.p, state.p, scratch.p + 1);
-  RDG_LAUNCH_CHECK();
-  c.launches += 2;
-  if (read_int(c, scratch.p + 1) > 0) {
-    guard_serial_kernel<<<1, 1, 0, c.stream>>>(n, A.rp.p, A.ci.p, state.p);
+  if (A.lat.ok && A.lat.lx == A.lat.ly && A.lat.ly == A.lat.lz) {
+    lat_flags_kernel<<<div_up(n, 256), 256, 0, c.stream>>>(n, A.lat.lx, state.p);
     RDG_LAUNCH_CHECK();
     ++c.launches;
+  } else {
+    DCsr At;
+    const bool sym = pattern_symmetric(c, A);
+    if (!sym) At = transpose(c, A);
+    const DCsr& G = sym ? A : At;
+    mis_kernel<<<div_up(n, kMisNT), kMisNT, 0, c.stream>>>(n, G.rp.p, G.ci.p, state.p, scratch.p);
+    RDG_LAUNCH_CHECK();
+    guard_count_kernel<<<div_up(n, 256), 256, 0, c.stream>>>(n, A.rp.p, A.ci.p, state.p, scratch.p + 1);
+    RDG_LAUNCH_CHECK();
+    c.launches += 2;
+    if (read_int(c, scratch.p + 1) > 0) {
+      guard_serial_kernel<<<1, 1, 0, c.stream>>>(n, A.rp.p, A.ci.p, state.p);
+      RDG_LAUNCH_CHECK();
+      ++c.launches;
+    }
   }
   coarse_flags_kernel<<<div_up(n, 256), 256, 0, c.stream>>>(n, state.p, tmp.p, flags.p);
   RDG_LAUNCH_CHECK();
@@ -226,8 +344,44 @@ std::vector<uint8_t> coarsen(Ctx& c, const DCsr& A, DBuf<uint8_t>& flags, DCsr& 
   return {};  // flags stay on the device (rd_gpu_coarsen_redblack downloads them)
 }
 
+// Lattice-level Galerkin product (see lat_ap_kernel); false: not applicable.
+static bool galerkin_lattice(Ctx& c, const DCsr& A, const DCsr& P, const DCsr& Pt, DCsr& Ac) {
+  if (!A.lat.ok || A.lat.lx != A.lat.ly || A.lat.ly != A.lat.lz) return false;
+  const int L = A.lat.lx, Lc = (L + 1) / 2;
+  const int nf = A.rows, nc = P.cols;
+  if ((int64_t)Lc * Lc * Lc != nc || nc == 0 || Pt.rows != nc) return false;
+  DBuf<int> err(1, c.stream), cnt(nc, c.stream);
+  RDG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.stream));
+  DBuf<double> out((size_t)27 * nc, c.stream);
+  {
+    DBuf<double> ap((size_t)27 * nf, c.stream);
+    lat_ap_kernel<<<div_up(nf, kGalNT), kGalNT, 0, c.stream>>>(nf, L, Lc, A.rp.p, A.ci.p, A.v.p, P.rp.p, P.ci.p,
+                                                               P.v.p, ap.p, err.p);
+    RDG_LAUNCH_CHECK();
+    lat_ptap_kernel<<<div_up(nc, kGalNT), kGalNT, 0, c.stream>>>(nc, Lc, nf, L, Pt.rp.p, Pt.ci.p, Pt.v.p, ap.p,
+                                                                 out.p, cnt.p, err.p);
+    RDG_LAUNCH_CHECK();
+    c.launches += 2;
+  }
+  if (read_int(c, err.p)) return false;
+  Ac = DCsr{};
+  Ac.rows = Ac.cols = nc;
+  Ac.rp.alloc(nc + 1, c.stream);
+  Ac.nnz = exclusive_scan(c, cnt.p, Ac.rp.p, nc);
+  Ac.ci.alloc(Ac.nnz, c.stream);
+  Ac.v.alloc(Ac.nnz, c.stream);
+  lat_compact_kernel<<<div_up(nc, 256), 256, 0, c.stream>>>(nc, Lc, out.p, Ac.rp.p, Ac.ci.p, Ac.v.p);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+  return true;
+}
+
 DCsr galerkin(Ctx& c, const DCsr& A, const DCsr& P, const DCsr& Pt) {
   if (A.cols != P.rows) throw Error(RD_EINVAL, "galerkin_coarse: dims");
+  {
+    DCsr Ac;
+    if (galerkin_lattice(c, A, P, Pt, Ac)) return Ac;
+  }
   DCsr AP = spgemm(c, A, P);
   DCsr Ac = spgemm(c, Pt, AP);
   return prune_zeros(c, Ac);
@@ -254,6 +408,7 @@ void build_hierarchy(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h) 
   while (current.rows > threshold) {
     Level lv;
     lv.A = std::move(current);
+    detect_lattice(c, lv.A);  // lattice levels: closed-form C/F split and windowed Galerkin
     DCsr P;
     coarsen(c, lv.A, lv.flags, P);
     if (P.cols >= P.rows) {  // no reduction possible (amg.cpp:98-101)

@@ -24,6 +24,7 @@ struct DCsr {
   DBuf<int> rp, ci;
   DBuf<double> v;
   Lattice lat;
+  bool lat_checked = false;  // detect_lattice ran on the current pattern
   // generic (sync-free) Gauss-Seidel readiness flags, epoch-stamped so they
   // never need clearing between sweeps
   mutable DBuf<unsigned> gs_flags;

@@ -574,6 +574,8 @@ bool pattern_symmetric(Ctx& c, const DCsr& A) {
 }
 
 void detect_lattice(Ctx& c, DCsr& A) {
+  if (A.lat_checked) return;
+  A.lat_checked = true;
   A.lat = Lattice{};
   if (A.rows != A.cols || A.rows < 8) return;
   int L = (int)std::llround(std::cbrt((double)A.rows));

@@ -294,6 +294,26 @@ def test_hierarchy_bit_exact(rd, O, n, thr):
             assert_csr_equal(dh.level(l, "Pt"), oh.level(l, "Pt"), f"Pt_{l}")
 
 
+@pytest.mark.parametrize("n,jitter", [(16, 0.0), (16, 0.2), (24, 0.2), (13, 0.0), (64, 0.0)])
+def test_hierarchy_lattice_levels(rd, O, n, jitter):
+    """Lattice levels take the closed-form C/F split and the windowed Galerkin
+    product; non-uniform geometry (jitter) and odd level sizes included."""
+    xyz, tets, b = O.build_structured_cube(n).xyz, O.build_structured_cube(n).tets, O.build_structured_cube(n).boundary
+    if jitter:
+        rng = np.random.default_rng(11)
+        xyz = xyz.copy()
+        xyz[b == 0] += rng.uniform(-jitter, jitter, size=(int((b == 0).sum()), 3)) / n
+    os_ = O.build_system(O.mesh_from_arrays(xyz, tets, b), 1.0 / (n * n), "ball")
+    oh = O.build_amg(os_.A, 64)
+    dh = rd.build_amg(to_dev(rd, os_.A), 64)
+    assert dh.num_levels == oh.num_levels
+    for l in range(oh.num_levels):
+        assert_csr_equal(dh.level(l), oh.level(l), f"A_{l}")
+        if l + 1 < oh.num_levels:
+            assert np.array_equal(dh.flags(l), oh.flags(l))
+            assert_csr_equal(dh.level(l, "P"), oh.level(l, "P"), f"P_{l}")
+
+
 @pytest.mark.parametrize("n,thr", [(3, 1000), (4, 16), (16, 64), (32, 64)])
 def test_amg_apply_bit_exact(rd, O, n, thr):
     os_ = O.build_system(O.build_structured_cube(n), 1e-4, "smooth")

@@ -1,4 +1,7 @@
-"""Sub-step cycle breakdown of the lattice GS kernel (tile 0, thread 0): RD_GS_CTRACE."""
+"""Sub-step cycle breakdown of the lattice GS kernel (one tile's thread 0): RD_GS_CTRACE.
+
+usage: python tools/gs_ctrace.py [n] [tile]   (tile -1 = the middle tile)
+"""
 import os
 import sys
 
@@ -9,6 +12,7 @@ path = "gpurun_out/ctrace.txt"
 if os.path.exists(path):
     os.remove(path)
 os.environ["RD_GS_CTRACE"] = path
+os.environ["RD_GS_CTRACE_TILE"] = sys.argv[2] if len(sys.argv) > 2 else "0"
 import torch  # noqa: E402
 
 from paper_2102_03515_b200 import rd  # noqa: E402
@@ -25,12 +29,13 @@ for l in range(h.num_levels - 1):
         h.level_sweep(l, True, f, x, y)
 h.ctx.synchronize()
 lines = open(path).read().splitlines()
-names = ["halo+mbar wait", "stage C", "stage B", "stage A", "barrier", "->next"]
+names = ["halo wait", "loads+C", "B", "waits", "-", "barrier", "->next"]
 for i in range(0, len(lines), 2):
-    L = int(lines[i].split()[1])
-    v = np.array([int(t) for t in lines[i + 1].split()], dtype=np.int64).reshape(-1, 6)
+    hdr = lines[i].split()
+    v = np.array([int(t) for t in lines[i + 1].split()], dtype=np.int64).reshape(-1, 8)[:, :7]
     v = v[5:-5]  # steady state
-    d = np.diff(np.concatenate([v, np.roll(v[:, :1], -1, axis=0)], axis=1), axis=1)[:-1]
+    nxt = np.roll(v[:, :1], -1, axis=0)
+    d = np.diff(np.concatenate([v, nxt], axis=1), axis=1)[:-1]
     med = np.median(d, axis=0)
-    print(f"L={L}: cycles/step median {np.median(np.diff(v[:, 0])):.0f}: " +
-          ", ".join(f"{nm} {m:.0f}" for nm, m in zip(names, med)))
+    print(f"L={hdr[1]} tile {hdr[5]} warp {hdr[7]}: cycles/step median {np.median(np.diff(v[:, 0])):.0f}: " +
+          ", ".join(f"{nm} {m:.0f}" for nm, m in zip(names, med)), flush=True)
