@@ -615,7 +615,9 @@ __global__ void __launch_bounds__(kLatNT) lat_values_kernel(int nd, int n, const
 }
 
 // Compacted K, M and A rows from the padded slots (split_fill_entry_kernel's
-// values; rows are contiguous, so a warp's stores cover one contiguous range).
+// values).  A warp's 32 rows are contiguous in each output CSR, so every lane
+// first places its row in a shared-memory staging area and the warp then
+// writes the range with coalesced stores.
 __global__ void __launch_bounds__(kLatNT) lat_split_kernel(int nd, int n, double rho, const int* __restrict__ d2v,
                                                           const int* __restrict__ v2d,
                                                           const double* __restrict__ Kp,
@@ -624,32 +626,56 @@ __global__ void __launch_bounds__(kLatNT) lat_split_kernel(int nd, int n, double
                                                           const int* __restrict__ krp, int* kci, double* kv,
                                                           const int* __restrict__ mrp, int* mci, double* mv,
                                                           const int* __restrict__ arp, int* aci, double* av) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= nd) return;
+  __shared__ int scol[kLatNT / 32][32 * 15];
+  __shared__ double sval[kLatNT / 32][32 * 15];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int r0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31;
+  if (r0 >= nd) return;
+  const int r = r0 + lane;
+  const bool row = r < nd;
+  const int rend = min(r0 + 32, nd);
   const int nv = n + 1;
-  const int v = d2v[r];
-  const unsigned m = mask[r];
-  int ko = krp[r], mo = mrp[r], ao = arp[r];
+  const int v = row ? d2v[r] : 0;
+  const unsigned m = row ? mask[r] : 0u;
+  int col[15];
+  double kq[15], mq[15];
 #pragma unroll
   for (int s = 0; s < 15; ++s) {
-    if (!(m >> s & 1u)) continue;
-    const int c = v2d[v + lat_code_off(c_lat_tab.sten[s], nv)];
-    const double kq = Kp[(int64_t)s * nd + r], mq = Mp[(int64_t)s * nd + r];
-    const bool k = kq != 0.0, mm = mq != 0.0;
-    if (k) {
-      kci[ko] = c;
-      kv[ko++] = kq;
-    }
-    if (mm) {
-      mci[mo] = c;
-      mv[mo++] = mq;
-    }
-    if (k || mm) {
-      aci[ao] = c;
-      av[ao++] = k && mm ? __dadd_rn(__dmul_rn(rho, kq), mq)
-                         : (k ? __dadd_rn(__dmul_rn(rho, kq), 0.0) : __dadd_rn(0.0, mq));
-    }
+    const bool on = (m >> s) & 1u;
+    col[s] = on ? v2d[v + lat_code_off(c_lat_tab.sten[s], nv)] : 0;
+    kq[s] = on ? Kp[(int64_t)s * nd + r] : 0.0;
+    mq[s] = on ? Mp[(int64_t)s * nd + r] : 0.0;
   }
+  int* sc = scol[wq];
+  double* sv = sval[wq];
+  auto emit = [&](const int* __restrict__ xrp, int* xci, double* xv, int which) {
+    const int base = xrp[r0];
+    int o = row ? xrp[r] - base : 0;
+#pragma unroll
+    for (int s = 0; s < 15; ++s) {
+      const bool k = kq[s] != 0.0, mm = mq[s] != 0.0;
+      const bool keep = which == 0 ? k : (which == 1 ? mm : (k || mm));
+      if (keep) {
+        sc[o] = col[s];
+        sv[o] = which == 0 ? kq[s]
+                           : (which == 1 ? mq[s]
+                                         : (k && mm ? __dadd_rn(__dmul_rn(rho, kq[s]), mq[s])
+                                                    : (k ? __dadd_rn(__dmul_rn(rho, kq[s]), 0.0)
+                                                         : __dadd_rn(0.0, mq[s]))));
+        ++o;
+      }
+    }
+    __syncwarp();
+    const int cnt = xrp[rend] - base;
+    for (int e = lane; e < cnt; e += 32) {
+      xci[base + e] = sc[e];
+      xv[base + e] = sv[e];
+    }
+    __syncwarp();
+  };
+  emit(krp, kci, kv, 0);
+  emit(mrp, mci, mv, 1);
+  emit(arp, aci, av, 2);
 }
 
 // Does the tet array equal the build_structured_cube enumeration for n?
