@@ -83,6 +83,29 @@ void sync_and_raise(Ctx& c) {
   if (e) throw Error(e, "device error");
 }
 
+// Lattice sweeps speculate on the division fast path; when the device flags a
+// miss (possibly behind an error it caused, e.g. a spurious p'Ap <= 0), the
+// whole call is rerun with exact sweeps.  Calls are functional (outputs never
+// alias inputs), so a rerun reproduces the exact result.
+template <class F>
+void exact_retry(Ctx& c, F&& body) {
+  try {
+    body();
+  } catch (const Error& e) {
+    if (c.gs_exact) throw;
+    const int dev = e.code == kErrSpeculation ? kErrSpeculation : take_device_error(c);
+    if (dev != kErrSpeculation) throw;
+    c.gs_exact = true;
+    try {
+      body();
+    } catch (...) {
+      c.gs_exact = false;
+      throw;
+    }
+    c.gs_exact = false;
+  }
+}
+
 void require(bool ok, const char* msg) {
   if (!ok) throw Error(RD_EINVAL, msg);
 }
@@ -364,10 +387,12 @@ int rd_gpu_sgs_sweep(rd_ctx* ctx, const rd_csr* a, const double* f, const double
     const double* fd = in_dev(c, f, n, tf);
     const double* ud = in_dev(c, u, n, tu);
     OutVec<double> o(c, out, n);
-    gs_pass(c, A, fd, ud, t.p, true);
-    gs_pass(c, A, fd, t.p, o.dev(), false);
-    o.finish();
-    sync_and_raise(c);
+    exact_retry(c, [&] {
+      gs_pass(c, A, fd, ud, t.p, true);
+      gs_pass(c, A, fd, t.p, o.dev(), false);
+      o.finish();
+      sync_and_raise(c);
+    });
   });
 }
 
@@ -432,9 +457,11 @@ int rd_gpu_amg_apply(rd_amg* h, const double* r, double* z) {
     DBuf<double> tr;
     const double* rd = in_dev(c, r, n, tr);
     OutVec<double> zo(c, z, n);
-    vcycle(c, h->h, rd, zo.dev(), nullptr);
-    zo.finish();
-    if (zo.host || tr.p) sync_and_raise(c);
+    exact_retry(c, [&] {
+      vcycle(c, h->h, rd, zo.dev(), nullptr);
+      zo.finish();
+      sync_and_raise(c);
+    });
   });
 }
 
@@ -443,7 +470,12 @@ int rd_gpu_amg_level_sweep(rd_amg* h, int level, int forward, const double* f, c
     require(level >= 0 && level < (int)h->h.levels.size(), "amg_level_sweep: bad level");
     require(is_device_ptr(f) && is_device_ptr(xout) && (!xin || is_device_ptr(xin)),
             "amg_level_sweep: device pointers required");
-    gs_pass(h->ctx->c, h->h.levels[level].A, f, xin, xout, forward != 0);
+    // asynchronous (no sync to check a speculation): exact sweeps
+    Ctx& c = h->ctx->c;
+    const bool was = c.gs_exact;
+    c.gs_exact = true;
+    gs_pass(c, h->h.levels[level].A, f, xin, xout, forward != 0);
+    c.gs_exact = was;
   });
 }
 
@@ -459,11 +491,14 @@ int rd_gpu_pcg(rd_ctx* ctx, const rd_csr* a, rd_amg* amg, const double* f, doubl
     DBuf<double> tf, hd(std::max(max_iter, 1), c.stream);
     const double* fd = in_dev(c, f, n, tf);
     OutVec<double> xo(c, x, n);
-    const PcgResultDev r = pcg_device(c, A, amg ? &amg->h : nullptr, fd, tol, max_iter, xo.dev(), hd.p);
-    xo.finish();
-    if (hist && r.iterations > 0)
-      RDG_CUDA(cudaMemcpyAsync(hist, hd.p, sizeof(double) * r.iterations, cudaMemcpyDefault, c.stream));
-    sync_and_raise(c);
+    PcgResultDev r;
+    exact_retry(c, [&] {
+      r = pcg_device(c, A, amg ? &amg->h : nullptr, fd, tol, max_iter, xo.dev(), hd.p);
+      xo.finish();
+      if (hist && r.iterations > 0)
+        RDG_CUDA(cudaMemcpyAsync(hist, hd.p, sizeof(double) * r.iterations, cudaMemcpyDefault, c.stream));
+      sync_and_raise(c);
+    });
     if (rep) {
       rep->iterations = r.iterations;
       rep->converged = r.converged ? 1 : 0;
@@ -492,8 +527,12 @@ int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, doubl
     build_hierarchy(c, A, 64, 1, h);
     RDG_CUDA(cudaStreamSynchronize(c.stream));
     const auto t1 = clk::now();
-    const PcgResultDev r = pcg_device(c, A, &h, fd, tol, 500, uo.dev(), nullptr);
-    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    PcgResultDev r;
+    exact_retry(c, [&] {
+      r = pcg_device(c, A, &h, fd, tol, 500, uo.dev(), nullptr);
+      RDG_CUDA(cudaStreamSynchronize(c.stream));
+      sync_and_raise(c);
+    });
     const auto t2 = clk::now();
     uo.finish();
     sync_and_raise(c);

@@ -260,6 +260,22 @@ def test_sgs_bit_exact_large(rd, O, n, target):
     assert np.array_equal(rd.sgs_sweep(A, f, u), O.sgs_sweep(Ao, f, u))
 
 
+@pytest.mark.parametrize("scale", [1e-300, 1e300])
+def test_sgs_speculation_fallback(rd, O, scale):
+    """Row sums far outside the division fast path (|s| < 2^-969, or quotients
+    near overflow) make the speculative lattice sweep flag itself; the call is
+    rerun with exact sweeps and must still match the reference bit for bit."""
+    n = 16
+    os_ = O.build_system(O.build_structured_cube(n), 1.0 / (n * n), "smooth")
+    A = to_dev(rd, os_.A)
+    f = O.pseudo_random_vec(A.rows, 21) * scale
+    u = np.zeros(A.rows)
+    assert np.array_equal(rd.sgs_sweep(A, f, u), O.sgs_sweep(os_.A, f, u))
+    h = rd.build_amg(A, 64)
+    oh = O.build_amg(os_.A, 64)
+    assert np.array_equal(h.apply(f), oh.apply(f))
+
+
 def test_structured_levels_detected(rd, O):
     os_ = O.build_system(O.build_structured_cube(32), 2.0 ** -10, "smooth")
     h = rd.build_amg(to_dev(rd, os_.A))
