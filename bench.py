@@ -42,7 +42,7 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=N_DEFAULT)
+    p.add_argument("--cells", "--n", dest="n", type=int, default=N_DEFAULT, help="cells per cube side")
     p.add_argument("--target", default=TARGET)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -115,6 +115,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def job_rate(elapsed_ms, work, world, device=None):
+    """Whole-job throughput: the slowest rank's device time (MAX) over all ranks' work (SUM).
+    Ranks are independent replicas (the exact lexicographic GS does not
+    shard), so there is no data-path collective -- only this timing reduction."""
+    import torch
+
+    t = torch.tensor([float(elapsed_ms)], dtype=torch.float64, device=device)
+    wk = torch.tensor([float(work)], dtype=torch.float64, device=device)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(wk, op=torch.distributed.ReduceOp.SUM)
+    return float(t.item()), float(wk.item()) / (float(t.item()) / 1e3)
+
+
 # ---------------------------------------------------------------------------- ours
 def run_ours(args, rank, world, local_rank):
     import numpy as np
@@ -169,14 +183,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     clk = clocks.stop()
     launches = ctx.launch_count - l0
-    elapsed_ms = e0.elapsed_time(e1)
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    work = torch.tensor([float(ndofs) * sum(its)], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(work, op=torch.distributed.ReduceOp.SUM)
-    elapsed_ms = float(t.item())
-    value = float(work.item()) / (elapsed_ms / 1e3)
+    elapsed_ms, value = job_rate(e0.elapsed_time(e1), float(ndofs) * sum(its), world, dev)
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
@@ -286,13 +293,9 @@ def run_ours(args, rank, world, local_rank):
         e2e_its = [e2e_step() for _ in range(args.steps)]
         b.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-        e2e_work = torch.tensor([float(ndofs) * sum(e2e_its)], dtype=torch.float64, device=dev)
-        if world > 1:
-            torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX)
-            torch.distributed.all_reduce(e2e_work, op=torch.distributed.ReduceOp.SUM)
-        result["e2e"] = {"value": float(e2e_work.item()) / (float(e2e_ms.item()) / 1e3), "unit": UNIT,
-                         "ms_per_step": float(e2e_ms.item()) / args.steps,
+        e2e_ms, e2e_value = job_rate(a.elapsed_time(b), float(ndofs) * sum(e2e_its), world, dev)
+        result["e2e"] = {"value": e2e_value, "unit": UNIT,
+                         "ms_per_step": e2e_ms / args.steps,
                          "h2d_bytes_per_step": int(xyz.nbytes + tets.nbytes + bnd.nbytes),
                          "d2h_bytes_per_step": int(8 * ndofs),
                          "path": "rd_gpu_mesh_create(pinned host TetMesh) -> rd_gpu_build_system -> "
