@@ -169,6 +169,14 @@ typedef struct {
 int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, double tol, double* u,
                             rd_solve_outcome* out);
 
+/* replaces rd::l2_error / rd::h1_semi_error (assembly.hpp:59-61, assembly.cpp:265-310) for the
+ * manufactured exact solution u = c sin(pi x) sin(pi y) sin(pi z), c = 1/(3 rho pi^2 + 1)
+ * (rd::manufactured_exact(rho), target.cpp:45-58): the P1 field with interior coefficients
+ * `coeffs` (n_dofs, host or device) and zero boundary values, degree-5 rule per tet.  Either
+ * output may be null.  RD_EINVAL if rho < 0 or sizes mismatch. */
+int rd_gpu_error_norms(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs,
+                       double rho, double* l2_error, double* h1_semi_error);
+
 #ifdef __cplusplus
 }
 #endif

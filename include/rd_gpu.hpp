@@ -130,6 +130,7 @@ class FemSystem {
     A = DeviceMatrix(ctx, rd_gpu_system_matrix(h, 2), h_);
   }
   int n_dofs() const { return rd_gpu_system_n_dofs(h_.get()); }
+  const rd_system* get() const { return h_.get(); }
   const double* f_device() const { return rd_gpu_system_load(h_.get()); }
   std::vector<double> f() const {
     std::vector<double> out(n_dofs());
@@ -270,5 +271,18 @@ inline SolveOutcome solve_system_amg(const DeviceMatrix& A, const double* f, dou
 }
 
 inline SolveOutcome solve_system_amg(const FemSystem& sys, double tol) { return solve_system_amg(sys.A, sys.f_device(), tol); }
+
+// assembly.hpp:59-61 l2_error / h1_semi_error with rd::manufactured_exact(rho) (target.cpp:45-58)
+struct ErrorNorms {
+  double l2 = 0.0, h1_semi = 0.0;
+};
+inline ErrorNorms error_norms(const TetMesh& mesh, const FemSystem& sys, const std::vector<double>& coeffs,
+                              double rho) {
+  if ((int)coeffs.size() != sys.n_dofs()) throw std::invalid_argument("error_norms: coefficient size mismatch");
+  ErrorNorms e;
+  check(rd_gpu_error_norms(mesh.context().get(), mesh.get(), sys.get(), coeffs.data(), rho, &e.l2, &e.h1_semi),
+        mesh.context().get());
+  return e;
+}
 
 }  // namespace rd_gpu

@@ -917,6 +917,102 @@ __global__ void lat_load_gather_kernel(int nd, int n, const int* __restrict__ d2
   f[r] = s;
 }
 
+// ---------------------------------------------------------------- error norms
+// assembly.cpp:265-310 against the manufactured exact solution: per tet the
+// degree-5 rule's sum (in the reference's operation order), then a fixed-order
+// block reduction (the reference sums tets sequentially; the order of the final
+// sum differs, so the norms agree to rounding, ~1e-15 relative).
+constexpr int kErrNT = 256;
+template <bool H1>
+__global__ void __launch_bounds__(kErrNT) error_norm_kernel(int nt, const int* __restrict__ tets,
+                                                          const double* __restrict__ xyz,
+                                                          const int* __restrict__ v2d,
+                                                          const double* __restrict__ coeffs, double cexact,
+                                                          double* partials, unsigned* counter, double* out) {
+  __shared__ double sh[kErrNT / 32];
+  const int t = blockIdx.x * kErrNT + threadIdx.x;
+  double contrib = 0.0;
+  if (t < nt) {
+    const int4 t4 = reinterpret_cast<const int4*>(tets)[t];
+    const int tv[4] = {t4.x, t4.y, t4.z, t4.w};
+    double V[4][3], nod[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) V[k][c] = xyz[3 * (int64_t)tv[k] + c];
+      const int d = v2d[tv[k]];
+      nod[k] = d >= 0 ? coeffs[d] : 0.0;  // nodal_field (assembly.cpp:358-363)
+    }
+    if (!H1) {
+      double a[3], b[3], e[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        a[c] = __dsub_rn(V[1][c], V[0][c]);
+        b[c] = __dsub_rn(V[2][c], V[0][c]);
+        e[c] = __dsub_rn(V[3][c], V[0][c]);
+      }
+      const double x0 = __dsub_rn(__dmul_rn(a[1], b[2]), __dmul_rn(a[2], b[1]));
+      const double x1 = __dsub_rn(__dmul_rn(a[2], b[0]), __dmul_rn(a[0], b[2]));
+      const double x2 = __dsub_rn(__dmul_rn(a[0], b[1]), __dmul_rn(a[1], b[0]));
+      const double dt = __dadd_rn(__dadd_rn(__dmul_rn(x0, e[0]), __dmul_rn(x1, e[1])), __dmul_rn(x2, e[2]));
+      const double vol = __ddiv_rn(fabs(dt), 6.0);  // mesh.cpp:188-191
+      double acc = 0.0;
+      for (int q = 0; q < 14; ++q) {
+        const double* lam = c_rules.p14[q];
+        double X[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) s = __dadd_rn(s, __dmul_rn(lam[k], V[k][c]));
+          X[c] = s;
+        }
+        double u = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u = __dadd_rn(u, __dmul_rn(lam[k], nod[k]));
+        const double d = __dsub_rn(u, __dmul_rn(cexact, sin3(X[0], X[1], X[2])));
+        acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_rules.w14[q], d), d));
+      }
+      contrib = __dmul_rn(vol, acc);
+    } else {
+      Geom G;
+      if (local_geom(V[0], V[1], V[2], V[3], G)) {
+        double gu[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) gu[c] = __dadd_rn(gu[c], __dmul_rn(nod[k], G.g[k][c]));
+        double acc = 0.0;
+        const double cp = __dmul_rn(cexact, kPi);
+        for (int q = 0; q < 14; ++q) {
+          const double* lam = c_rules.p14[q];
+          double X[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s = __dadd_rn(s, __dmul_rn(lam[k], V[k][c]));
+            X[c] = s;
+          }
+          const double sx = sin(__dmul_rn(kPi, X[0])), cx = cos(__dmul_rn(kPi, X[0]));
+          const double sy = sin(__dmul_rn(kPi, X[1])), cy = cos(__dmul_rn(kPi, X[1]));
+          const double sz = sin(__dmul_rn(kPi, X[2])), cz = cos(__dmul_rn(kPi, X[2]));
+          const double ge0 = __dmul_rn(__dmul_rn(__dmul_rn(cp, cx), sy), sz);
+          const double ge1 = __dmul_rn(__dmul_rn(__dmul_rn(cp, sx), cy), sz);
+          const double ge2 = __dmul_rn(__dmul_rn(__dmul_rn(cp, sx), sy), cz);
+          const double d0 = __dsub_rn(gu[0], ge0), d1 = __dsub_rn(gu[1], ge1), d2 = __dsub_rn(gu[2], ge2);
+          const double sq = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+          acc = __dadd_rn(acc, __dmul_rn(c_rules.w14[q], sq));
+        }
+        contrib = __dmul_rn(G.vol, acc);
+      }
+    }
+  }
+  const double bsum = block_sum_fixed<kErrNT>(contrib, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = bsum;
+  finish_reduction<kErrNT>(partials, counter, sh, [&](double tot) { *out = tot; });
+}
+
 int read_flag(Ctx& c, const int* d) {
   int h = 0;
   RDG_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -1113,6 +1209,33 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
     c.launches += 2;
   }
   RDG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, double rho, double* l2,
+                 double* h1) {
+  if (!(rho >= 0.0)) throw Error(RD_EINVAL, "manufactured_exact: rho must be >= 0");
+  upload_rules(c);
+  const double cexact = 1.0 / (3.0 * rho * kPi * kPi + 1.0);  // target.cpp:45-58
+  const int nt = m.nt;
+  const int nb = std::max(div_up(nt, kErrNT), 1);
+  DBuf<double> partials(nb, c.stream), outv(2, c.stream);
+  DBuf<unsigned> counter(1, c.stream);
+  RDG_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), c.stream));
+  RDG_CUDA(cudaMemsetAsync(outv.p, 0, 2 * sizeof(double), c.stream));
+  if (nt > 0) {
+    error_norm_kernel<false><<<nb, kErrNT, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, s.v2d.p, coeffs, cexact,
+                                                          partials.p, counter.p, outv.p);
+    RDG_LAUNCH_CHECK();
+    error_norm_kernel<true><<<nb, kErrNT, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, s.v2d.p, coeffs, cexact,
+                                                         partials.p, counter.p, outv.p + 1);
+    RDG_LAUNCH_CHECK();
+    c.launches += 2;
+  }
+  double h[2];
+  RDG_CUDA(cudaMemcpyAsync(h, outv.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  RDG_CUDA(cudaStreamSynchronize(c.stream));
+  if (l2) *l2 = std::sqrt(h[0]);
+  if (h1) *h1 = std::sqrt(h[1]);
 }
 
 }  // namespace rdg

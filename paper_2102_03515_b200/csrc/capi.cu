@@ -543,4 +543,16 @@ int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, doubl
   });
 }
 
+int rd_gpu_error_norms(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs, double rho,
+                       double* l2, double* h1) {
+  return guard(ctx, [&] {
+    require(mesh && sys && coeffs, "error_norms: null argument");
+    require(sys->s.nv == mesh->m.nv, "error_norms: system does not belong to the mesh");
+    Ctx& c = ctx->c;
+    DBuf<double> tc;
+    const double* cd = in_dev(c, coeffs, sys->s.n_dofs, tc);
+    error_norms(c, mesh->m, sys->s, cd, rho, l2, h1);
+  });
+}
+
 }  // extern "C"

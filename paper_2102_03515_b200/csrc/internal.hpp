@@ -119,6 +119,8 @@ void build_structured_cube(Ctx& c, int n, DMesh& m);
 // sets m.lattice_n when the tets are exactly the build_structured_cube enumeration
 void detect_cube_lattice(Ctx& c, DMesh& m);
 void build_system(Ctx& c, const DMesh& m, double rho, int target_kind, uint64_t seed, DSystem& s);
+// l2 / h1-semi error of the P1 field `coeffs` (device, n_dofs) vs the manufactured exact solution
+void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, double rho, double* l2, double* h1);
 
 }  // namespace rdg
 

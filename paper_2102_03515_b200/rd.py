@@ -122,6 +122,7 @@ def lib():
         "rd_gpu_amg_level_sweep": (_I, [_P, _I, _I, _P, _P, _P]),
         "rd_gpu_pcg": (_I, [_P, _P, _P, _P, _D, _I, _P, _P, _P]),
         "rd_gpu_solve_system_amg": (_I, [_P, _P, _P, _D, _P, _P]),
+        "rd_gpu_error_norms": (_I, [_P, _P, _P, _P, _D, C.POINTER(_D), C.POINTER(_D)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -378,6 +379,20 @@ def build_system(mesh: TetMesh, rho: float, target: str = "smooth", seed: int = 
     h = _P()
     ctx.check(lib().rd_gpu_build_system(ctx.h, mesh.h, float(rho), C.byref(t), C.byref(h)))
     return FemSystem(h, ctx, mesh, rho)
+
+
+def error_norms(sys: FemSystem, coeffs, rho_exact: float):
+    """assembly.hpp:59-61 l2_error / h1_semi_error against rd::manufactured_exact(rho_exact)
+    (target.cpp:45-58), on the device.  `coeffs`: interior dof values (host array or device pointer)."""
+    ctx = sys.ctx
+    if isinstance(coeffs, np.ndarray) or isinstance(coeffs, (list, tuple)):
+        coeffs = np.ascontiguousarray(coeffs, np.float64)
+        if coeffs.size != sys.n_dofs:
+            raise RdInvalidArgument("error_norms: coefficient vector size mismatch")
+    l2, h1 = _D(), _D()
+    ctx.check(lib().rd_gpu_error_norms(ctx.h, sys.mesh.h, sys.h, _ptr(coeffs) if sys.n_dofs else None,
+                                       float(rho_exact), C.byref(l2), C.byref(h1)))
+    return l2.value, h1.value
 
 
 # ------------------------------------------------------------------ kernels

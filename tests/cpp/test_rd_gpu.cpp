@@ -132,6 +132,17 @@ int main() {
     CHECK(out.converged);
     std::printf("C1 n=32: %d iterations, setup %.3f ms, solve %.3f ms\n", out.iterations, 1e3 * out.setup_seconds,
                 1e3 * out.solve_seconds);
+    // assembly.cpp:265-310 error norms against the manufactured solution (rho_exact = rho)
+    const ErrorNorms e = error_norms(mesh, sys, out.u, 1.0 / 1024.0);
+    CHECK(e.l2 > 0.0 && e.l2 < 1e-2 && e.h1_semi > e.l2);
+    std::printf("C1 n=32: l2 %.17g h1 %.17g\n", e.l2, e.h1_semi);
+    bool threw = false;
+    try {
+      error_norms(mesh, sys, out.u, -1.0);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
   }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail;

@@ -18,5 +18,11 @@ def test_cpp_reference_cases(O):
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
     its = int(re.search(r"C1 n=32: (\d+) iterations", out.stdout).group(1))
-    ref = O.solve_system_amg(O.build_system(O.build_structured_cube(32), 1.0 / 1024.0, "smooth"))
+    om = O.build_structured_cube(32)
+    os_ = O.build_system(om, 1.0 / 1024.0, "smooth")
+    ref = O.solve_system_amg(os_)
     assert its == ref.iterations
+    m = re.search(r"C1 n=32: l2 (\S+) h1 (\S+)", out.stdout)
+    l2o = O.l2_error_manufactured(om, os_, ref.u, 1.0 / 1024.0)
+    h1o = O.h1_semi_error_manufactured(om, os_, ref.u, 1.0 / 1024.0)
+    assert abs(float(m.group(1)) - l2o) <= 1e-9 * l2o and abs(float(m.group(2)) - h1o) <= 1e-9 * h1o

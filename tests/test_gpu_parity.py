@@ -387,6 +387,27 @@ def test_solve_system_parity(rd, O, n, rho, target):
     assert np.abs(out.u - ref.u).max() <= 1e-10 * np.abs(ref.u).max()
 
 
+@pytest.mark.parametrize("n,rho", [(8, 1.0), (16, 2.0 ** -8), (32, 2.0 ** -10)])
+def test_error_norms_manufactured(rd, O, n, rho):
+    """assembly.cpp:265-310 on the device: the converged solution of the smooth target
+    against rd::manufactured_exact(rho).  CUDA sin/cos vs glibc and a different order of
+    the final sum over tets: agreement to 1e-12 relative."""
+    om = O.build_structured_cube(n)
+    os_ = O.build_system(om, rho, "smooth")
+    ref = O.solve_system_amg(os_, 1e-10)
+    l2o = O.l2_error_manufactured(om, os_, ref.u, rho)
+    h1o = O.h1_semi_error_manufactured(om, os_, ref.u, rho)
+    ds = rd.build_system(rd.build_structured_cube(n), rho, "smooth")
+    l2, h1 = rd.error_norms(ds, ref.u, rho)
+    assert abs(l2 - l2o) <= 1e-12 * l2o and abs(h1 - h1o) <= 1e-12 * h1o
+    # zero field: the norms of the exact solution itself
+    l2z, h1z = rd.error_norms(ds, np.zeros(ds.n_dofs), rho)
+    assert abs(l2z - O.l2_error_manufactured(om, os_, np.zeros(ds.n_dofs), rho)) <= 1e-12 * l2z
+    assert abs(h1z - O.h1_semi_error_manufactured(om, os_, np.zeros(ds.n_dofs), rho)) <= 1e-12 * h1z
+    with pytest.raises(ValueError):
+        rd.error_norms(ds, ref.u, -1.0)
+
+
 @pytest.mark.parametrize("rho", [1.0, 1e-2, 1e-4, 1e-6, 2.0 ** -12])
 def test_c3_rho_sweep_n64(rd, O, rho):  # BASELINE config 3 at full size
     O.set_num_threads(8)
