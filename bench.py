@@ -250,6 +250,28 @@ def run_ours(args, rank, world, local_rank):
         "frac": gs_gbs / peak, "traffic": traffic.get("gs_sweep"),
         "bytes_per_launch": gs_bytes, "launch_ms": gs_ms, "share_of_step_est": share,
     }
+    # per kernel class: algorithmic bytes / measured time, vs measured and spec HBM
+    nl = h.num_levels
+    lv = [(h.level(l).rows, h.level(l).nnz, h.level(l, "P").nnz if l + 1 < nl else 0) for l in range(nl)]
+    vc_bytes = sum(60 * Z_ + 168 * N_ + 24 * ZP + 20 * lv[l + 1][0] for l, (N_, Z_, ZP) in enumerate(lv[:-1]))
+    vc_bytes += 8 * lv[-1][0] ** 2
+    zr = torch.rand(N, dtype=torch.float64, device=dev)
+    zz = torch.empty(N, dtype=torch.float64, device=dev)
+    vcycle_ms = timed(lambda: h.apply(zr, zz))
+    it_bytes = vc_bytes + 12 * Z + 92 * N
+    it_ms = 1e3 * statistics.mean(solve_s) / max(1, its0)
+    SPEC_HBM = 8000.0
+
+    def cls(bytes_, ms):
+        gbs = bytes_ / (ms * 1e-3) / 1e9
+        return {"bytes": bytes_, "ms": ms, "achieved_gbs": gbs, "frac_measured": gbs / peak, "frac_spec": gbs / SPEC_HBM}
+
+    result["roofline_classes"] = {
+        "spmv": cls(spmv_bytes, spmv_ms), "gs_sweep_level0": cls(gs_bytes, gs_ms),
+        "vcycle": cls(vc_bytes, vcycle_ms),
+        "pcg_iteration": dict(cls(it_bytes, it_ms), note="solve_seconds / iterations (includes the host loop)"),
+        "ceiling_dof_iters_per_s": peak * 1e9 / (it_bytes / N),
+    }
     result["kernels"] = {
         "spmv": {"bytes_per_launch": spmv_bytes, "launch_ms": spmv_ms,
                  "achieved_gbs": spmv_bytes / (spmv_ms * 1e-3) / 1e9,
@@ -322,10 +344,17 @@ def cpu_baseline(n, target):
     cores = host_threads()
     O.set_num_threads(cores)
     r = O.pipeline(n, rho_for(n), target, 0, TOL)
-    return {"value": r["n_dofs"] * r["iterations"] / r["total_s"], "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"one full C2 step on the CPU oracle (n={n}: build_system + build_amg + pcg, "
-                      f"{r['iterations']} iterations), {r['total_s']:.1f} s; SGS/setup serial as in the reference",
-            "phases_s": {"build": r["build_s"], "setup": r["setup_s"], "solve": r["solve_s"]}}
+    out = {"value": r["n_dofs"] * r["iterations"] / r["total_s"], "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"one full C2 step on the CPU oracle (n={n}: build_system + build_amg + pcg, "
+                     f"{r['iterations']} iterations), {r['total_s']:.1f} s; SGS/setup serial as in the reference",
+           "phases_s": {"build": r["build_s"], "setup": r["setup_s"], "solve": r["solve_s"]}}
+    if cores > 1 and not os.environ.get("RD_BENCH_NO_CPU1"):  # threads = 1 as well
+        O.set_num_threads(1)
+        r1 = O.pipeline(n, rho_for(n), target, 0, TOL)
+        out["single_thread"] = {"value": r1["n_dofs"] * r1["iterations"] / r1["total_s"], "total_s": r1["total_s"],
+                                "phases_s": {"build": r1["build_s"], "setup": r1["setup_s"], "solve": r1["solve_s"]}}
+        O.set_num_threads(cores)
+    return out
 
 
 # ---------------------------------------------------------------------------- reference arm
