@@ -11,7 +11,11 @@
 //     conservative-product accumulation (linalg.cu spgemm).
 //   * coarsest level: dense LLT in one CTA.
 #include <algorithm>
+#include <utility>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.hpp"
 
@@ -116,37 +120,48 @@ __global__ void to_dense_kernel(int n, const int* __restrict__ rp, const int* __
 }
 
 // Left-looking Cholesky in one CTA, operation order identical to the oracle's
-// llt_compute (the CPU checker in oracle/).  L overwrites the dense copy.
-__global__ void llt_kernel(int n, double* L, int* err) {
+// llt_compute (the CPU checker in oracle/).  L overwrites the dense copy; with
+// SMEM the factor is staged in shared memory (row stride n + 1: a warp's column
+// reads fall in distinct banks) and written back at the end.
+template <bool SMEM>
+__global__ void llt_kernel(int n, double* Lg, int* err) {
+  extern __shared__ double lsh[];
   __shared__ double piv;
   __shared__ int bad;
+  const int ld = SMEM ? n + 1 : n;
+  double* L = SMEM ? lsh : Lg;
+  if (SMEM) {
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) lsh[(e / n) * ld + e % n] = Lg[e];
+  }
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
   for (int j = 0; j < n; ++j) {
     if (threadIdx.x == 0) {
-      double s = L[(size_t)j * n + j];
-      for (int k = 0; k < j; ++k) s = __dsub_rn(s, __dmul_rn(L[(size_t)j * n + k], L[(size_t)j * n + k]));
+      double s = L[(size_t)j * ld + j];
+      for (int k = 0; k < j; ++k) s = __dsub_rn(s, __dmul_rn(L[(size_t)j * ld + k], L[(size_t)j * ld + k]));
       if (!(s > 0.0)) {
         bad = 1;
       } else {
         piv = __dsqrt_rn(s);
-        L[(size_t)j * n + j] = piv;
+        L[(size_t)j * ld + j] = piv;
       }
     }
     __syncthreads();
     if (bad) break;
     for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
-      double t = L[(size_t)i * n + j];
-      for (int k = 0; k < j; ++k) t = __dsub_rn(t, __dmul_rn(L[(size_t)i * n + k], L[(size_t)j * n + k]));
-      L[(size_t)i * n + j] = __ddiv_rn(t, piv);
+      double t = L[(size_t)i * ld + j];
+      for (int k = 0; k < j; ++k) t = __dsub_rn(t, __dmul_rn(L[(size_t)i * ld + k], L[(size_t)j * ld + k]));
+      L[(size_t)i * ld + j] = __ddiv_rn(t, piv);
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    if (bad) *err = 1;
-    // zero the strict upper triangle (never read; keeps downloads clean)
+  if (SMEM) {
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) Lg[e] = lsh[(e / n) * ld + e % n];
   }
+  if (threadIdx.x == 0 && bad) *err = 1;
 }
+constexpr int kLltSmemMax = 160 * 1024;
+size_t llt_smem(int n) { return sizeof(double) * (size_t)n * (n + 1); }
 
 // LLT solve in one CTA: forward L y = b (row sums ascending in k), then
 // L^T x = y (sums descending in k) -- same order as the oracle's llt_solve.
@@ -286,33 +301,252 @@ __global__ void lat_compact_kernel(int nc, int Lc, const double* __restrict__ ou
   }
 }
 
-// P^T on a lattice level with the all-even coarsening: the rows of P^T come out
-// in ascending fine index by walking each coarse point's 3x3x3 fine neighbourhood
-// in (dz, dy, dx) order -- no atomics, no per-row sort (same result as transpose()).
-template <bool FILL>
-__global__ void lat_pt_kernel(int nc, int Lc, int L, const int* __restrict__ prp, const int* __restrict__ pci,
-                              const double* __restrict__ pv, int* cnt, const int* __restrict__ trp, int* tci,
-                              double* tv) {
+// ---------------------------------------------------------------- closed-form lattice level
+// With the exact in-box 15-point stencil verified on an L^3 box, the greedy
+// C/F split is the all-even set (lat_flags_kernel) and everything the level
+// needs follows in closed form:
+//   * P row of fine point p with odd axes S: C -> (p/2, 1); F -> p - e_S and,
+//     when inside the box, p + e_S, each with weight 1/count (p_fill_kernel);
+//   * P^T row of coarse point I: the fine points 2I + d, d in the stencil
+//     (ascending), with the same weights (every other fine point misses I);
+//   * row offsets of both are lexicographic counts of per-axis predicates;
+//   * A_c = P^T (A P) entry (I, J) = sum over ascending k in P^T row I of
+//     P_kI * (sum over ascending m in A row k of A_km * P_mJ) -- the order of
+//     the two ordered Eigen products (lat_ap_kernel / lat_ptap_kernel), fused
+//     per coarse row with every window slot a compile-time register.
+namespace latc {
+struct Stencil {
+  int d[15][3];
+};
+// ascending linear offset (same table as lattice_check_kernel)
+constexpr Stencil kSt = {{{-1, -1, -1}, {0, -1, -1}, {-1, 0, -1}, {0, 0, -1}, {-1, -1, 0},
+                          {0, -1, 0},   {-1, 0, 0},  {0, 0, 0},   {1, 0, 0},  {0, 1, 0},
+                          {1, 1, 0},    {0, 0, 1},   {1, 0, 1},   {0, 1, 1},  {1, 1, 1}}};
+constexpr int st(int j, int a) { return kSt.d[j][a]; }
+constexpr int slot(int ox, int oy, int oz) { return (oz + 1) * 9 + (oy + 1) * 3 + (ox + 1); }
+// 2I + e inside the fine box along one axis, e in [-2, 2]
+struct Ax {
+  bool lo, h1, h2;  // I >= 1, 2I + 1 < L, 2I + 2 < L
+};
+template <int E>
+__device__ __forceinline__ bool inb(const Ax& a) {
+  static_assert(E >= -2 && E <= 2, "offset");
+  if constexpr (E < 0) return a.lo;
+  else if constexpr (E == 0) return true;
+  else if constexpr (E == 1) return a.h1;
+  else return a.h2;
+}
+// window slots of A_c row I that AP row 2I + d(KD) can reach
+constexpr unsigned touched(int kd) {
+  unsigned m = 0;
+  for (int md = 0; md < 15; ++md) {
+    const int e[3] = {st(kd, 0) + st(md, 0), st(kd, 1) + st(md, 1), st(kd, 2) + st(md, 2)};
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int a = 0; a < 3; ++a) {
+      const int odd = e[a] & 1;
+      lo[a] = (e[a] - odd) / 2;
+      hi[a] = (e[a] + odd) / 2;
+    }
+    m |= 1u << slot(lo[0], lo[1], lo[2]);
+    m |= 1u << slot(hi[0], hi[1], hi[2]);
+  }
+  return m;
+}
+
+template <int KD, int MD>
+__device__ __forceinline__ void ap_term(double (&V)[27], int& pos, const double* __restrict__ av, const Ax& ax,
+                                        const Ax& ay, const Ax& az) {
+  constexpr int ex = st(KD, 0) + st(MD, 0), ey = st(KD, 1) + st(MD, 1), ez = st(KD, 2) + st(MD, 2);
+  if (!(inb<ex>(ax) && inb<ey>(ay) && inb<ez>(az))) return;
+  const double a = av[pos++];
+  constexpr int sx = ex & 1, sy = ey & 1, sz = ez & 1;
+  if constexpr ((sx | sy | sz) == 0) {  // m is a C point: P row (m/2, 1)
+    constexpr int s = slot(ex / 2, ey / 2, ez / 2);
+    V[s] = __dadd_rn(V[s], __dmul_rn(1.0, a));
+  } else {  // F point: low m - e_S, high m + e_S when inside (only +1 offsets can leave the box)
+    const bool hin = (!(sx && ex == 1) || ax.h2) && (!(sy && ey == 1) || ay.h2) && (!(sz && ez == 1) || az.h2);
+    const double t = __dmul_rn(hin ? 0.5 : 1.0, a);
+    constexpr int sl = slot((ex - sx) / 2, (ey - sy) / 2, (ez - sz) / 2);
+    constexpr int sh = slot((ex + sx) / 2, (ey + sy) / 2, (ez + sz) / 2);
+    V[sl] = __dadd_rn(V[sl], t);
+    if (hin) V[sh] = __dadd_rn(V[sh], t);
+  }
+}
+
+template <int KD, int... MD>
+__device__ __forceinline__ void k_term(double (&W)[27], int k0, int L, const int* __restrict__ arp,
+                                       const double* __restrict__ av, const Ax& ax, const Ax& ay, const Ax& az,
+                                       std::integer_sequence<int, MD...>) {
+  constexpr int dx = st(KD, 0), dy = st(KD, 1), dz = st(KD, 2);
+  if (!(inb<dx>(ax) && inb<dy>(ay) && inb<dz>(az))) return;
+  const int k = k0 + (dz * L + dy) * L + dx;
+  double wk;  // P_kI
+  if constexpr (dx == 0 && dy == 0 && dz == 0)
+    wk = 1.0;
+  else if constexpr (dx <= 0 && dy <= 0 && dz <= 0)
+    wk = 0.5;
+  else
+    wk = (inb<2 * dx>(ax) && inb<2 * dy>(ay) && inb<2 * dz>(az)) ? 0.5 : 1.0;
+  double V[27];
+#pragma unroll
+  for (int s = 0; s < 27; ++s) V[s] = 0.0;
+  int pos = arp[k];
+  (ap_term<KD, MD>(V, pos, av, ax, ay, az), ...);
+  constexpr unsigned tm = touched(KD);
+#pragma unroll
+  for (int s = 0; s < 27; ++s)
+    if ((tm >> s) & 1u) W[s] = __dadd_rn(W[s], __dmul_rn(V[s], wk));
+}
+
+template <int... KD>
+__device__ __forceinline__ void rap_row(double (&W)[27], int k0, int L, const int* __restrict__ arp,
+                                        const double* __restrict__ av, const Ax& ax, const Ax& ay, const Ax& az,
+                                        std::integer_sequence<int, KD...>) {
+  (k_term<KD>(W, k0, L, arp, av, ax, ay, az, std::make_integer_sequence<int, 15>{}), ...);
+}
+
+// Row offsets of a stencil-structured CSR over a box of side n: row I holds the
+// offsets d of the 15-point table with pred(d_a, I_a) on every axis, where
+// pred(-1, u) = u >= 1, pred(0, u) = true, pred(+1, u) = u < mp.  The offset of
+// row I is the lexicographic count of (row, d) pairs before it.
+__device__ __forceinline__ long long cnt_pred(int d, int v, int mp) {
+  return d < 0 ? (v > 0 ? v - 1 : 0) : d == 0 ? v : min(v, mp);
+}
+__device__ __forceinline__ bool pred(int d, int u, int mp) { return d < 0 ? u >= 1 : d == 0 ? true : u < mp; }
+__device__ __forceinline__ void stencil_offset(const int (&D)[15][3], int n, int mp, int ix, int iy, int iz,
+                                               long long& o, long long& tot) {
+  o = 0;
+  tot = 0;
+#pragma unroll
+  for (int j = 0; j < 15; ++j) {
+    const int dx = D[j][0], dy = D[j][1], dz = D[j][2];
+    const long long nx = cnt_pred(dx, n, mp), ny = cnt_pred(dy, n, mp);
+    o += cnt_pred(dz, iz, mp) * ny * nx +
+         (pred(dz, iz, mp) ? cnt_pred(dy, iy, mp) * nx + (pred(dy, iy, mp) ? cnt_pred(dx, ix, mp) : 0) : 0);
+    tot += cnt_pred(dz, n, mp) * ny * nx;
+  }
+}
+}  // namespace latc
+
+constexpr int kRapNT = 128;
+#define RD_LAT_D15                                                                                       \
+  {{-1, -1, -1}, {0, -1, -1}, {-1, 0, -1}, {0, 0, -1}, {-1, -1, 0}, {0, -1, 0}, {-1, 0, 0}, {0, 0, 0}, \
+   {1, 0, 0},    {0, 1, 0},   {1, 1, 0},   {0, 0, 1},  {1, 0, 1},   {0, 1, 1},  {1, 1, 1}}
+
+// DIRECT: write A_c straight into its 15-point lattice CSR (closed-form offsets)
+// and only flag a pattern mismatch; otherwise the 27-slot window rows go to
+// `out` / `cnt` for the scan + compaction of the exact (pruned) pattern.
+template <bool DIRECT>
+__global__ void __launch_bounds__(kRapNT) lat_rap_kernel(int nc, int Lc, int L, const int* __restrict__ arp,
+                                                         const double* __restrict__ av, double* out, int* cnt,
+                                                         int* crp, int* cci, double* cv, int* notlat) {
+  const int I = blockIdx.x * kRapNT + threadIdx.x;
+  if (I >= nc) return;
+  const int ix = I % Lc, iy = I / Lc % Lc, iz = I / (Lc * Lc);
+  const latc::Ax ax{ix >= 1, 2 * ix + 1 < L, 2 * ix + 2 < L};
+  const latc::Ax ay{iy >= 1, 2 * iy + 1 < L, 2 * iy + 2 < L};
+  const latc::Ax az{iz >= 1, 2 * iz + 1 < L, 2 * iz + 2 < L};
+  double W[27];
+#pragma unroll
+  for (int s = 0; s < 27; ++s) W[s] = 0.0;
+  latc::rap_row(W, (2 * iz * L + 2 * iy) * L + 2 * ix, L, arp, av, ax, ay, az,
+                std::make_integer_sequence<int, 15>{});
+  int c = 0;
+  bool bad = false;
+  long long o = 0;
+  if (DIRECT) {
+    const int D[15][3] = RD_LAT_D15;
+    long long tot;
+    latc::stencil_offset(D, Lc, Lc - 1, ix, iy, iz, o, tot);
+    crp[I] = (int)o;
+    if (I == nc - 1) crp[nc] = (int)tot;
+  }
+#pragma unroll
+  for (int s = 0; s < 27; ++s) {
+    const int ox = s % 3 - 1, oy = s / 3 % 3 - 1, oz = s / 9 - 1;
+    const bool same = (ox >= 0 && oy >= 0 && oz >= 0) || (ox <= 0 && oy <= 0 && oz <= 0);
+    const bool in = (unsigned)(ix + ox) < (unsigned)Lc && (unsigned)(iy + oy) < (unsigned)Lc &&
+                    (unsigned)(iz + oz) < (unsigned)Lc;
+    const bool nz = W[s] != 0.0;
+    bad |= nz != (same && in);  // A_c keeps the exact in-box 15-point pattern?
+    if (DIRECT) {
+      if (same && in) {  // slots ascend with the column index
+        cci[o] = I + (oz * Lc + oy) * Lc + ox;
+        cv[o] = W[s];
+        ++o;
+      }
+    } else {
+      c += nz;
+      out[(size_t)s * nc + I] = W[s];
+    }
+  }
+  if (!DIRECT) cnt[I] = c;
+  if (bad) atomicExch(notlat, 1);
+}
+
+// P of a lattice level: rows, row offsets (closed form) and the C/F flags
+__global__ void lat_p_kernel(int L, int Lc, int* rp, int* ci, double* v, uint8_t* flags) {
+  const int n = L * L * L;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int x = i % L, y = i / L % L, z = i / (L * L);
+  // row length 1 + [F and p + e_S inside]; [F and inside] = [ok] - [even] with
+  // ok(u) = (u != L - 1 or L odd); counts below i in lexicographic order
+  const int nok = L - ((L & 1) ? 0 : 1);
+  auto okc = [&](int u) { return u; };  // #{u' < u : ok(u')} for u <= L - 1
+  auto ok = [&](int u) { return (L & 1) || u != L - 1; };
+  const long long below_ok =
+      (long long)okc(z) * nok * nok + (ok(z) ? (long long)okc(y) * nok + (ok(y) ? okc(x) : 0) : 0);
+  auto evc = [](int u) { return (u + 1) >> 1; };
+  const long long below_even = (long long)evc(z) * Lc * Lc + (!(z & 1) ? (long long)evc(y) * Lc + (!(y & 1) ? evc(x) : 0) : 0);
+  const int o = (int)(i + below_ok - below_even);
+  rp[i] = o;
+  if (i == n - 1) rp[n] = (int)((long long)n + (long long)nok * nok * nok - (long long)Lc * Lc * Lc);
+  const int sx = x & 1, sy = y & 1, sz = z & 1;
+  const int lo = ((z >> 1) * Lc + (y >> 1)) * Lc + (x >> 1);
+  if (!(sx | sy | sz)) {
+    flags[i] = 1;
+    ci[o] = lo;
+    v[o] = 1.0;
+    return;
+  }
+  flags[i] = 0;
+  const bool hin = (!sx || x + 1 < L) && (!sy || y + 1 < L) && (!sz || z + 1 < L);
+  const double w = __ddiv_rn(1.0, hin ? 2.0 : 1.0);
+  ci[o] = lo;
+  v[o] = w;
+  if (hin) {
+    ci[o + 1] = (((z + sz) >> 1) * Lc + ((y + sy) >> 1)) * Lc + ((x + sx) >> 1);
+    v[o + 1] = w;
+  }
+}
+
+// P^T of a lattice level (closed form; same rows as transpose(P))
+__global__ void lat_pt_kernel(int L, int Lc, int* rp, int* ci, double* v) {
+  const int nc = Lc * Lc * Lc;
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
   if (I >= nc) return;
-  const int fx = 2 * (I % Lc), fy = 2 * (I / Lc % Lc), fz = 2 * (I / (Lc * Lc));
-  int o = FILL ? trp[I] : 0;
-  for (int dz = -1; dz <= 1; ++dz)
-    for (int dy = -1; dy <= 1; ++dy)
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int x = fx + dx, y = fy + dy, z = fz + dz;
-        if (x < 0 || y < 0 || z < 0 || x >= L || y >= L || z >= L) continue;
-        const int k = (z * L + y) * L + x;
-        for (int e = prp[k]; e < prp[k + 1]; ++e)
-          if (pci[e] == I) {
-            if (FILL) {
-              tci[o] = k;
-              tv[o] = pv[e];
-            }
-            ++o;
-          }
-      }
-  if (!FILL) cnt[I] = o;
+  const int ix = I % Lc, iy = I / Lc % Lc, iz = I / (Lc * Lc);
+  const int D[15][3] = RD_LAT_D15;
+  long long o, tot;
+  latc::stencil_offset(D, Lc, L / 2, ix, iy, iz, o, tot);  // 2I + d inside: I_a < L/2 for d_a = +1
+  rp[I] = (int)o;
+  if (I == nc - 1) rp[nc] = (int)tot;
+  const int k0 = (2 * iz * L + 2 * iy) * L + 2 * ix;
+#pragma unroll
+  for (int j = 0; j < 15; ++j) {
+    const int dx = D[j][0], dy = D[j][1], dz = D[j][2];
+    if (!(latc::pred(dx, ix, L / 2) && latc::pred(dy, iy, L / 2) && latc::pred(dz, iz, L / 2))) continue;
+    double w = 1.0;
+    if (j != 7) {
+      const bool neg = dx <= 0 && dy <= 0 && dz <= 0;
+      const bool hin = neg || ((dx == 0 || 2 * ix + 2 < L) && (dy == 0 || 2 * iy + 2 < L) && (dz == 0 || 2 * iz + 2 < L));
+      w = __ddiv_rn(1.0, hin ? 2.0 : 1.0);
+    }
+    ci[o] = k0 + (dz * L + dy) * L + dx;
+    v[o] = w;
+    ++o;
+  }
 }
 
 int read_int(Ctx& c, const int* d) {
@@ -416,72 +650,191 @@ DCsr galerkin(Ctx& c, const DCsr& A, const DCsr& P, const DCsr& Pt) {
   return prune_zeros(c, Ac);
 }
 
-void dense_llt(Ctx& c, const DCsr& A, DBuf<double>& L) {
+void dense_llt(Ctx& c, const DCsr& A, DBuf<double>& L, int* err_dev) {
   const int n = A.rows;
   L.alloc((size_t)n * n, c.stream);
   RDG_CUDA(cudaMemsetAsync(L.p, 0, sizeof(double) * n * n, c.stream));
   to_dense_kernel<<<n, 64, 0, c.stream>>>(n, A.rp.p, A.ci.p, A.v.p, L.p);
   RDG_LAUNCH_CHECK();
-  DBuf<int> err(1, c.stream);
-  RDG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.stream));
-  llt_kernel<<<1, 256, 0, c.stream>>>(n, L.p, err.p);
+  DBuf<int> err;
+  if (!err_dev) {
+    err.alloc(1, c.stream);
+    RDG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.stream));
+  }
+  if (llt_smem(n) <= (size_t)kLltSmemMax) {
+    static bool attr = false;
+    if (!attr) {
+      RDG_CUDA(cudaFuncSetAttribute(llt_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLltSmemMax));
+      attr = true;
+    }
+    llt_kernel<true><<<1, 256, llt_smem(n), c.stream>>>(n, L.p, err_dev ? err_dev : err.p);
+  } else {
+    llt_kernel<false><<<1, 256, 0, c.stream>>>(n, L.p, err_dev ? err_dev : err.p);
+  }
   RDG_LAUNCH_CHECK();
   c.launches += 2;
-  if (read_int(c, err.p)) throw Error(RD_ENOTSPD, "build_amg: coarsest level not positive definite");
+  if (!err_dev && read_int(c, err.p)) throw Error(RD_ENOTSPD, "build_amg: coarsest level not positive definite");
 }
 
-void build_hierarchy(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h) {
+namespace {
+bool lattice_cube(const DCsr& A) { return A.lat.ok && A.lat.lx == A.lat.ly && A.lat.ly == A.lat.lz; }
+
+// total of latc::stencil_offset on the host
+int64_t stencil_total(int n, int mp) {
+  const int D[15][3] = RD_LAT_D15;
+  auto N = [&](int d) -> int64_t { return d < 0 ? std::max(n - 1, 0) : d == 0 ? n : std::min(n, mp); };
+  int64_t t = 0;
+  for (auto& d : D) t += N(d[0]) * N(d[1]) * N(d[2]);
+  return t;
+}
+
+// One lattice level in closed form (see lat_rap_kernel): P, P^T and the flags
+// without scans or host round trips.  direct: A_c goes straight into the
+// 15-point lattice layout and *notlat_dev records whether that was exact (the
+// caller checks once, after the whole hierarchy); otherwise A_c is compacted
+// from its window rows with one host round trip for its size.
+void lattice_level(Ctx& c, Level& lv, DCsr& Ac, int* notlat_dev, bool direct) {
+  const DCsr& A = lv.A;
+  const int L = A.lat.lx, Lc = (L + 1) / 2, n = A.rows, nc = Lc * Lc * Lc;
+  const int nok = L - ((L & 1) ? 0 : 1);
+  const int64_t pnnz = (int64_t)n + (int64_t)nok * nok * nok - nc;
+  const int64_t cnnz = stencil_total(Lc, Lc - 1);
+  if (pnnz > 0x7fffffffLL || cnnz > 0x7fffffffLL)
+    throw Error(RD_EINVAL, "index overflow: more than INT32_MAX entries (SpMat<int>)");
+  lv.flags.alloc(n, c.stream);
+  DCsr& P = lv.P;
+  P = DCsr{};
+  P.rows = n;
+  P.cols = nc;
+  P.nnz = pnnz;
+  P.rp.alloc(n + 1, c.stream);
+  P.ci.alloc(pnnz, c.stream);
+  P.v.alloc(pnnz, c.stream);
+  lat_p_kernel<<<div_up(n, 256), 256, 0, c.stream>>>(L, Lc, P.rp.p, P.ci.p, P.v.p, lv.flags.p);
+  RDG_LAUNCH_CHECK();
+  DCsr& T = lv.Pt;
+  T = DCsr{};
+  T.rows = nc;
+  T.cols = n;
+  T.nnz = pnnz;
+  T.rp.alloc(nc + 1, c.stream);
+  T.ci.alloc(pnnz, c.stream);
+  T.v.alloc(pnnz, c.stream);
+  lat_pt_kernel<<<div_up(nc, 256), 256, 0, c.stream>>>(L, Lc, T.rp.p, T.ci.p, T.v.p);
+  RDG_LAUNCH_CHECK();
+  c.launches += 2;
+  Ac = DCsr{};
+  Ac.rows = Ac.cols = nc;
+  Ac.rp.alloc(nc + 1, c.stream);
+  Ac.lat_checked = true;
+  if (direct) {
+    Ac.nnz = cnnz;
+    Ac.ci.alloc(cnnz, c.stream);
+    Ac.v.alloc(cnnz, c.stream);
+    lat_rap_kernel<true><<<div_up(nc, kRapNT), kRapNT, 0, c.stream>>>(nc, Lc, L, A.rp.p, A.v.p, nullptr, nullptr,
+                                                                       Ac.rp.p, Ac.ci.p, Ac.v.p, notlat_dev);
+    RDG_LAUNCH_CHECK();
+    ++c.launches;
+    Ac.lat = nc >= 8 ? Lattice{Lc, Lc, Lc, true} : Lattice{};
+    return;
+  }
+  DBuf<int> notlat(1, c.stream), cnt(nc, c.stream);
+  DBuf<double> out((size_t)27 * nc, c.stream);
+  RDG_CUDA(cudaMemsetAsync(notlat.p, 0, sizeof(int), c.stream));
+  lat_rap_kernel<false><<<div_up(nc, kRapNT), kRapNT, 0, c.stream>>>(nc, Lc, L, A.rp.p, A.v.p, out.p, cnt.p,
+                                                                      nullptr, nullptr, nullptr, notlat.p);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+  int nl = 0;
+  Ac.nnz = exclusive_scan(c, cnt.p, Ac.rp.p, nc, notlat.p, &nl);
+  Ac.ci.alloc(Ac.nnz, c.stream);
+  Ac.v.alloc(Ac.nnz, c.stream);
+  lat_compact_kernel<<<div_up(nc, 256), 256, 0, c.stream>>>(nc, Lc, out.p, Ac.rp.p, Ac.ci.p, Ac.v.p);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+  // the pattern check of detect_lattice, folded into the product
+  Ac.lat = (nl == 0 && nc >= 8) ? Lattice{Lc, Lc, Lc, true} : Lattice{};
+}
+}  // namespace
+
+namespace {
+// RD_SETUP_TRACE=1: synchronise after each setup phase and print its host time
+// (diagnostic only; the syncs it adds are not in the product path)
+struct SetupTrace {
+  Ctx& c;
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  explicit SetupTrace(Ctx& cc) : c(cc), on(getenv("RD_SETUP_TRACE") && atoi(getenv("RD_SETUP_TRACE")) != 0) {
+    if (on) {
+      cudaStreamSynchronize(c.stream);
+      t0 = std::chrono::steady_clock::now();
+    }
+  }
+  void mark(const char* what, int level) {
+    if (!on) return;
+    cudaStreamSynchronize(c.stream);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[setup] L%d %-10s %8.1f us\n", level, what,
+            std::chrono::duration<double, std::micro>(t - t0).count());
+    t0 = t;
+  }
+};
+}  // namespace
+
+namespace {
+// direct: lattice levels write A_c in the lattice layout without host round
+// trips; returns false if one of them turned out not to be exact (then the
+// caller rebuilds with direct = false).
+bool build_levels(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, bool borrow, bool direct) {
+  SetupTrace tr(c);
   h.levels.clear();
   h.smoothing_steps = m;
-  DCsr current = csr_copy(c, A);
+  constexpr int kMaxLat = 64;  // lattice levels halve the side: at most log2(INT_MAX) of them
+  DBuf<int> flags_dev(kMaxLat + 64, c.stream);  // [0, kMaxLat): not-lattice per level; then setup errors
+  RDG_CUDA(cudaMemsetAsync(flags_dev.p, 0, sizeof(int) * (kMaxLat + 64), c.stream));
+  int nlat = 0;
+  DCsr current = borrow ? csr_view(A) : csr_copy(c, A);
+  tr.mark("copy", 0);
   while (current.rows > threshold) {
+    const int li = (int)h.levels.size();
     Level lv;
     lv.A = std::move(current);
-    detect_lattice(c, lv.A);  // lattice levels: closed-form C/F split and windowed Galerkin
+    detect_lattice(c, lv.A);  // lattice levels: closed-form P, P^T and fused Galerkin product
+    tr.mark("detect", li);
+    if (lattice_cube(lv.A) && nlat < kMaxLat) {
+      lattice_level(c, lv, current, flags_dev.p + nlat++, direct);
+      lv.has_p = true;
+      tr.mark("lattice", li);
+      h.levels.push_back(std::move(lv));
+      continue;
+    }
     DCsr P;
     coarsen(c, lv.A, lv.flags, P);
+    tr.mark("coarsen", li);
     if (P.cols >= P.rows) {  // no reduction possible (amg.cpp:98-101)
       current = std::move(lv.A);
       lv.flags.release();
       break;
     }
     lv.P = std::move(P);
-    const int Lf = lv.A.lat.lx, Lc = (Lf + 1) / 2;
-    if (lv.A.lat.ok && Lf == lv.A.lat.ly && Lf == lv.A.lat.lz && (int64_t)Lc * Lc * Lc == lv.P.cols) {
-      DCsr& T = lv.Pt;
-      T = DCsr{};
-      T.rows = lv.P.cols;
-      T.cols = lv.P.rows;
-      T.rp.alloc(T.rows + 1, c.stream);
-      DBuf<int> cnt(T.rows + 1, c.stream);
-      lat_pt_kernel<false><<<div_up(T.rows, 256), 256, 0, c.stream>>>(T.rows, Lc, Lf, lv.P.rp.p, lv.P.ci.p, lv.P.v.p,
-                                                                       cnt.p, nullptr, nullptr, nullptr);
-      RDG_LAUNCH_CHECK();
-      T.nnz = exclusive_scan(c, cnt.p, T.rp.p, T.rows);
-      c.launches += 1;
-      if (T.nnz == lv.P.nnz) {
-        T.ci.alloc(T.nnz, c.stream);
-        T.v.alloc(T.nnz, c.stream);
-        lat_pt_kernel<true><<<div_up(T.rows, 256), 256, 0, c.stream>>>(T.rows, Lc, Lf, lv.P.rp.p, lv.P.ci.p,
-                                                                        lv.P.v.p, nullptr, T.rp.p, T.ci.p, T.v.p);
-        RDG_LAUNCH_CHECK();
-        ++c.launches;
-      } else {  // an entry outside the window: not the all-even coarsening after all
-        lv.Pt = transpose(c, lv.P);
-      }
-    } else {
-      lv.Pt = transpose(c, lv.P);
-    }
+    lv.Pt = transpose(c, lv.P);
     lv.has_p = true;
+    tr.mark("transpose", li);
     current = galerkin(c, lv.A, lv.P, lv.Pt);
+    tr.mark("galerkin", li);
     h.levels.push_back(std::move(lv));
   }
   Level last;
   last.A = std::move(current);
   h.levels.push_back(std::move(last));
   h.nc = h.levels.back().A.rows;
-  if (h.nc > 0) dense_llt(c, h.levels.back().A, h.Lc);
-  // work vectors; structured-smoother detection per level
+  // setup errors stay on the device until the single read-back below:
+  // [kMaxLat] coarsest LLT, [kMaxLat + 1 + l] level l's structured-smoother layout
+  const size_t nerr = std::min<size_t>(h.levels.size() + 1, 64);
+  int* serr = flags_dev.p + kMaxLat;
+  if (h.nc > 0) dense_llt(c, h.levels.back().A, h.Lc, serr);
+  tr.mark("llt", (int)h.levels.size() - 1);
+  // work vectors; structured-smoother layout per level
   for (size_t l = 0; l < h.levels.size(); ++l) {
     Level& lv = h.levels[l];
     const int n = std::max(lv.A.rows, 1);
@@ -493,9 +846,26 @@ void build_hierarchy(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h) 
     lv.res.alloc(n, c.stream);
     if (lv.has_p) {
       detect_lattice(c, lv.A);
-      lattice_prepare(c, lv.A);
+      lattice_prepare(c, lv.A, 1 + l < nerr ? serr + 1 + l : nullptr);
     }
+    tr.mark("prepare", (int)l);
   }
+  std::vector<int> f(kMaxLat + nerr);
+  RDG_CUDA(cudaMemcpyAsync(f.data(), flags_dev.p, sizeof(int) * f.size(), cudaMemcpyDeviceToHost, c.stream));
+  RDG_CUDA(cudaStreamSynchronize(c.stream));
+  for (int l = 0; l < nlat; ++l)
+    if (f[l]) return false;  // a lattice A_c lost the 15-point pattern: rebuild exactly
+  if (f[kMaxLat]) throw Error(RD_ENOTSPD, "build_amg: coarsest level not positive definite");
+  for (size_t l = 1; l < nerr; ++l) {
+    if (f[kMaxLat + l] == 2) throw Error(RD_EZERODIAG, "sgs_sweep: zero diagonal");
+    if (f[kMaxLat + l]) throw Error(RD_ERUNTIME, "lattice smoother: pattern/layout mismatch");
+  }
+  return true;
+}
+}  // namespace
+
+void build_hierarchy(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, bool borrow) {
+  if (!build_levels(c, A, threshold, m, h, borrow, /*direct=*/true)) build_levels(c, A, threshold, m, h, borrow, false);
 }
 
 void coarse_solve(Ctx& c, Hierarchy& h, const double* r, double* z) {

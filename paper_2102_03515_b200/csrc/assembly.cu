@@ -1107,6 +1107,14 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
           s.M.v.p, s.A.rp.p, s.A.ci.p, s.A.v.p);
       RDG_LAUNCH_CHECK();
       ++c.launches;
+      if ((int64_t)nd == (int64_t)(n - 1) * (n - 1) * (n - 1)) {
+        // every inner vertex is a dof: A's rows are the lexicographic (n-1)^3 box,
+        // and its pattern is the full in-box 15-point stencil (every mesh edge has
+        // a strictly positive mass entry, so no slot is culled) -- what
+        // detect_lattice would verify.  K may cull exact zeros, so it is not marked.
+        s.A.lat = Lattice{n - 1, n - 1, n - 1, n - 1 >= 2};
+        s.A.lat_checked = true;
+      }
     } else {  // a dof on the cube's surface (custom boundary flags): generic path
       RDG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.stream));
       lattice = false;

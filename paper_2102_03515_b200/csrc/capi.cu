@@ -524,7 +524,7 @@ int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, doubl
     RDG_CUDA(cudaStreamSynchronize(c.stream));
     const auto t0 = clk::now();
     Hierarchy h;
-    build_hierarchy(c, A, 64, 1, h);
+    build_hierarchy(c, A, 64, 1, h, /*borrow=*/true);  // A outlives h (this call)
     RDG_CUDA(cudaStreamSynchronize(c.stream));
     const auto t1 = clk::now();
     PcgResultDev r;

@@ -39,7 +39,9 @@ struct DCsr {
 // ---------------------------------------------------------------- scan
 // Exclusive prefix sum of n int32 counts into int32 offsets[n+1]; returns the
 // total (throws RD_EINVAL if it exceeds INT32_MAX, the reference's index type).
-int64_t exclusive_scan(Ctx& c, const int* counts, int* offsets, int64_t n);
+// `also_dev` (optional): one more device int read back with the same sync.
+int64_t exclusive_scan(Ctx& c, const int* counts, int* offsets, int64_t n, const int* also_dev = nullptr,
+                       int* also_host = nullptr);
 
 // ---------------------------------------------------------------- linalg.cu
 void spmv(Ctx& c, const DCsr& A, const double* x, double* y);
@@ -54,6 +56,7 @@ DCsr transpose(Ctx& c, const DCsr& A);
 DCsr spgemm(Ctx& c, const DCsr& A, const DCsr& B);  // Eigen conservative product order
 DCsr prune_zeros(Ctx& c, const DCsr& A);
 DCsr csr_copy(Ctx& c, const DCsr& A);
+DCsr csr_view(const DCsr& A);  // non-owning view of A's arrays (lattice facts carried over)
 bool pattern_symmetric(Ctx& c, const DCsr& A);
 // detect a monotone (15-point Kuhn or sub-) stencil on a box; fills A.lat
 void detect_lattice(Ctx& c, DCsr& A);
@@ -63,8 +66,9 @@ void detect_lattice(Ctx& c, DCsr& A);
 // nullptr = zero vector).  Optionally accumulates dot(r, xout) into dot_out.
 void gs_pass(Ctx& c, const DCsr& A, const double* f, const double* xin, double* xout, bool fwd,
              double* dot_out = nullptr, const double* dot_with = nullptr);
-// setup-time layout for the structured smoother (no-op unless A.lat.ok)
-void lattice_prepare(Ctx& c, const DCsr& A);
+// setup-time layout for the structured smoother (no-op unless A.lat.ok); with
+// err_dev the layout check is left on the device (1 mismatch, 2 zero diagonal)
+void lattice_prepare(Ctx& c, const DCsr& A, int* err_dev = nullptr);
 
 // ---------------------------------------------------------------- amg.cu
 struct Level {
@@ -84,10 +88,12 @@ struct Hierarchy {
 
 std::vector<uint8_t> coarsen(Ctx& c, const DCsr& A, DBuf<uint8_t>& flags_dev, DCsr& P);
 DCsr galerkin(Ctx& c, const DCsr& A, const DCsr& P, const DCsr& Pt);
-void build_hierarchy(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h);
+// borrow: level 0 views A's arrays (A must outlive the hierarchy and stay unchanged)
+void build_hierarchy(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, bool borrow = false);
 // z = V(r) on device; if dot_out, also writes r.z (deterministic)
 void vcycle(Ctx& c, Hierarchy& h, const double* r, double* z, double* dot_out);
-void dense_llt(Ctx& c, const DCsr& A, DBuf<double>& L);  // throws RD_ENOTSPD
+// throws RD_ENOTSPD, or (err_dev) leaves the failure flag on the device
+void dense_llt(Ctx& c, const DCsr& A, DBuf<double>& L, int* err_dev = nullptr);
 
 // ---------------------------------------------------------------- pcg.cu
 struct PcgResultDev {

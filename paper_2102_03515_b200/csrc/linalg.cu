@@ -104,9 +104,13 @@ __global__ void scan_tiles(const int* __restrict__ in, int64_t n, const long lon
 }
 }  // namespace
 
-int64_t exclusive_scan(Ctx& c, const int* counts, int* offsets, int64_t n) {
+int64_t exclusive_scan(Ctx& c, const int* counts, int* offsets, int64_t n, const int* also_dev, int* also_host) {
   if (n <= 0) {
     RDG_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int), c.stream));
+    if (also_dev) {
+      RDG_CUDA(cudaMemcpyAsync(also_host, also_dev, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+      RDG_CUDA(cudaStreamSynchronize(c.stream));
+    }
     return 0;
   }
   const int nb = div_up(n, kScanTile);
@@ -120,7 +124,10 @@ int64_t exclusive_scan(Ctx& c, const int* counts, int* offsets, int64_t n) {
   c.launches += 3;
   long long* hp = reinterpret_cast<long long*>(c.h_pinned + 8);  // pinned: a true async readback
   RDG_CUDA(cudaMemcpyAsync(hp, bsum.p + nb, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
+  int* ha = reinterpret_cast<int*>(c.h_pinned + 9);
+  if (also_dev) RDG_CUDA(cudaMemcpyAsync(ha, also_dev, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   RDG_CUDA(cudaStreamSynchronize(c.stream));
+  if (also_dev) *also_host = *ha;
   const long long total = *hp;
   if (total > 0x7fffffffLL) throw Error(RD_EINVAL, "index overflow: more than INT32_MAX entries (SpMat<int>)");
   return total;
@@ -461,12 +468,26 @@ __global__ void lattice_check_kernel(int rows, const int* __restrict__ rp, const
 }
 }  // namespace
 
+DCsr csr_view(const DCsr& A) {
+  DCsr B;
+  B.rows = A.rows;
+  B.cols = A.cols;
+  B.nnz = A.nnz;
+  B.lat = A.lat;
+  B.lat_checked = A.lat_checked;
+  B.rp = DBuf<int>::view(A.rp.p, A.rp.n);
+  B.ci = DBuf<int>::view(A.ci.p, A.ci.n);
+  B.v = DBuf<double>::view(A.v.p, A.v.n);
+  return B;
+}
+
 DCsr csr_copy(Ctx& c, const DCsr& A) {
   DCsr B;
   B.rows = A.rows;
   B.cols = A.cols;
   B.nnz = A.nnz;
   B.lat = A.lat;
+  B.lat_checked = A.lat_checked;
   B.rp.alloc(A.rows + 1, c.stream);
   B.ci.alloc(A.nnz, c.stream);
   B.v.alloc(A.nnz, c.stream);

@@ -310,24 +310,84 @@ def test_hierarchy_bit_exact(rd, O, n, thr):
             assert_csr_equal(dh.level(l, "Pt"), oh.level(l, "Pt"), f"Pt_{l}")
 
 
-@pytest.mark.parametrize("n,jitter", [(16, 0.0), (16, 0.2), (24, 0.2), (13, 0.0), (64, 0.0)])
-def test_hierarchy_lattice_levels(rd, O, n, jitter):
-    """Lattice levels take the closed-form C/F split and the windowed Galerkin
-    product; non-uniform geometry (jitter) and odd level sizes included."""
+@pytest.mark.parametrize("n,jitter,thr", [(16, 0.0, 64), (16, 0.2, 64), (24, 0.2, 64), (13, 0.0, 64), (64, 0.0, 64),
+                                          (10, 0.1, 1), (5, 0.0, 1), (3, 0.0, 4), (12, 0.0, 8)])
+def test_hierarchy_lattice_levels(rd, O, n, jitter, thr):
+    """Lattice levels take the closed-form C/F split, P, P^T and the fused Galerkin
+    product; non-uniform geometry (jitter), odd and even level sides (high-face F
+    points with a single C neighbour) and hierarchies down to one coarse point."""
     xyz, tets, b = O.build_structured_cube(n).xyz, O.build_structured_cube(n).tets, O.build_structured_cube(n).boundary
     if jitter:
         rng = np.random.default_rng(11)
         xyz = xyz.copy()
         xyz[b == 0] += rng.uniform(-jitter, jitter, size=(int((b == 0).sum()), 3)) / n
     os_ = O.build_system(O.mesh_from_arrays(xyz, tets, b), 1.0 / (n * n), "ball")
-    oh = O.build_amg(os_.A, 64)
-    dh = rd.build_amg(to_dev(rd, os_.A), 64)
+    oh = O.build_amg(os_.A, thr)
+    dh = rd.build_amg(to_dev(rd, os_.A), thr)
     assert dh.num_levels == oh.num_levels
     for l in range(oh.num_levels):
         assert_csr_equal(dh.level(l), oh.level(l), f"A_{l}")
         if l + 1 < oh.num_levels:
             assert np.array_equal(dh.flags(l), oh.flags(l))
             assert_csr_equal(dh.level(l, "P"), oh.level(l, "P"), f"P_{l}")
+            assert_csr_equal(dh.level(l, "Pt"), oh.level(l, "Pt"), f"Pt_{l}")
+    r = O.pseudo_random_vec(os_.A.rows, 3)
+    assert np.array_equal(dh.apply(r), oh.apply(r))
+
+
+@pytest.mark.parametrize("n,rho", [(9, 1.0), (16, 2.0 ** -8), (33, 1e-6)])
+def test_hierarchy_from_device_assembly(rd, O, n, rho):
+    """A from the lattice assembly carries its lattice facts (no detection pass);
+    the hierarchy built on it is the oracle's, level by level."""
+    ds = rd.build_system(rd.build_structured_cube(n), rho, "ball")
+    os_ = O.build_system(O.build_structured_cube(n), rho, "ball")
+    oh = O.build_amg(os_.A, 64)
+    dh = rd.build_amg(ds.A, 64)
+    assert dh.num_levels == oh.num_levels
+    for l in range(oh.num_levels):
+        assert_csr_equal(dh.level(l), oh.level(l), f"A_{l}")
+        if l + 1 < oh.num_levels:
+            assert_csr_equal(dh.level(l, "P"), oh.level(l, "P"), f"P_{l}")
+            assert_csr_equal(dh.level(l, "Pt"), oh.level(l, "Pt"), f"Pt_{l}")
+            assert dh.structured(l)
+
+
+@pytest.mark.parametrize("variant", ["random_zeros", "cancelled_coarse_entry"])
+def test_hierarchy_lattice_explicit_zeros(rd, O, variant):
+    """Explicit zero values on a lattice pattern: the fine level stays a lattice
+    (the split is pattern based) and the Galerkin product prunes exact zeros.  In
+    the second variant (identity plus one coupling -1/2 between fine points 2I and
+    2I + e_x) the coarse entry (I, I + e_x) cancels to exactly zero, so level 1
+    loses the 15-point pattern and continues on the generic path."""
+    os_ = O.build_system(O.build_structured_cube(17), 2.0 ** -8, "ball")
+    A = os_.A
+    L = 16
+    rows = np.repeat(np.arange(A.rows), np.diff(A.rp))
+    if variant == "random_zeros":
+        v = A.v.copy()
+        rng = np.random.default_rng(4)
+        v[(rows != A.ci) & (rng.random(v.size) < 0.3)] = 0.0
+    else:
+        v = np.where(rows == A.ci, 1.0, 0.0)
+        a = (4 * L + 4) * L + 4
+        for i, j in ((a, a + 1), (a + 1, a)):
+            k = A.rp[i] + int(np.searchsorted(A.ci[A.rp[i]:A.rp[i + 1]], j))
+            assert A.ci[k] == j
+            v[k] = -0.5
+    Az = O.Csr(A.rows, A.cols, A.rp, A.ci, v)
+    oh = O.build_amg(Az, 8)
+    dh = rd.build_amg(to_dev(rd, Az), 8)
+    assert dh.num_levels == oh.num_levels
+    for l in range(oh.num_levels):
+        assert_csr_equal(dh.level(l), oh.level(l), f"A_{l}")
+        if l + 1 < oh.num_levels:
+            assert np.array_equal(dh.flags(l), oh.flags(l))
+            assert_csr_equal(dh.level(l, "P"), oh.level(l, "P"), f"P_{l}")
+            assert_csr_equal(dh.level(l, "Pt"), oh.level(l, "Pt"), f"Pt_{l}")
+    assert dh.structured(0)
+    assert dh.structured(1) == (variant == "random_zeros")
+    r = O.pseudo_random_vec(A.rows, 5)
+    assert np.array_equal(dh.apply(r), oh.apply(r))
 
 
 @pytest.mark.parametrize("n,thr", [(3, 1000), (4, 16), (16, 64), (32, 64)])
