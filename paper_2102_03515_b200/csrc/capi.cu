@@ -2,6 +2,7 @@
 //
 // Each function converts rdg::Error into the status code that maps onto the
 // reference's exception type and leaves the message in rd_gpu_last_error().
+#include <cstdlib>
 #include <chrono>
 #include <cstring>
 
@@ -470,10 +471,13 @@ int rd_gpu_amg_level_sweep(rd_amg* h, int level, int forward, const double* f, c
     require(level >= 0 && level < (int)h->h.levels.size(), "amg_level_sweep: bad level");
     require(is_device_ptr(f) && is_device_ptr(xout) && (!xin || is_device_ptr(xin)),
             "amg_level_sweep: device pointers required");
-    // asynchronous (no sync to check a speculation): exact sweeps
+    // asynchronous (no sync to check a speculation): exact sweeps.  RD_GS_LEVEL_SPEC=1
+    // (timing probes only) runs the V-cycle's speculative kernel and leaves any
+    // speculation flag unchecked.
     Ctx& c = h->ctx->c;
     const bool was = c.gs_exact;
-    c.gs_exact = true;
+    static const bool spec = getenv("RD_GS_LEVEL_SPEC") && atoi(getenv("RD_GS_LEVEL_SPEC")) != 0;
+    c.gs_exact = !spec;
     gs_pass(c, h->h.levels[level].A, f, xin, xout, forward != 0);
     c.gs_exact = was;
   });

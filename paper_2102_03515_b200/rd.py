@@ -19,7 +19,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "librd_gpu.so")
+# RD_GPU_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("RD_GPU_LIB") or os.path.join(_HERE, "_build", "librd_gpu.so")
 
 RD_OK, RD_EINVAL, RD_ERUNTIME, RD_ENOTSPD, RD_EZERODIAG, RD_ECUDA, RD_ENCCL, RD_EDEGENERATE = range(8)
 

@@ -1,7 +1,8 @@
 """Per-warp step timing of the v5 lattice GS kernel (one tile, lane 0 of each warp): RD_GS_CTRACE.
 
 usage: python tools/gs_ctrace5.py [n] [tile] [level]
-probes per step: 0 start, 1 cells taken, 2 fresh values, 3 row sum, 4 x, 5 loads issued.
+probes per step (time order): 0 start, 2 old values + leading row terms, 1 fresh values,
+3 row sum, 4 x, 5 stores/loads issued.
 """
 import os
 import sys
@@ -32,14 +33,14 @@ for l in range(h.num_levels - 1):
     h.level_sweep(l, True, f, x, y)
 h.ctx.synchronize()
 lines = open(path).read().splitlines()
-names = ["cells", "shfl", "sum", "div", "stores/loads", "->next"]
+names = ["box+lead", "fresh wait", "sum", "div", "stores/loads", "->next"]
 i = 0
 while i < len(lines):
     hdr = lines[i].split()
     ns = int(hdr[3])
     starts = []
     for w in range(4):
-        v = np.array([int(t) for t in lines[i + 1 + 2 * w].split()], dtype=np.int64).reshape(-1, 8)[:, :6]
+        v = np.array([int(t) for t in lines[i + 1 + 2 * w].split()], dtype=np.int64).reshape(-1, 8)[:, [0, 2, 1, 3, 4, 5]]
         v = v[:ns]
         starts.append(v[:, 0])
         vv = v[10:ns - 10]

@@ -43,3 +43,19 @@ while i < len(lines):
     if nty * ntz > 1:
         # lag of each tile's step 0 vs its first-row step, along the diagonal
         print("   first-step time per tile (y fastest):", np.round(steps[:, 0], 1)[: min(24, nty * ntz)])
+    if nty * ntz > 1:
+        # halo hand-off: tile (y, z) step k needs the (y-1, z) tile's step k + TY - 1 (its last
+        # line's row of the same position) and the (y, z-1) tile's step k + TZ - 1
+        TY, TZ = 16, 8
+        ly, lz = [], []
+        for t in range(nty * ntz):
+            ty_, tz_ = t % nty, t // nty
+            if ty_ > 0:
+                o = t - 1
+                ly.append(np.median(steps[t, : ns - TY] - steps[o, TY - 1: ns - 1]))
+            if tz_ > 0:
+                o = t - nty
+                lz.append(np.median(steps[t, : ns - TZ] - steps[o, TZ - 1: ns - 1]))
+        print(f"   median hand-off lag: y {np.median(ly):.2f} us, z {np.median(lz):.2f} us; "
+              f"tile start offsets: mean per y-tile {np.median(np.diff(steps[:nty, 0])):.2f} us, "
+              f"per z-tile {np.median(np.diff(steps[::nty, 0])):.2f} us")
