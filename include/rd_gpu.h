@@ -177,6 +177,51 @@ int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, doubl
 int rd_gpu_error_norms(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs,
                        double rho, double* l2_error, double* h1_semi_error);
 
+/* ------------------------------------------------------------ distributed (z-slab) pieces
+ * SURVEY.md §8(e).  The reference has no distributed solver (its parallelism is
+ * the thread pool of parallel.cpp:12-73); these calls are the per-rank device
+ * work of the slab-partitioned AMG-PCG that paper_2102_03515_b200/dist.py drives
+ * over torch.distributed (NCCL halo planes + dot reductions).  DEVICE pointers
+ * only; every call is stream-ordered on the context's stream and asynchronous
+ * (device-detected errors surface at the next rd_gpu_synchronize).              */
+
+/* speculative-division miss of a lattice sweep, reported by rd_gpu_synchronize
+ * after asynchronous sweeps: rerun the computation with exact sweeps.        */
+#define RD_GS_SPECULATION_MISS 0x5ec
+int rd_gpu_ctx_set_exact_sweeps(rd_ctx* ctx, int exact);
+
+/* rows [row0, row1) of a, keeping columns [col0, col1) renumbered from 0 (RD_EINVAL
+ * if a kept row has a column outside): a rank's block of A_l / P_l / Pt_l.       */
+int rd_gpu_csr_rowblock(rd_ctx* ctx, const rd_csr* a, int row0, int row1, int col0, int col1, rd_csr** out);
+/* res = r - A z  (the V-cycle residual, amg.cpp:127) */
+int rd_gpu_residual(rd_ctx* ctx, const rd_csr* a, const double* r, const double* z, double* res);
+/* z += P zc  (the V-cycle correction, amg.cpp:130) */
+int rd_gpu_prolong_add(rd_ctx* ctx, const rd_csr* p, const double* zc, double* z);
+/* *out_dev = a . b (deterministic fixed-order reduction; out_dev on the device) */
+int rd_gpu_dot_async(rd_ctx* ctx, int n, const double* a, const double* b, double* out_dev);
+/* x += alpha p, r -= alpha Ap  /  p = z + beta p   (linalg.cpp:84-85,99) */
+int rd_gpu_pcg_update_xr(rd_ctx* ctx, int64_t n, double alpha, const double* p, const double* ap, double* x,
+                         double* r);
+int rd_gpu_pcg_update_p(rd_ctx* ctx, int64_t n, double beta, const double* z, double* p);
+/* the V-cycle of the sub-hierarchy from `level` (amg.cpp:121-132 entered at level l):
+ * r, z of rows(A_level); the coarse tail of a distributed V-cycle, on rank 0   */
+int rd_gpu_amg_apply_from(rd_amg* h, int level, const double* r, double* z);
+
+/* One rank's z-slab [zlo, zhi) of a lattice level (a: the level's whole-box matrix,
+ * e.g. rd_gpu_amg_level_matrix(h, l, 0)).  Local vectors hold planes [g0, g1):
+ * the slab plus one ghost plane on each side where the box has one.           */
+typedef struct rd_slab rd_slab;
+int rd_gpu_slab_create(rd_ctx* ctx, const rd_csr* a, int zlo, int zhi, rd_slab** out);
+void rd_gpu_slab_free(rd_slab* s);
+int rd_gpu_slab_info(const rd_slab* s, int* lattice_side, int* g0, int* g1);
+/* One Gauss-Seidel pass (half of sgs_sweep, amg.cpp:67-88) over the slab's rows.
+ * f, xin (NULL = zero vector), xout: local vectors (planes [g0, g1); xin's
+ * downstream ghost plane = old values).  in_plane: the L*L values of the upstream
+ * ghost plane (zlo-1 forward, zhi backward; NULL = zeros) -- the neighbour's
+ * fresh values reproduce the whole-box sweep bit for bit.                       */
+int rd_gpu_slab_sweep(rd_slab* s, int forward, const double* f, const double* xin, double* xout,
+                      const double* in_plane);
+
 #ifdef __cplusplus
 }
 #endif

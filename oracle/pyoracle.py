@@ -89,6 +89,7 @@ def lib():
         "or_amg_level_csr": (_P, [_P, _I, _I]),
         "or_amg_level_flags": (_I, [_P, _I, _pu8]),
         "or_amg_apply": (_I, [_P, _I, _pd, _pd]),
+        "or_amg_apply_from": (_I, [_P, _I, _I, _pd, _pd]),
         "or_pcg": (_I, [_P, _I, _P, _pd, _D, _I, _pd, C.POINTER(_I), C.POINTER(_I), _pd]),
         "or_solve_system_amg": (_I, [_P, _D, _pd, C.POINTER(_I), C.POINTER(_I), C.POINTER(_D), C.POINTER(_D)]),
         "or_pipeline": (_I, [_I, _D, _I, C.c_uint64, _D, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I),
@@ -385,6 +386,13 @@ class AmgHierarchy:
         r = np.ascontiguousarray(r, np.float64)
         z = np.zeros(max(r.size, 1))
         _check(lib().or_amg_apply(self._h.h, r.size, r if r.size else np.zeros(1), z))
+        return z[: r.size]
+
+    def apply_from(self, level: int, r) -> np.ndarray:
+        """The V-cycle entered at `level` (amg.cpp:121-132): the coarse tail of a distributed cycle."""
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.zeros(max(r.size, 1))
+        _check(lib().or_amg_apply_from(self._h.h, int(level), r.size, r if r.size else np.zeros(1), z))
         return z[: r.size]
 
 

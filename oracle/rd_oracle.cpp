@@ -1332,6 +1332,15 @@ int or_amg_apply(const or_amg* h, int n, const double* r, double* z) {
     std::memcpy(z, out.data(), out.size() * sizeof(double));
   });
 }
+// the V-cycle entered at `level` (amg.cpp:121-132 recursion from level l): checks the
+// coarse tail that rank 0 runs in the distributed solve
+int or_amg_apply_from(const or_amg* h, int level, int n, const double* r, double* z) {
+  return guard([&] {
+    if (level < 0 || (size_t)level >= h->h.levels.size()) throw std::invalid_argument("amg_apply_from: level");
+    const Vec out = vcycle(h->h, static_cast<size_t>(level), Vec(r, r + n));
+    std::memcpy(z, out.data(), out.size() * sizeof(double));
+  });
+}
 
 int or_pcg(const or_csr* a, int precond, const or_amg* h, const double* f, double tol, int max_iter, double* x,
            int* iterations, int* converged, double* history) {

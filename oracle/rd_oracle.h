@@ -91,6 +91,7 @@ int or_amg_num_levels(const or_amg* h);
 or_csr* or_amg_level_csr(or_amg* h, int level, int which);
 int or_amg_level_flags(const or_amg* h, int level, uint8_t* flags);
 int or_amg_apply(const or_amg* h, int n, const double* r, double* z);
+int or_amg_apply_from(const or_amg* h, int level, int n, const double* r, double* z);
 
 /* linalg.cpp:64-102; precond: 0 identity, 1 jacobi, 2 amg (uses h) */
 int or_pcg(const or_csr* a, int precond, const or_amg* h, const double* f,

@@ -877,23 +877,23 @@ void coarse_solve(Ctx& c, Hierarchy& h, const double* r, double* z) {
 }
 
 // V-cycle with zero initial guess (amg.cpp:119-132), unrolled over levels.
-void vcycle(Ctx& c, Hierarchy& h, const double* r, double* z, double* dot_out) {
+void vcycle(Ctx& c, Hierarchy& h, const double* r, double* z, double* dot_out, int l0) {
   const int L = static_cast<int>(h.levels.size());
   const int m = h.smoothing_steps;
-  if (L == 1) {
+  if (l0 == L - 1) {
     coarse_solve(c, h, r, z);
     if (dot_out) dot(c, h.nc, r, z, dot_out);
     return;
   }
   std::vector<const double*> rl(L);
   std::vector<double*> zl(L);
-  rl[0] = r;
-  zl[0] = z;
-  for (int l = 1; l < L; ++l) {
+  rl[l0] = r;
+  zl[l0] = z;
+  for (int l = l0 + 1; l < L; ++l) {
     rl[l] = h.levels[l].r.p;
     zl[l] = h.levels[l].z.p;
   }
-  for (int l = 0; l + 1 < L; ++l) {
+  for (int l = l0; l + 1 < L; ++l) {
     Level& lv = h.levels[l];
     const double* cur = nullptr;  // zero initial guess
     for (int s = 0; s < m; ++s) {
@@ -906,16 +906,16 @@ void vcycle(Ctx& c, Hierarchy& h, const double* r, double* z, double* dot_out) {
     spmv(c, lv.Pt, lv.res.p, h.levels[l + 1].r.p);
   }
   coarse_solve(c, h, rl[L - 1], zl[L - 1]);
-  for (int l = L - 2; l >= 0; --l) {
+  for (int l = L - 2; l >= l0; --l) {
     Level& lv = h.levels[l];
     prolong_add(c, lv.P, zl[l + 1], zl[l]);
     for (int s = 0; s < m; ++s) {
       gs_pass(c, lv.A, rl[l], zl[l], lv.t.p, true);
-      const bool last = (l == 0 && s == m - 1);
-      gs_pass(c, lv.A, rl[l], lv.t.p, zl[l], false, last ? dot_out : nullptr, last ? rl[0] : nullptr);
+      const bool last = (l == l0 && s == m - 1);
+      gs_pass(c, lv.A, rl[l], lv.t.p, zl[l], false, last ? dot_out : nullptr, last ? rl[l0] : nullptr);
     }
   }
-  if (m == 0 && dot_out) dot(c, h.levels[0].A.rows, r, z, dot_out);
+  if (m == 0 && dot_out) dot(c, h.levels[l0].A.rows, r, z, dot_out);
 }
 
 }  // namespace rdg

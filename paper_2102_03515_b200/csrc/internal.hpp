@@ -70,6 +70,20 @@ void gs_pass(Ctx& c, const DCsr& A, const double* f, const double* xin, double* 
 // err_dev the layout check is left on the device (1 mismatch, 2 zero diagonal)
 void lattice_prepare(Ctx& c, const DCsr& A, int* err_dev = nullptr);
 
+// distributed z-slab smoother (dist.cu): one rank's planes [zlo, zhi) of a lattice
+// level; local vectors hold planes [g0, g1) (the slab plus one ghost plane per side)
+struct SlabSmoother {
+  int L = 0, zlo = 0, zhi = 0, g0 = 0, g1 = 0, ntz = 0;
+  DBuf<double> pack[2];            // fwd, bwd step-major packed stencil of the slab's tiles
+  DBuf<unsigned long long> xh;     // tagged cells {value, tag} of planes [g0, g1)
+  unsigned epoch = 0;
+};
+// A: the level's whole-box matrix (verified lattice)
+void slab_prepare(Ctx& c, const DCsr& A, int zlo, int zhi, SlabSmoother& s);
+// in_plane: the upstream ghost plane's values (L*L; null = zeros), fresh (exact) or old (block)
+void gs_pass_slab(Ctx& c, SlabSmoother& s, const double* f, const double* xin, double* xout, bool fwd,
+                  const double* in_plane);
+
 // ---------------------------------------------------------------- amg.cu
 struct Level {
   DCsr A, P, Pt;
@@ -91,7 +105,8 @@ DCsr galerkin(Ctx& c, const DCsr& A, const DCsr& P, const DCsr& Pt);
 // borrow: level 0 views A's arrays (A must outlive the hierarchy and stay unchanged)
 void build_hierarchy(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, bool borrow = false);
 // z = V(r) on device; if dot_out, also writes r.z (deterministic)
-void vcycle(Ctx& c, Hierarchy& h, const double* r, double* z, double* dot_out);
+// l0 > 0: the V-cycle of the sub-hierarchy from level l0 (r, z of level l0's size)
+void vcycle(Ctx& c, Hierarchy& h, const double* r, double* z, double* dot_out, int l0 = 0);
 // throws RD_ENOTSPD, or (err_dev) leaves the failure flag on the device
 void dense_llt(Ctx& c, const DCsr& A, DBuf<double>& L, int* err_dev = nullptr);
 

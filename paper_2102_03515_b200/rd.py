@@ -23,6 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RD_GPU_LIB") or os.path.join(_HERE, "_build", "librd_gpu.so")
 
 RD_OK, RD_EINVAL, RD_ERUNTIME, RD_ENOTSPD, RD_EZERODIAG, RD_ECUDA, RD_ENCCL, RD_EDEGENERATE = range(8)
+RD_GS_SPECULATION_MISS = 0x5EC  # rd_gpu_synchronize after asynchronous speculative sweeps: rerun exactly
 
 TARGETS = {"smooth": 0, "box": 1, "nonzero_bc": 2, "ball": 3, "sine_random": 4, "zero": 5, "one": 6,
            "quadratic": 7}
@@ -52,8 +53,12 @@ class RdCudaError(RdError):
     pass
 
 
+class RdSpeculationMiss(RdError):
+    """An asynchronous speculative lattice sweep left the division fast path: rerun exactly."""
+
+
 _EXC = {RD_EINVAL: RdInvalidArgument, RD_ENOTSPD: RdNotSpdError, RD_EZERODIAG: RdZeroDiagonalError,
-        RD_EDEGENERATE: RdDegenerateTetError, RD_ECUDA: RdCudaError}
+        RD_EDEGENERATE: RdDegenerateTetError, RD_ECUDA: RdCudaError, RD_GS_SPECULATION_MISS: RdSpeculationMiss}
 
 _P = C.c_void_p
 _I = C.c_int
@@ -124,6 +129,19 @@ def lib():
         "rd_gpu_pcg": (_I, [_P, _P, _P, _P, _D, _I, _P, _P, _P]),
         "rd_gpu_solve_system_amg": (_I, [_P, _P, _P, _D, _P, _P]),
         "rd_gpu_error_norms": (_I, [_P, _P, _P, _P, _D, C.POINTER(_D), C.POINTER(_D)]),
+        # distributed (z-slab) pieces, dist.py
+        "rd_gpu_ctx_set_exact_sweeps": (_I, [_P, _I]),
+        "rd_gpu_csr_rowblock": (_I, [_P, _P, _I, _I, _I, _I, C.POINTER(_P)]),
+        "rd_gpu_residual": (_I, [_P, _P, _P, _P, _P]),
+        "rd_gpu_prolong_add": (_I, [_P, _P, _P, _P]),
+        "rd_gpu_dot_async": (_I, [_P, _I, _P, _P, _P]),
+        "rd_gpu_pcg_update_xr": (_I, [_P, C.c_int64, _D, _P, _P, _P, _P]),
+        "rd_gpu_pcg_update_p": (_I, [_P, C.c_int64, _D, _P, _P]),
+        "rd_gpu_amg_apply_from": (_I, [_P, _I, _P, _P]),
+        "rd_gpu_slab_create": (_I, [_P, _P, _I, _I, C.POINTER(_P)]),
+        "rd_gpu_slab_free": (None, [_P]),
+        "rd_gpu_slab_info": (_I, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
+        "rd_gpu_slab_sweep": (_I, [_P, _I, _P, _P, _P, _P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
