@@ -47,6 +47,12 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile", action="store_true", help="short run for ncu: 1 step, no extras")
+    p.add_argument("--mode", default="exact", choices=["exact", "block"],
+                   help="N > 1: smoother hand-off between slabs (exact = the single-GPU sweep bit for bit)")
+    p.add_argument("--gather-rows", dest="gather_rows", type=int, default=262144,
+                   help="N > 1: levels with at most this many rows run whole on rank 0")
+    p.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of slabs")
+    p.add_argument("--dist", action="store_true", help="run the slab-distributed path even at N = 1")
     return p.parse_args()
 
 
@@ -127,6 +133,144 @@ def job_rate(elapsed_ms, work, world, device=None):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         torch.distributed.all_reduce(wk, op=torch.distributed.ReduceOp.SUM)
     return float(t.item()), float(wk.item()) / (float(t.item()) / 1e3)
+
+
+# ---------------------------------------------------------------------------- ours, N > 1
+def run_dist(args, rank, world, local_rank):
+    """N > 1: the C2 solve cut into z-slabs across the ranks (dist.py):
+    one step = build_system + build_amg (replicated) + slab localisation + the distributed
+    PCG (NCCL halo planes, rank-ordered dot sums, coarse levels on rank 0).  The total work
+    is fixed as N grows: strong scaling."""
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.Stream(dev)  # rd kernels, torch copies and NCCL waits all order on it
+    with torch.cuda.stream(stream):
+        return _run_dist(args, rank, world, local_rank, dev, stream)
+
+
+def _run_dist(args, rank, world, local_rank, dev, stream):
+    import torch
+
+    from paper_2102_03515_b200 import rd
+    from paper_2102_03515_b200.dist import DeviceOps, DistSolver, TorchComm
+
+    ctx = rd.Context(local_rank, stream.cuda_stream)
+    comm = TorchComm()
+    n = args.n
+    rho = rho_for(n)
+    mesh = rd.build_structured_cube(n, ctx)
+    ctx.synchronize()
+    last = {}
+
+    def step():
+        ops = DeviceOps(n, rho, args.target, ctx=ctx, device=local_rank, mesh=mesh)
+        solver = DistSolver(comm, ops, gather_rows=args.gather_rows, mode=args.mode)
+        res = solver.pcg(TOL, 500)
+        last.update(ops=ops, solver=solver, res=res)
+        return ops.rows[0], res
+
+    def barrier():
+        torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    l0 = ctx.launch_count
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    its = []
+    for _ in range(args.steps):
+        ndofs, res = step()
+        assert res.converged
+        its.append(res.iterations)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launch_count - l0
+    # every rank solved the same system: the job's work is counted once (strong scaling)
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    value = float(ndofs) * sum(its) / (elapsed_ms / 1e3)
+    solver = last["solver"]
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated Kuhn lattice, ball target, seeded)",
+        "config": {"workload": f"C2 cut into {world} z-slabs: build_system + build_amg (replicated) + "
+                               f"distributed pcg, n={n} ({ndofs} dofs), rho=h^2, {args.target} target, rtol {TOL}",
+                   "n": n, "n_dofs": ndofs, "rho": rho, "target": args.target, "tol": TOL,
+                   "parallelism": f"z-slabs x{world} ({args.mode} smoother hand-off), "
+                                  f"{solver.G} distributed level(s), coarse tail on rank 0",
+                   "slab_cuts": solver.plan.cuts,
+                   "l2": "inputs exceed L2 (device mesh 255 MB, A 364 MB > 126 MB L2); no flush"},
+        "iterations": its[0],
+        "clocks": clk,
+        "gpu_launches": launches,
+        "exchanges_per_iteration": {"halo_planes": "1 per face before SpMV/residual/restriction/"
+                                                   "prolongation/smoother", "dot_bytes": 16 * world,
+                                    "plane_bytes": 8 * (n - 1) ** 2},
+    }
+    # the dominant kernel on this rank: its level-0 slab forward sweep, timed alone
+    ops = last["ops"]
+    lo, hi = solver.plan.owned(0, rank)
+    P = (n - 1) ** 2
+    rows = (hi - lo) * P
+    f = ops.f_local
+    xin = torch.rand_like(f)
+    xo = torch.empty_like(f)
+    for _ in range(3):
+        ops.sweep(0, True, f, xin, xo, None)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    R = 20
+    for _ in range(R):
+        ops.sweep(0, True, f, xin, xo, None)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / R
+    Zs = ops.blkA[0].nnz
+    by = 8 * Zs + 4 * (rows + 1) + 24 * rows
+    peak, peak_kind = peaks()
+    result["roofline"] = {"kernel": f"slab gs_sweep level 0 (rank 0: planes [{lo}, {hi}))", "bound": "hbm",
+                          "achieved": by / (ms * 1e-3) / 1e9, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                          "frac": by / (ms * 1e-3) / 1e9 / peak, "traffic": None, "bytes_per_launch": by,
+                          "launch_ms": ms}
+    # e2e: the same distributed solve, u gathered on rank 0 and read back to pinned host memory
+    u_host = torch.empty(ndofs, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        nd, res = step()
+        full = last["solver"].gather_solution(res.x_local)
+        if rank == 0:
+            u_host.copy_(full)
+        return res.iterations
+
+    e2e_step()
+    barrier()
+    torch.cuda.synchronize()
+    a.record(stream)
+    e2e_its = [e2e_step() for _ in range(args.steps)]
+    b.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    result["e2e"] = {"value": float(ndofs) * sum(e2e_its) / (e2e_ms / 1e3), "unit": UNIT,
+                     "ms_per_step": e2e_ms / args.steps, "h2d_bytes_per_step": 0,
+                     "d2h_bytes_per_step": int(8 * ndofs),
+                     "path": "device-generated mesh -> distributed solve -> u gathered on rank 0 -> pinned host"}
+    return result
 
 
 # ---------------------------------------------------------------------------- ours
@@ -400,20 +544,33 @@ def main():
         # the CPU reference arm runs on rank 0 alone; the other ranks exit without work
         if rank != 0:
             return
-    if world > 1 and args.impl == "ours":
+    use_pg = args.impl == "ours" and (world > 1 or args.dist)
+    if use_pg:
+        import socket
+
         import torch
 
+        if world == 1:  # a one-rank group for --dist at N = 1
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(port))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         backend = "nccl" if torch.cuda.is_available() else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group(backend=backend)
     if args.impl == "reference":
         res = run_reference(args, rank, world)
+    elif (world > 1 and not args.replicas) or args.dist:
+        res = run_dist(args, rank, world, local_rank)
     else:
         res = run_ours(args, rank, world, local_rank)
     if rank == 0 and res is not None:
         print(json.dumps(res), flush=True)
-    if world > 1 and args.impl == "ours":
+    if use_pg:
         import torch
 
         torch.distributed.destroy_process_group()

@@ -202,13 +202,17 @@ class DeviceOps:
     when the context is created here, so torch copies and NCCL waits order with it.
     """
 
-    def __init__(self, n: int, rho: float, target: str = "ball", seed: int = 0, ctx=None, device: int = 0):
+    def __init__(self, n: int, rho: float, target: str = "ball", seed: int = 0, ctx=None, device: int = 0,
+                 mesh=None):
         from . import rd
 
         self.rd = rd
         self.device = torch.device("cuda", device)
-        self.ctx = ctx or rd.Context(device, torch.cuda.current_stream(self.device).cuda_stream)
-        self.mesh = rd.build_structured_cube(n, self.ctx)
+        if ctx is None and mesh is None:
+            # order with torch's current stream (handle 0 = the legacy default stream: cudaStreamLegacy)
+            ctx = rd.Context(device, torch.cuda.current_stream(self.device).cuda_stream or 1)
+        self.ctx = ctx or mesh.ctx
+        self.mesh = mesh if mesh is not None else rd.build_structured_cube(n, self.ctx)
         self.sys = rd.build_system(self.mesh, rho, target, seed)
         self.A = self.sys.A
         self.h = rd.build_amg(self.A)
