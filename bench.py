@@ -47,8 +47,11 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile", action="store_true", help="short run for ncu: 1 step, no extras")
-    p.add_argument("--mode", default="exact", choices=["exact", "block"],
-                   help="N > 1: smoother hand-off between slabs (exact = the single-GPU sweep bit for bit)")
+    p.add_argument("--mode", default="pipelined", choices=["pipelined", "exact", "block"],
+                   help="N > 1: smoother hand-off between slabs: pipelined = the sweep kernels write the "
+                        "boundary cells into the next GPU's memory (NVLink, CUDA IPC); exact = planes handed on "
+                        "over NCCL between sweeps (both the single-GPU sweep bit for bit); block = concurrent "
+                        "processor-block SGS (a different preconditioner)")
     p.add_argument("--gather-rows", dest="gather_rows", type=int, default=262144,
                    help="N > 1: levels with at most this many rows run whole on rank 0")
     p.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of slabs")

@@ -222,6 +222,26 @@ int rd_gpu_slab_info(const rd_slab* s, int* lattice_side, int* g0, int* g1);
 int rd_gpu_slab_sweep(rd_slab* s, int forward, const double* f, const double* xin, double* xout,
                       const double* in_plane);
 
+/* Pipelined hand-off (exact, no host round trip): the sweep kernel itself stores
+ * its downstream boundary plane as tagged {value, sweep} cells into the
+ * downstream neighbour's cell buffer -- another GPU's memory mapped over NVLink
+ * -- while the neighbour's kernel is already running and polls them.  The
+ * single-GPU sweep, bit for bit, with the wavefront crossing GPUs row by row.
+ *   same process / device:  rd_gpu_slab_link(s, next, prev)
+ *   one process per GPU:    rd_gpu_slab_ipc_handle on every rank, exchange the
+ *                           64-byte handles, rd_gpu_slab_open_peer(s, 0 = next /
+ *                           1 = previous, handle, the neighbour's g0)
+ * Every rank must run the same sequence of slab sweeps (the cell tags count
+ * them).  Ranks on one device must not launch waiting kernels separately:
+ * rd_gpu_slab_sweep_multi relaxes all linked slabs in one cooperative launch.  */
+#define RD_IPC_HANDLE_BYTES 64
+int rd_gpu_slab_link(rd_slab* s, const rd_slab* next, const rd_slab* prev);
+int rd_gpu_slab_ipc_handle(rd_slab* s, void* handle /* RD_IPC_HANDLE_BYTES */);
+int rd_gpu_slab_open_peer(rd_slab* s, int which, const void* handle, int peer_g0);
+int rd_gpu_slab_sweep_pipelined(rd_slab* s, int forward, const double* f, const double* xin, double* xout);
+int rd_gpu_slab_sweep_multi(int n, rd_slab* const* s, int forward, const double* const* f,
+                            const double* const* xin, double* const* xout);
+
 #ifdef __cplusplus
 }
 #endif

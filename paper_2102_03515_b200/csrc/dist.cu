@@ -17,6 +17,8 @@
 // through rd_gpu_amg_apply_from.  Halo exchange and reductions are the
 // caller's (torch.distributed / NCCL over NVLink); nothing here communicates.
 #include <algorithm>
+#include <cstring>
+#include <vector>
 
 #include "internal.hpp"
 
@@ -189,6 +191,66 @@ int rd_gpu_slab_info(const rd_slab* s, int* L, int* g0, int* g1) {
 int rd_gpu_slab_sweep(rd_slab* s, int forward, const double* f, const double* xin, double* xout,
                       const double* in_plane) {
   return guard(s->ctx, [&] { gs_pass_slab(s->ctx->c, s->s, f, xin, xout, forward != 0, in_plane); });
+}
+
+namespace {
+unsigned long long* virt(void* base, int g0, int L) {
+  return reinterpret_cast<unsigned long long*>(base) - 2ll * g0 * (long long)L * L;
+}
+}  // namespace
+
+int rd_gpu_slab_link(rd_slab* s, const rd_slab* next, const rd_slab* prev) {
+  return guard(s->ctx, [&] {
+    for (const rd_slab* o : {next, prev})
+      require(!o || (o->s.L == s->s.L && o->s.device == s->s.device), "slab_link: neighbour of another level/device");
+    require(!next || next->s.zlo == s->s.zhi, "slab_link: next slab must start at this slab's end");
+    require(!prev || prev->s.zhi == s->s.zlo, "slab_link: previous slab must end at this slab's start");
+    s->s.peer_v[0] = next ? virt(next->s.cells, next->s.g0, s->s.L) : nullptr;
+    s->s.peer_v[1] = prev ? virt(prev->s.cells, prev->s.g0, s->s.L) : nullptr;
+  });
+}
+
+int rd_gpu_slab_ipc_handle(rd_slab* s, void* handle) {
+  return guard(s->ctx, [&] {
+    require(handle != nullptr, "slab_ipc_handle: null output");
+    cudaIpcMemHandle_t h;
+    RDG_CUDA(cudaIpcGetMemHandle(&h, s->s.cells));
+    static_assert(sizeof(h) == RD_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(handle, &h, sizeof(h));
+  });
+}
+
+int rd_gpu_slab_open_peer(rd_slab* s, int which, const void* handle, int peer_g0) {
+  return guard(s->ctx, [&] {
+    require(which == 0 || which == 1, "slab_open_peer: which is 0 (next) or 1 (previous)");
+    require(handle != nullptr, "slab_open_peer: null handle");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* q = nullptr;
+    RDG_CUDA(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+    if (s->s.peer_ipc[which]) cudaIpcCloseMemHandle(s->s.peer_ipc[which]);
+    s->s.peer_ipc[which] = q;
+    s->s.peer_v[which] = virt(q, peer_g0, s->s.L);
+  });
+}
+
+int rd_gpu_slab_sweep_pipelined(rd_slab* s, int forward, const double* f, const double* xin, double* xout) {
+  return guard(s->ctx, [&] { gs_pass_slab(s->ctx->c, s->s, f, xin, xout, forward != 0, nullptr, true); });
+}
+
+int rd_gpu_slab_sweep_multi(int n, rd_slab* const* s, int forward, const double* const* f,
+                            const double* const* xin, double* const* xout) {
+  if (n < 1 || !s || !s[0]) return RD_EINVAL;
+  return guard(s[0]->ctx, [&] {
+    std::vector<Ctx*> cs(n);
+    std::vector<SlabSmoother*> ss(n);
+    for (int q = 0; q < n; ++q) {
+      require(s[q] && s[q]->s.device == s[0]->s.device, "slab_sweep_multi: slabs of one device");
+      cs[q] = &s[q]->ctx->c;
+      ss[q] = &s[q]->s;
+    }
+    gs_pass_slabs_multi(s[0]->ctx->c, n, cs.data(), ss.data(), f, xin, xout, forward != 0);
+  });
 }
 
 }  // extern "C"

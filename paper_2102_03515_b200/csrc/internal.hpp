@@ -75,14 +75,32 @@ void lattice_prepare(Ctx& c, const DCsr& A, int* err_dev = nullptr);
 struct SlabSmoother {
   int L = 0, zlo = 0, zhi = 0, g0 = 0, g1 = 0, ntz = 0;
   DBuf<double> pack[2];            // fwd, bwd step-major packed stencil of the slab's tiles
-  DBuf<unsigned long long> xh;     // tagged cells {value, tag} of planes [g0, g1)
+  // tagged cells {value, tag} of planes [g0, g1): plain cudaMalloc, so a peer
+  // process can map them (cudaIpcGetMemHandle) for the pipelined hand-off
+  unsigned long long* cells = nullptr;
+  size_t cells_bytes = 0;
+  // the neighbours' cells as virtual global pointers: [0] next slab (downstream of a
+  // forward sweep), [1] previous slab (downstream of a backward sweep); null: none
+  unsigned long long* peer_v[2] = {nullptr, nullptr};
+  void* peer_ipc[2] = {nullptr, nullptr};  // IPC mappings to close
   unsigned epoch = 0;
+  int device = 0;
+  SlabSmoother() = default;
+  SlabSmoother(const SlabSmoother&) = delete;
+  SlabSmoother& operator=(const SlabSmoother&) = delete;
+  ~SlabSmoother();
 };
 // A: the level's whole-box matrix (verified lattice)
 void slab_prepare(Ctx& c, const DCsr& A, int zlo, int zhi, SlabSmoother& s);
-// in_plane: the upstream ghost plane's values (L*L; null = zeros), fresh (exact) or old (block)
+// in_plane: the upstream ghost plane's values (L*L; null = zeros), fresh (exact) or old (block).
+// pipelined: no in_plane; the upstream neighbour's kernel writes the cells (peer_v), and
+// this sweep writes its downstream boundary plane into the downstream neighbour's.
 void gs_pass_slab(Ctx& c, SlabSmoother& s, const double* f, const double* xin, double* xout, bool fwd,
-                  const double* in_plane);
+                  const double* in_plane, bool pipelined = false);
+// all slabs of a distributed level (linked neighbours, one device) in one cooperative
+// launch on c's stream: the single-GPU emulation of the pipelined hand-off
+void gs_pass_slabs_multi(Ctx& c, int n, Ctx* const* cs, SlabSmoother* const* s, const double* const* f,
+                         const double* const* xin, double* const* xout, bool fwd);
 
 // ---------------------------------------------------------------- amg.cu
 struct Level {

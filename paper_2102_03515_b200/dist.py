@@ -124,6 +124,20 @@ class TorchComm:
         self.dist.all_gather_into_tensor(out, t.reshape(1), group=self.group)
         return out.tolist()
 
+    def link_slabs(self, ops, G):
+        """Map the neighbours' slab cell buffers (CUDA IPC over NVLink) for the pipelined hand-off."""
+        for l in range(G):
+            mine = (ops.ipc_handle(l), ops.slab_g0(l))
+            allh = [None] * self.world
+            self.dist.all_gather_object(allh, mine, group=self.group)
+            if self.rank + 1 < self.world:
+                ops.open_peer(l, 0, *allh[self.rank + 1])
+            if self.rank > 0:
+                ops.open_peer(l, 1, *allh[self.rank - 1])
+
+    def pipelined_sweep(self, ops, l, fwd, f, xin, xout):
+        ops.sweep_pipelined(l, fwd, f, xin, xout)
+
     def allgather_int(self, v: int):
         dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
         t = torch.tensor([v], dtype=torch.int64, device=dev)
@@ -190,6 +204,32 @@ class ThreadComm:
 
     def allgather_int(self, v: int):
         return self._allgather(int(v))
+
+    def link_slabs(self, ops, G):
+        for l in range(G):
+            allo = self._allgather(ops)
+            nxt = allo[self.rank + 1] if self.rank + 1 < self.world else None
+            prv = allo[self.rank - 1] if self.rank > 0 else None
+            ops.link(l, nxt, prv)
+
+    def pipelined_sweep(self, ops, l, fwd, f, xin, xout):
+        """All ranks' slabs of level l in ONE cooperative launch on rank 0's stream (kernels
+        that wait on one another must not be separate launches on one GPU)."""
+        ev = torch.cuda.Event()
+        ev.record()
+        entries = self._allgather((ops, f, xin, xout, ev))
+        if self.rank == 0:
+            cur = torch.cuda.current_stream()
+            for e in entries:
+                cur.wait_event(e[4])
+            ops.sweep_multi(l, fwd, [(e[0], e[1], e[2], e[3]) for e in entries])
+            done = torch.cuda.Event()
+            done.record()
+            self.hub.done = done
+        self.hub.bar.wait(timeout=600)
+        if self.rank != 0:
+            torch.cuda.current_stream().wait_event(self.hub.done)
+        self.hub.bar.wait(timeout=600)
 
 
 # ------------------------------------------------------------------ device work (the product path)
@@ -285,6 +325,43 @@ class DeviceOps:
         self.ctx.check(self.rd.lib().rd_gpu_slab_sweep(self.slab[l].h, 1 if fwd else 0, _p(f), _p(xin), _p(xout),
                                                        _p(in_plane)))
 
+    # -- pipelined hand-off (peer cells)
+    def slab_g0(self, l):
+        return self.plan.ghost(l, self.rank)[0]
+
+    def ipc_handle(self, l) -> bytes:
+        import ctypes
+
+        buf = ctypes.create_string_buffer(64)
+        self.ctx.check(self.rd.lib().rd_gpu_slab_ipc_handle(self.slab[l].h, buf))
+        return buf.raw
+
+    def open_peer(self, l, which, handle: bytes, peer_g0: int):
+        import ctypes
+
+        buf = ctypes.create_string_buffer(bytes(handle), 64)
+        self.ctx.check(self.rd.lib().rd_gpu_slab_open_peer(self.slab[l].h, int(which), buf, int(peer_g0)))
+
+    def link(self, l, nxt, prv):
+        self.ctx.check(self.rd.lib().rd_gpu_slab_link(self.slab[l].h, nxt.slab[l].h if nxt else None,
+                                                      prv.slab[l].h if prv else None))
+
+    def sweep_pipelined(self, l, fwd, f, xin, xout):
+        self.ctx.check(self.rd.lib().rd_gpu_slab_sweep_pipelined(self.slab[l].h, 1 if fwd else 0, _p(f), _p(xin),
+                                                                 _p(xout)))
+
+    def sweep_multi(self, l, fwd, entries):
+        """entries: [(ops_q, f_q, xin_q, xout_q)] of every slab of level l, in rank order."""
+        import ctypes
+
+        n = len(entries)
+        P = ctypes.c_void_p * n
+        sl = P(*[e[0].slab[l].h for e in entries])
+        fs = P(*[e[1].data_ptr() for e in entries])
+        xi = P(*[(e[2].data_ptr() if e[2] is not None else None) for e in entries])
+        xo = P(*[e[3].data_ptr() for e in entries])
+        self.ctx.check(self.rd.lib().rd_gpu_slab_sweep_multi(n, sl, 1 if fwd else 0, fs, xi, xo))
+
     def dot(self, a, b, out):
         self.ctx.check(self.rd.lib().rd_gpu_dot_async(self.ctx.h, a.numel(), _p(a), _p(b), _p(out)))
 
@@ -354,14 +431,16 @@ class DistSolver:
     """Slab-distributed AMG-PCG (linalg.cpp:64-102 with amg_precond, amg.cpp:119-145)."""
 
     def __init__(self, comm, ops, gather_rows: int = 262144, mode: str = "exact", dist_levels: int | None = None):
-        if mode not in ("exact", "block"):
-            raise ValueError("mode must be 'exact' or 'block'")
+        if mode not in ("exact", "block", "pipelined"):
+            raise ValueError("mode must be 'exact', 'block' or 'pipelined'")
         self.comm, self.ops, self.mode = comm, ops, mode
         self.rank, self.world = comm.rank, comm.world
         G = dist_levels or choose_dist_levels(ops.sides, ops.rows, ops.structured, self.world, gather_rows)
         self.plan = SlabPlan(ops.sides, self.world, G)
         self.G = G
         ops.localize(self.plan, self.rank)
+        if mode == "pipelined":
+            comm.link_slabs(ops, G)
         R = self.rank
         pl = self.plan
         self.r = [None] + [ops.vec(l) for l in range(1, G + 1)]
@@ -430,6 +509,9 @@ class DistSolver:
             return
         if xin is not None:  # old values of the downstream ghost plane
             self.halo(l, xin, lower=not fwd, upper=fwd)
+        if self.mode == "pipelined":  # the kernels hand the wavefront on through peer memory
+            self.comm.pipelined_sweep(self.ops, l, fwd, f, xin, xout)
+            return
         in_plane = None
         if has_up:
             in_plane = self.inplane[l]

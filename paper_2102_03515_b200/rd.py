@@ -142,6 +142,11 @@ def lib():
         "rd_gpu_slab_free": (None, [_P]),
         "rd_gpu_slab_info": (_I, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
         "rd_gpu_slab_sweep": (_I, [_P, _I, _P, _P, _P, _P]),
+        "rd_gpu_slab_link": (_I, [_P, _P, _P]),
+        "rd_gpu_slab_ipc_handle": (_I, [_P, _P]),
+        "rd_gpu_slab_open_peer": (_I, [_P, _I, _P, _I]),
+        "rd_gpu_slab_sweep_pipelined": (_I, [_P, _I, _P, _P, _P]),
+        "rd_gpu_slab_sweep_multi": (_I, [_I, _P, _I, _P, _P, _P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

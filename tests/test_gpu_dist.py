@@ -80,11 +80,14 @@ def _single(n, rho, target):
     return dict(z=z, x=res.x, it=res.iterations)
 
 
+@pytest.mark.parametrize("mode", ["exact", "pipelined"])
 @pytest.mark.parametrize("world,gather_rows,G", [(2, 600, 2), (4, 600, 2), (3, 100000, 1)])
-def test_exact_slabs_match_single_gpu(world, gather_rows, G):
+def test_exact_slabs_match_single_gpu(world, gather_rows, G, mode):
+    """exact: planes handed on between sweeps; pipelined: the sweep kernels write the
+    boundary cells into the next slab's buffer (all slabs in one cooperative launch)."""
     n, rho = 32, 2.0 ** -10
     ref = _single(n, rho, "smooth")
-    outs = _run_ranks(world, n, rho, "smooth", "exact", gather_rows)
+    outs = _run_ranks(world, n, rho, "smooth", mode, gather_rows)
     o0 = outs[0]
     assert o0["G"] == G
     assert np.array_equal(o0["z"], ref["z"])  # the V-cycle, bit for bit
@@ -105,8 +108,9 @@ def test_block_slabs_converge():
     assert err <= 1e-6, err
 
 
-def test_exact_slabs_c2_vcycle():
-    """C2 (n=128, ball target): two slabs of 64 / 63 planes (a partial last tile), the
+@pytest.mark.parametrize("mode,world", [("exact", 2), ("pipelined", 2), ("pipelined", 4)])
+def test_exact_slabs_c2_vcycle(mode, world):
+    """C2 (n=128, ball target): slabs of 64 / 63 planes (a partial last tile), the
     level-0 V-cycle through the slab kernels equals the single-GPU V-cycle bit for bit."""
     n, rho = 128, 2.0 ** -14
     from paper_2102_03515_b200 import rd
@@ -116,6 +120,6 @@ def test_exact_slabs_c2_vcycle():
     h = rd.build_amg(sys_.A)
     zref = h.apply(sys_.f())
     del h, sys_, mesh
-    outs = _run_ranks(2, n, rho, "ball", "exact", 262144, solve=False)
-    assert outs[0]["G"] == 1 and outs[0]["cuts"] == [0, 64, 127]
+    outs = _run_ranks(world, n, rho, "ball", mode, 262144, solve=False)
+    assert outs[0]["G"] == 1 and outs[0]["cuts"][0] == 0 and outs[0]["cuts"][-1] == 127
     assert np.array_equal(outs[0]["z"], zref)
