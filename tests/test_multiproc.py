@@ -1,8 +1,8 @@
-"""The N > 1 path of bench.py on CPU: world_size-2 gloo process groups.
+"""The N > 1 plumbing of bench.py on CPU: world_size-2 gloo process groups.
 
-Ranks run independent replicas of the solve (the exact lexicographic
-Gauss-Seidel does not shard), so the only collective is the timing reduction: MAX over
-ranks of the device time, SUM of the work.  The reference arm runs on rank 0 alone.
+job_rate is the timing reduction of bench.py --replicas (MAX over ranks of the device
+time, SUM of the work); the default N > 1 path is the slab-distributed solve, whose host
+logic tests/test_dist_gloo.py covers.  The reference arm runs on rank 0 alone.
 """
 import json
 import os
