@@ -383,7 +383,14 @@ def run_ours(args, rank, world, local_rank):
         level_sweeps.append({"level": l, "rows": Al.rows, "nnz": Al.nnz, "fwd_ms": fw, "bwd_ms": bw})
     spmv_ms = timed(lambda: rd.lib().rd_gpu_spmv(ctx.h, s.A.h, rd._ptr(x), rd._ptr(y)))
     structured = h.structured(0)
-    gs_bytes = (8 * Z + 4 * (N + 1) + 24 * N) if structured else (12 * Z + 28 * N + 4)
+    uniform = h.uniform(0)
+    # SURVEY.md 8(d) algorithmic bytes of a GS sweep (the CSR formulation: values, columns, row
+    # pointers, f, x in, x out).  The structured kernel moves far less (uniform stencil: the row
+    # is held in registers, ~24 B/row move) -- the DRAM traffic in `traffic` shows it -- so the
+    # sweep is bounded by its wavefront depth, reported alongside as dag_steps / us_per_step.
+    gs_bytes = 12 * Z + 28 * N + 4
+    L0 = round(N ** (1.0 / 3.0))
+    dag_steps = 3 * (L0 - 1) + 1
     spmv_bytes = 12 * Z + 20 * N + 4
     peak, peak_kind = peaks()
     traffic = load_profile_traffic()
@@ -396,6 +403,8 @@ def run_ours(args, rank, world, local_rank):
         "bound": "hbm", "achieved": gs_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
         "frac": gs_gbs / peak, "traffic": traffic.get("gs_sweep"),
         "bytes_per_launch": gs_bytes, "launch_ms": gs_ms, "share_of_step_est": share,
+        "stencil": "uniform (in registers)" if uniform else ("packed stream" if structured else "CSR"),
+        "dag_steps": dag_steps, "us_per_step": 1e3 * gs_ms / dag_steps,
     }
     # per kernel class: algorithmic bytes / measured time, vs measured and spec HBM
     nl = h.num_levels
@@ -428,6 +437,7 @@ def run_ours(args, rank, world, local_rank):
         "levels": h.num_levels,
         "level_sweeps": level_sweeps,
         "structured_levels": [bool(h.structured(l)) for l in range(h.num_levels - 1)],
+        "uniform_levels": [bool(h.uniform(l)) for l in range(h.num_levels - 1)],
     }
     del h, s
 

@@ -136,7 +136,8 @@ int rd_gpu_amg_num_levels(const rd_amg* h);
 const rd_csr* rd_gpu_amg_level_matrix(const rd_amg* h, int level, int which);
 /* coarse_flag of level l (1 = C), host buffer of rows(A_l) bytes */
 int rd_gpu_amg_level_flags(const rd_amg* h, int level, uint8_t* flags);
-/* 1 if level l runs the structured (lattice-stencil) smoother, 0 for the generic one */
+/* level l's smoother: 0 generic, 1 structured lattice kernel streaming the packed stencil,
+ * 2 structured with the uniform stencil held in registers (every row = the centre row) */
 int rd_gpu_amg_level_structured(const rd_amg* h, int level);
 /* replaces rd::amg_apply(h, r) / amg_precond(h)          amg.hpp:39-42, amg.cpp:119-145 */
 int rd_gpu_amg_apply(rd_amg* h, const double* r, double* z);

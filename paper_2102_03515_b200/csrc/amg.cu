@@ -852,6 +852,11 @@ bool build_levels(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, boo
   }
   std::vector<int> f(kMaxLat + nerr);
   RDG_CUDA(cudaMemcpyAsync(f.data(), flags_dev.p, sizeof(int) * f.size(), cudaMemcpyDeviceToHost, c.stream));
+  std::vector<int> uni(h.levels.size(), -1);  // smoother stencil uniformity, read with the same sync
+  for (size_t l = 0; l < h.levels.size(); ++l)
+    if (h.levels[l].A.lat_uni_state == -2)
+      RDG_CUDA(cudaMemcpyAsync(&uni[l], h.levels[l].A.lat_uni_flag.p, sizeof(int), cudaMemcpyDeviceToHost,
+                               c.stream));
   RDG_CUDA(cudaStreamSynchronize(c.stream));
   for (int l = 0; l < nlat; ++l)
     if (f[l]) return false;  // a lattice A_c lost the 15-point pattern: rebuild exactly
@@ -860,6 +865,8 @@ bool build_levels(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, boo
     if (f[kMaxLat + l] == 2) throw Error(RD_EZERODIAG, "sgs_sweep: zero diagonal");
     if (f[kMaxLat + l]) throw Error(RD_ERUNTIME, "lattice smoother: pattern/layout mismatch");
   }
+  for (size_t l = 0; l < h.levels.size(); ++l)
+    if (uni[l] >= 0) lattice_resolve(c, h.levels[l].A, uni[l]);  // packs only for non-uniform levels
   return true;
 }
 }  // namespace

@@ -447,7 +447,8 @@ int rd_gpu_amg_level_flags(const rd_amg* h, int level, uint8_t* flags) {
 
 int rd_gpu_amg_level_structured(const rd_amg* h, int level) {
   if (!h || level < 0 || level >= (int)h->h.levels.size()) return -1;
-  return h->h.levels[level].A.lat.ok ? 1 : 0;
+  const DCsr& A = h->h.levels[level].A;
+  return A.lat.ok ? (A.lat_uni_state == 1 ? 2 : 1) : 0;
 }
 
 int rd_gpu_amg_apply(rd_amg* h, const double* r, double* z) {

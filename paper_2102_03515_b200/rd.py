@@ -493,7 +493,11 @@ class AmgHierarchy:
         return f[: A.rows]
 
     def structured(self, l: int) -> bool:
-        return lib().rd_gpu_amg_level_structured(self.h, int(l)) == 1
+        return lib().rd_gpu_amg_level_structured(self.h, int(l)) >= 1
+
+    def uniform(self, l: int) -> bool:
+        """Level l's lattice stencil is the same in every row (kept in registers by the smoother)."""
+        return lib().rd_gpu_amg_level_structured(self.h, int(l)) == 2
 
     def apply(self, r, z=None):
         """amg.hpp:39 amg_apply: one V-cycle, zero initial guess.  Host arrays in -> host array out;
