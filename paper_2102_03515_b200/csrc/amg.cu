@@ -852,6 +852,11 @@ bool build_levels(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, boo
   }
   std::vector<int> f(kMaxLat + nerr);
   RDG_CUDA(cudaMemcpyAsync(f.data(), flags_dev.p, sizeof(int) * f.size(), cudaMemcpyDeviceToHost, c.stream));
+  DBuf<int> tail_bad(1, c.stream);  // the one-CTA coarse tail's class check, read with the same sync
+  RDG_CUDA(cudaMemsetAsync(tail_bad.p, 0, sizeof(int), c.stream));
+  coarse_tail_prepare(c, h, tail_bad.p);
+  int tail_bad_h = 0;
+  RDG_CUDA(cudaMemcpyAsync(&tail_bad_h, tail_bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   std::vector<int> uni(h.levels.size(), -1);  // smoother stencil uniformity, read with the same sync
   for (size_t l = 0; l < h.levels.size(); ++l)
     if (h.levels[l].A.lat_uni_state == -2)
@@ -867,6 +872,7 @@ bool build_levels(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, boo
   }
   for (size_t l = 0; l < h.levels.size(); ++l)
     if (uni[l] >= 0) lattice_resolve(c, h.levels[l].A, uni[l]);  // packs only for non-uniform levels
+  if (tail_bad_h) h.tail_level = -1;
   return true;
 }
 }  // namespace
@@ -892,6 +898,14 @@ void vcycle(Ctx& c, Hierarchy& h, const double* r, double* z, double* dot_out, i
     if (dot_out) dot(c, h.nc, r, z, dot_out);
     return;
   }
+  const int ct = coarse_tail_level(c, h);
+  const int tl = ct >= 0 ? std::max(ct, l0) : -1;  // the one-CTA tail takes levels >= tl
+  if (tl == l0) {
+    coarse_tail(c, h, l0, r, z);
+    if (dot_out) dot(c, h.levels[l0].A.rows, r, z, dot_out);
+    return;
+  }
+  const int lend = tl >= 0 ? tl : L - 1;  // levels [l0, lend) smoothed here
   std::vector<const double*> rl(L);
   std::vector<double*> zl(L);
   rl[l0] = r;
@@ -900,7 +914,7 @@ void vcycle(Ctx& c, Hierarchy& h, const double* r, double* z, double* dot_out, i
     rl[l] = h.levels[l].r.p;
     zl[l] = h.levels[l].z.p;
   }
-  for (int l = l0; l + 1 < L; ++l) {
+  for (int l = l0; l < lend; ++l) {
     Level& lv = h.levels[l];
     const double* cur = nullptr;  // zero initial guess
     for (int s = 0; s < m; ++s) {
@@ -912,8 +926,11 @@ void vcycle(Ctx& c, Hierarchy& h, const double* r, double* z, double* dot_out, i
     residual(c, lv.A, rl[l], zl[l], lv.res.p);
     spmv(c, lv.Pt, lv.res.p, h.levels[l + 1].r.p);
   }
-  coarse_solve(c, h, rl[L - 1], zl[L - 1]);
-  for (int l = L - 2; l >= l0; --l) {
+  if (tl >= 0)
+    coarse_tail(c, h, tl, rl[tl], zl[tl]);
+  else
+    coarse_solve(c, h, rl[L - 1], zl[L - 1]);
+  for (int l = lend - 1; l >= l0; --l) {
     Level& lv = h.levels[l];
     prolong_add(c, lv.P, zl[l + 1], zl[l]);
     for (int s = 0; s < m; ++s) {

@@ -1,0 +1,392 @@
+// coarse_tail.cu -- the bottom of the V-cycle (amg.cpp:119-132) in ONE thread block.
+//
+// Below a 16^3 lattice level the multi-CTA smoother is all fixed cost: a launch,
+// a prologue and tile hand-offs for a wavefront of at most 46 steps.  From the
+// first such level down, every operation of the V-cycle -- symmetric Gauss-Seidel
+// pre-smoothing, residual, restriction, the coarsest dense LLT solve,
+// prolongation, post-smoothing -- runs in a single CTA with all vectors resident
+// in shared memory and one __syncthreads between dependent steps:
+//
+//  * Gauss-Seidel in place on the shared-memory x, one thread per x-line, as a
+//    wavefront over a + y + z (reflected for the backward pass).  Rows of one
+//    wavefront step never couple on the 15-point stencil, rows of earlier steps
+//    already hold new values and rows of later steps old ones -- exactly the
+//    sequential relax(i) of amg.cpp:67-88, same operands in the same order;
+//  * matrix values row-major in slot order (the lattice stencil's ascending
+//    column order, absent slots predicated away), one 128-byte row per thread per
+//    step, prefetched a step ahead;
+//  * residual, P^T and P row by row, sums from +0 in column order as spmv does
+//    (linalg.cpp:19-33); the LLT substitutions in the order of llt_solve_kernel.
+//
+// Bit-identical to the multi-launch V-cycle; ~20 launches per V-cycle become one.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "internal.hpp"
+
+namespace rdg {
+namespace {
+
+constexpr int kTailNT = 256;
+constexpr int kTailMaxL = 16;  // lattice side: L^2 <= kTailNT lines
+
+struct TailLev {
+  int n, L;
+  const double* table;                              // [64][16] class rows (slot order, recip in 15)
+  const int* prp; const int* pci; const double* pv;  // P_l
+  const int* trp; const int* tci; const double* tv;  // Pt_l
+};
+
+struct TailParams {
+  int nlev;  // smoothed levels of the tail
+  TailLev lv[kTailMaxLevels];
+  int nc;
+  const double* Lc;
+  const double* r;
+  double* z;
+  int* err;
+  int m;  // smoothing steps
+  long long* clk;  // RD_TAIL_CLOCKS probes only: phase timestamps of thread 0
+};
+
+__device__ __forceinline__ unsigned tail_mask(int a, int y, int z, int L) {
+  const bool am = a > 0, ap = a < L - 1, ym = y > 0, yp = y < L - 1, zm = z > 0, zp = z < L - 1;
+  return (unsigned)(am && ym && zm) | (unsigned)(ym && zm) << 1 | (unsigned)(am && zm) << 2 | (unsigned)zm << 3 |
+         (unsigned)(am && ym) << 4 | (unsigned)ym << 5 | (unsigned)am << 6 | 1u << 7 | (unsigned)ap << 8 |
+         (unsigned)yp << 9 | (unsigned)(ap && yp) << 10 | (unsigned)zp << 11 | (unsigned)(ap && zp) << 12 |
+         (unsigned)(yp && zp) << 13 | (unsigned)(ap && yp && zp) << 14;
+}
+
+__device__ __forceinline__ void l2_prefetch(const void* src, unsigned bytes) {
+  if (bytes >= 16) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes & ~15u) : "memory");
+}
+
+// position class of a lattice coordinate: 0 first, 3 last, 2 second-to-last, 1 interior.
+// Every level's rows are equal within a class triple (checked at setup).
+__device__ __forceinline__ int pos_class(int t, int L) { return t == 0 ? 0 : t == L - 1 ? 3 : t == L - 2 ? 2 : 1; }
+
+
+extern __shared__ __align__(16) double tail_sm[];  // every vector of the tail (offsets below)
+
+// one Gauss-Seidel pass in place on x (shared), f (shared), the level's class
+// rows (tb, shared): nothing in the step loop touches global memory (a pending
+// global load would hold every step's __syncthreads).
+template <bool FWD>
+__device__ void tail_sweep(const TailLev& lv, int fo, int xo, int tbo, int* err) {
+  const double* f = tail_sm + fo;
+  double* x = tail_sm + xo;
+  const double* tb = tail_sm + tbo;
+  const int L = lv.L, P = L * L;
+  const int line = threadIdx.x;
+  const bool has = line < P;
+  const int y = has ? line % L : 0, z = has ? line / L : 0;
+  const int yo = FWD ? y : L - 1 - y, zo = FWD ? z : L - 1 - z;
+  const int base = (zo * L + yo) * L;
+  const int cyz = pos_class(yo, L) * 4 + pos_class(zo, L);
+  const int off[15] = {-1 - L - P, -L - P, -1 - P, -P, -1 - L, -L, -1, 0, 1, L, 1 + L, P, 1 + P, L + P, 1 + L + P};
+  const int steps = 3 * (L - 1) + 1;
+  for (int s = 0; s < steps; ++s) {
+    const int a = s - y - z;
+    if (has && a >= 0 && a < L) {
+      const int ao = FWD ? a : L - 1 - a;
+      const int i = base + ao;
+      const unsigned m = tail_mask(ao, yo, zo, L);
+      const double2* row = reinterpret_cast<const double2*>(tb + (pos_class(ao, L) * 16 + cyz) * 16);
+      double v[16];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double2 t = row[k];
+        v[2 * k] = t.x;
+        v[2 * k + 1] = t.y;
+      }
+      double sum = f[i];
+#pragma unroll
+      for (int k = 0; k < 15; ++k) {
+        if (k == 7) continue;
+        const bool pr = (m >> k) & 1u;  // branch-free: absent slots read x_i and keep the sum
+        const double t = __dsub_rn(sum, __dmul_rn(v[k], x[pr ? i + off[k] : i]));
+        sum = pr ? t : sum;
+      }
+      const double d = v[7];
+      if (d == 0.0) atomicCAS(err, 0, RD_EZERODIAG);
+      double q = div_fast(sum, d, v[15]);
+      if (!(sum == 0.0 || div_is_fast(sum, d, q))) q = __ddiv_rn(sum, d);
+      x[i] = sum == 0.0 ? __dmul_rn(sum, v[15]) : q;
+    }
+    __syncthreads();
+  }
+}
+
+// res = r - A z (the lattice rows), all in shared memory
+__device__ void tail_residual(const TailLev& lv, int ro, int zo, int reso, int tbo) {
+  const double* r = tail_sm + ro;
+  const double* z = tail_sm + zo;
+  double* res = tail_sm + reso;
+  const double* tb = tail_sm + tbo;
+  const int L = lv.L, P = L * L;
+  const int off[15] = {-1 - L - P, -L - P, -1 - P, -P, -1 - L, -L, -1, 0, 1, L, 1 + L, P, 1 + P, L + P, 1 + L + P};
+  for (int i = threadIdx.x; i < lv.n; i += kTailNT) {
+    const int a = i % L, y = (i / L) % L, zz = i / P;
+    const double* v = tb + ((pos_class(a, L) * 4 + pos_class(y, L)) * 4 + pos_class(zz, L)) * 16;
+    const unsigned m = tail_mask(a, y, zz, L);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 15; ++k) {
+      const bool pr = (m >> k) & 1u;
+      const double t = __dadd_rn(s, __dmul_rn(v[k], z[pr ? i + off[k] : i]));
+      s = pr ? t : s;
+    }
+    res[i] = __dsub_rn(r[i], s);
+  }
+}
+
+// y = M x for a CSR block in global memory (x, y shared), sums from +0
+__device__ void tail_spmv(int rows, const int* rp, const int* ci, const double* val, int xo, int yo, bool add) {
+  const double* x = tail_sm + xo;
+  double* y = tail_sm + yo;
+  for (int i = threadIdx.x; i < rows; i += kTailNT) {
+    double s = 0.0;
+    for (int k = __ldg(rp + i); k < __ldg(rp + i + 1); ++k) s = __dadd_rn(s, __dmul_rn(__ldg(val + k), x[__ldg(ci + k)]));
+    y[i] = add ? __dadd_rn(y[i], s) : s;
+  }
+}
+
+__global__ void __launch_bounds__(kTailNT, 1) coarse_tail_kernel(TailParams p) {
+  // layout (element offsets into tail_sm): per level k: r_k, z_k; then res, rc, Lc
+  auto ro = [&](int k) {
+    int o = 0;
+    for (int j = 0; j < k; ++j) o += 2 * p.lv[j].n;
+    return o;
+  };
+  auto zo = [&](int k) { return ro(k) + p.lv[k].n; };
+  int maxn = 0;
+  for (int k = 0; k < p.nlev; ++k) maxn = max(maxn, p.lv[k].n);
+  const int reso = ro(p.nlev), rco = reso + maxn, lo = rco + p.nc;
+  auto tbo = [&](int k) { return ((lo + p.nc * p.nc + 1) & ~1) + k * 64 * 16; };  // class rows (16-B aligned)
+  double* Rc = tail_sm + rco;
+  const double* Lm = tail_sm + lo;
+  const int tid = threadIdx.x;
+  int ck = 0;
+  auto mark = [&]() {
+    if (p.clk && tid == 0) p.clk[ck] = clock64();
+    ++ck;
+  };
+  mark();
+  // pull every level's row values and P / P^T into L2 first: between V-cycles the
+  // fine-level streams evict them, and a step is far shorter than an HBM miss
+  if (tid >= 32 && tid - 32 < p.nlev) {
+    const TailLev& lv = p.lv[tid - 32];
+    const unsigned np = (unsigned)lv.prp[lv.n];  // nnz(P) = nnz(P^T)
+    l2_prefetch(lv.pci, np * 4);
+    l2_prefetch(lv.pv, np * 8);
+    l2_prefetch(lv.tci, np * 4);
+    l2_prefetch(lv.tv, np * 8);
+  }
+  for (int i = tid; i < p.lv[0].n; i += kTailNT) tail_sm[i] = p.r[i];
+  for (int k = 0; k < p.nlev; ++k)
+    for (int i = tid; i < 64 * 16; i += kTailNT) tail_sm[tbo(k) + i] = __ldg(p.lv[k].table + i);
+  __syncthreads();
+  mark();
+  // ---- down: pre-smooth from zero, residual, restrict
+  for (int k = 0; k < p.nlev; ++k) {
+    const TailLev& lv = p.lv[k];
+    for (int i = tid; i < lv.n; i += kTailNT) tail_sm[zo(k) + i] = 0.0;
+    __syncthreads();
+    for (int s = 0; s < p.m; ++s) {
+      tail_sweep<true>(lv, ro(k), zo(k), tbo(k), p.err);
+      tail_sweep<false>(lv, ro(k), zo(k), tbo(k), p.err);
+    }
+    mark();
+    tail_residual(lv, ro(k), zo(k), reso, tbo(k));
+    __syncthreads();
+    mark();
+    tail_spmv(k + 1 < p.nlev ? p.lv[k + 1].n : p.nc, lv.trp, lv.tci, lv.tv, reso, k + 1 < p.nlev ? ro(k + 1) : rco,
+              false);
+    __syncthreads();
+    mark();
+  }
+  // ---- coarsest: L y = r, L^T x = y in place on rc (the order of llt_solve_kernel)
+  for (int i = tid; i < p.nc * p.nc; i += kTailNT) tail_sm[lo + i] = __ldg(p.Lc + i);
+  __syncthreads();
+  const int n = p.nc;
+  for (int k = 0; k < n; ++k) {
+    const double yk = __ddiv_rn(Rc[k], Lm[k * n + k]);
+    __syncthreads();
+    if (tid == 0) Rc[k] = yk;
+    for (int i = k + 1 + tid; i < n; i += kTailNT) Rc[i] = __dsub_rn(Rc[i], __dmul_rn(Lm[i * n + k], yk));
+    __syncthreads();
+  }
+  for (int k = n - 1; k >= 0; --k) {
+    const double xk = __ddiv_rn(Rc[k], Lm[k * n + k]);
+    __syncthreads();
+    if (tid == 0) Rc[k] = xk;
+    for (int i = tid; i < k; i += kTailNT) Rc[i] = __dsub_rn(Rc[i], __dmul_rn(Lm[k * n + i], xk));
+    __syncthreads();
+  }
+  mark();
+  // ---- up: prolongate, post-smooth
+  for (int k = p.nlev - 1; k >= 0; --k) {
+    const TailLev& lv = p.lv[k];
+    tail_spmv(lv.n, lv.prp, lv.pci, lv.pv, k + 1 < p.nlev ? zo(k + 1) : rco, zo(k), true);
+    __syncthreads();
+    mark();
+    for (int s = 0; s < p.m; ++s) {
+      tail_sweep<true>(lv, ro(k), zo(k), tbo(k), p.err);
+      tail_sweep<false>(lv, ro(k), zo(k), tbo(k), p.err);
+    }
+    mark();
+  }
+  for (int i = tid; i < p.lv[0].n; i += kTailNT) p.z[i] = tail_sm[zo(0) + i];
+}
+
+// the 64 class rows of a verified lattice level: slot values of a representative
+// row (absent slots +0) and the diagonal's division reciprocal in slot 15
+__global__ void tail_table_kernel(int L, const int* __restrict__ rp, const double* __restrict__ v, double* tb) {
+  const int c = threadIdx.x;  // 64 threads: class (ca, cy, cz) = c / 16, c / 4 % 4, c % 4
+  if (c >= 64) return;
+  const int rep[4] = {0, 1, L - 2, L - 1};
+  const int ca = c / 16, cy = c / 4 % 4, cz = c % 4;
+  double* o = tb + c * 16;
+  for (int sl = 0; sl < 16; ++sl) o[sl] = 0.0;
+  o[7] = o[15] = 1.0;
+  const int a = rep[ca], y = rep[cy], z = rep[cz];
+  if (a < 0 || y < 0 || z < 0 || pos_class(a, L) != ca || pos_class(y, L) != cy || pos_class(z, L) != cz) return;
+  const int i = (z * L + y) * L + a;
+  const unsigned m = tail_mask(a, y, z, L);
+  const int b = rp[i];
+  for (int sl = 0; sl < 15; ++sl)
+    o[sl] = ((m >> sl) & 1u) ? v[b + __popc(m & ((1u << sl) - 1u))] : 0.0;
+  o[15] = o[7] != 0.0 ? div_recip(o[7]) : 1.0;  // nvcc's d-only division part
+}
+
+// every row equals its class row slot by slot (bit for bit); else *bad = 1
+__global__ void tail_check_kernel(int L, const int* __restrict__ rp, const double* __restrict__ v,
+                                  const double* __restrict__ tb, int* bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L * L * L) return;
+  const int a = i % L, y = (i / L) % L, z = i / (L * L);
+  const unsigned m = tail_mask(a, y, z, L);
+  const int b = rp[i];
+  if (rp[i + 1] - b != __popc(m)) {
+    *bad = 1;
+    return;
+  }
+  const double* o = tb + ((pos_class(a, L) * 4 + pos_class(y, L)) * 4 + pos_class(z, L)) * 16;
+  for (int sl = 0; sl < 15; ++sl)
+    if (((m >> sl) & 1u) &&
+        __double_as_longlong(v[b + __popc(m & ((1u << sl) - 1u))]) != __double_as_longlong(o[sl]))
+      *bad = 1;
+}
+
+size_t tail_smem(const Hierarchy& h, int c0) {
+  size_t d = 0, maxn = 0;
+  for (size_t l = c0; l + 1 < h.levels.size(); ++l) {
+    d += 2 * (size_t)h.levels[l].A.rows;
+    maxn = std::max(maxn, (size_t)h.levels[l].A.rows);
+  }
+  d += maxn + (size_t)h.nc + (size_t)h.nc * h.nc + 1 + (size_t)(h.levels.size() - 1 - c0) * 64 * 16;
+  return d * sizeof(double);
+}
+
+}  // namespace
+
+// Setup: the first level the one-CTA tail can take.  From there down every
+// smoothed level must be a verified cubic lattice of side <= 16 whose rows are
+// equal within each position class (the class check runs on the device and
+// lands in *bad; the caller reads it with its own sync and drops the tail if set),
+// at most kTailMaxLevels of them, the vectors fitting in shared memory.
+void coarse_tail_prepare(Ctx& c, Hierarchy& h, int* bad) {
+  h.tail_checked = true;
+  h.tail_level = -1;
+  static const bool off = getenv("RD_NO_COARSE_TAIL") && atoi(getenv("RD_NO_COARSE_TAIL")) != 0;
+  const int nl = (int)h.levels.size();
+  if (off || nl < 2 || h.nc < 1) return;
+  int c0 = nl - 1;
+  while (c0 - 1 >= 0) {
+    const DCsr& A = h.levels[c0 - 1].A;
+    if (!(A.lat.ok && A.lat.lx == A.lat.ly && A.lat.lx == A.lat.lz && A.lat.lx <= kTailMaxL)) break;
+    --c0;
+  }
+  if (c0 == nl - 1) return;  // no small lattice level above the coarsest
+  while (nl - 1 - c0 > kTailMaxLevels) ++c0;
+  int maxsm = 0;
+  RDG_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+  while (c0 < nl - 1 && tail_smem(h, c0) > (size_t)maxsm) ++c0;
+  if (c0 >= nl - 1) return;
+  for (int l = c0; l + 1 < nl; ++l) {
+    Level& lv = h.levels[l];
+    const int L = lv.A.lat.lx;
+    lv.tail_table.alloc(64 * 16, c.stream);
+    tail_table_kernel<<<1, 64, 0, c.stream>>>(L, lv.A.rp.p, lv.A.v.p, lv.tail_table.p);
+    RDG_LAUNCH_CHECK();
+    tail_check_kernel<<<div_up(lv.A.rows, 256), 256, 0, c.stream>>>(L, lv.A.rp.p, lv.A.v.p, lv.tail_table.p, bad);
+    RDG_LAUNCH_CHECK();
+    c.launches += 2;
+  }
+  static bool attr = false;
+  if (!attr) {
+    RDG_CUDA(cudaFuncSetAttribute(coarse_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    attr = true;
+  }
+  h.tail_level = c0;
+}
+
+int coarse_tail_level(Ctx& c, Hierarchy& h) {
+  if (!h.tail_checked) {  // a hierarchy assembled without build_hierarchy: check here
+    DBuf<int> bad(1, c.stream);
+    RDG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
+    coarse_tail_prepare(c, h, bad.p);
+    int hb = 0;
+    RDG_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    if (hb) h.tail_level = -1;
+  }
+  return h.tail_level;
+}
+
+void coarse_tail(Ctx& c, Hierarchy& h, int c0, const double* r, double* z) {
+  TailParams p{};
+  const int nl = (int)h.levels.size();
+  p.nlev = nl - 1 - c0;
+  for (int k = 0; k < p.nlev; ++k) {
+    const Level& lv = h.levels[c0 + k];
+    TailLev& t = p.lv[k];
+    t.n = lv.A.rows;
+    t.L = lv.A.lat.lx;
+    t.table = lv.tail_table.p;
+    t.prp = lv.P.rp.p;
+    t.pci = lv.P.ci.p;
+    t.pv = lv.P.v.p;
+    t.trp = lv.Pt.rp.p;
+    t.tci = lv.Pt.ci.p;
+    t.tv = lv.Pt.v.p;
+  }
+  p.nc = h.nc;
+  p.Lc = h.Lc.p;
+  p.r = r;
+  p.z = z;
+  p.err = c.d_err;
+  p.m = h.smoothing_steps;
+  static const bool probe = getenv("RD_TAIL_CLOCKS") != nullptr;
+  DBuf<long long> clk;
+  if (probe) {
+    clk.alloc(64, c.stream);
+    RDG_CUDA(cudaMemsetAsync(clk.p, 0, 64 * sizeof(long long), c.stream));
+    p.clk = clk.p;
+  }
+
+  coarse_tail_kernel<<<1, kTailNT, tail_smem(h, c0), c.stream>>>(p);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+  if (probe) {
+    long long hc[64];
+    RDG_CUDA(cudaMemcpyAsync(hc, clk.p, sizeof(hc), cudaMemcpyDeviceToHost, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    fprintf(stderr, "tail clocks:");
+    for (int k = 1; k < 64 && hc[k]; ++k) fprintf(stderr, " %lld", hc[k] - hc[k - 1]);
+    fprintf(stderr, "\n");
+  }
+}
+
+}  // namespace rdg

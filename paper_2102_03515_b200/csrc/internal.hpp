@@ -119,14 +119,23 @@ struct Level {
   bool has_p = false;
   // work vectors
   DBuf<double> r, z, t, res;
+  DBuf<double> tail_table;  // coarse_tail.cu: the 64 position-class rows of a small lattice level
 };
 
+constexpr int kTailMaxLevels = 6;
 struct Hierarchy {
   std::vector<Level> levels;
   int smoothing_steps = 1;
   int nc = 0;              // coarsest dimension
   DBuf<double> Lc;         // coarsest LLT factor (row-major, lower)
+  bool tail_checked = false;
+  int tail_level = -1;     // first level of the one-CTA coarse tail (-1: none)
 };
+
+// coarse_tail.cu: the V-cycle from level c0 down and back up in one thread block
+void coarse_tail_prepare(Ctx& c, Hierarchy& h, int* bad_dev);  // setup (device-side check)
+int coarse_tail_level(Ctx& c, Hierarchy& h);
+void coarse_tail(Ctx& c, Hierarchy& h, int c0, const double* r, double* z);
 
 std::vector<uint8_t> coarsen(Ctx& c, const DCsr& A, DBuf<uint8_t>& flags_dev, DCsr& P);
 DCsr galerkin(Ctx& c, const DCsr& A, const DCsr& P, const DCsr& Pt);
