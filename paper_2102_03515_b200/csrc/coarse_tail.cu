@@ -69,29 +69,34 @@ __device__ __forceinline__ int pos_class(int t, int L) { return t == 0 ? 0 : t =
 
 extern __shared__ __align__(16) double tail_sm[];  // every vector of the tail (offsets below)
 
-// one Gauss-Seidel pass in place on x (shared), f (shared), the level's class
-// rows (tb, shared): nothing in the step loop touches global memory (a pending
-// global load would hold every step's __syncthreads).
+// z vectors live zero-padded, (L+2)^3 with a +0 halo: an absent slot of a class
+// row is +0 and reads a halo +0, so its term is +0 * +0 = +0 and s - (+0) == s for
+// every s -- the boundary rows need no predicates and the row sum is a plain chain.
+__device__ __forceinline__ int padi(int a, int y, int z, int L) { return (a + 1) + (L + 2) * ((y + 1) + (L + 2) * (z + 1)); }
+__device__ __forceinline__ int padof(int i, int L) { return padi(i % L, (i / L) % L, i / (L * L), L); }
+
+// one Gauss-Seidel pass in place on the padded x (shared), f (shared), the level's
+// class rows (tb, shared): nothing in the step loop touches global memory (a
+// pending global load would hold every step's __syncthreads).
 template <bool FWD>
 __device__ void tail_sweep(const TailLev& lv, int fo, int xo, int tbo, int* err) {
   const double* f = tail_sm + fo;
   double* x = tail_sm + xo;
   const double* tb = tail_sm + tbo;
-  const int L = lv.L, P = L * L;
+  const int L = lv.L, P = L * L, Q = L + 2, QQ = Q * Q;
   const int line = threadIdx.x;
   const bool has = line < P;
   const int y = has ? line % L : 0, z = has ? line / L : 0;
   const int yo = FWD ? y : L - 1 - y, zo = FWD ? z : L - 1 - z;
-  const int base = (zo * L + yo) * L;
+  const int base = (zo * L + yo) * L, pbase = padi(0, yo, zo, L);
   const int cyz = pos_class(yo, L) * 4 + pos_class(zo, L);
-  const int off[15] = {-1 - L - P, -L - P, -1 - P, -P, -1 - L, -L, -1, 0, 1, L, 1 + L, P, 1 + P, L + P, 1 + L + P};
+  const int off[15] = {-1 - Q - QQ, -Q - QQ, -1 - QQ, -QQ, -1 - Q, -Q, -1, 0, 1, Q, 1 + Q, QQ, 1 + QQ, Q + QQ, 1 + Q + QQ};
   const int steps = 3 * (L - 1) + 1;
   for (int s = 0; s < steps; ++s) {
     const int a = s - y - z;
     if (has && a >= 0 && a < L) {
       const int ao = FWD ? a : L - 1 - a;
-      const int i = base + ao;
-      const unsigned m = tail_mask(ao, yo, zo, L);
+      const int ip = pbase + ao;
       const double2* row = reinterpret_cast<const double2*>(tb + (pos_class(ao, L) * 16 + cyz) * 16);
       double v[16];
 #pragma unroll
@@ -100,72 +105,135 @@ __device__ void tail_sweep(const TailLev& lv, int fo, int xo, int tbo, int* err)
         v[2 * k] = t.x;
         v[2 * k + 1] = t.y;
       }
-      double sum = f[i];
+      double sum = f[base + ao];
 #pragma unroll
-      for (int k = 0; k < 15; ++k) {
-        if (k == 7) continue;
-        const bool pr = (m >> k) & 1u;  // branch-free: absent slots read x_i and keep the sum
-        const double t = __dsub_rn(sum, __dmul_rn(v[k], x[pr ? i + off[k] : i]));
-        sum = pr ? t : sum;
-      }
+      for (int k = 0; k < 15; ++k)
+        if (k != 7) sum = __dsub_rn(sum, __dmul_rn(v[k], x[ip + off[k]]));
       const double d = v[7];
       if (d == 0.0) atomicCAS(err, 0, RD_EZERODIAG);
       double q = div_fast(sum, d, v[15]);
       if (!(sum == 0.0 || div_is_fast(sum, d, q))) q = __ddiv_rn(sum, d);
-      x[i] = sum == 0.0 ? __dmul_rn(sum, v[15]) : q;
+      x[ip] = sum == 0.0 ? __dmul_rn(sum, v[15]) : q;
     }
     __syncthreads();
   }
 }
 
-// res = r - A z (the lattice rows), all in shared memory
+// res = r - A z (the lattice rows; z padded), all in shared memory
 __device__ void tail_residual(const TailLev& lv, int ro, int zo, int reso, int tbo) {
   const double* r = tail_sm + ro;
   const double* z = tail_sm + zo;
   double* res = tail_sm + reso;
   const double* tb = tail_sm + tbo;
-  const int L = lv.L, P = L * L;
-  const int off[15] = {-1 - L - P, -L - P, -1 - P, -P, -1 - L, -L, -1, 0, 1, L, 1 + L, P, 1 + P, L + P, 1 + L + P};
+  const int L = lv.L, P = L * L, Q = L + 2, QQ = Q * Q;
+  const int off[15] = {-1 - Q - QQ, -Q - QQ, -1 - QQ, -QQ, -1 - Q, -Q, -1, 0, 1, Q, 1 + Q, QQ, 1 + QQ, Q + QQ, 1 + Q + QQ};
   for (int i = threadIdx.x; i < lv.n; i += kTailNT) {
     const int a = i % L, y = (i / L) % L, zz = i / P;
     const double* v = tb + ((pos_class(a, L) * 4 + pos_class(y, L)) * 4 + pos_class(zz, L)) * 16;
-    const unsigned m = tail_mask(a, y, zz, L);
+    const int ip = padi(a, y, zz, L);
     double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < 15; ++k) {
-      const bool pr = (m >> k) & 1u;
-      const double t = __dadd_rn(s, __dmul_rn(v[k], z[pr ? i + off[k] : i]));
-      s = pr ? t : s;
-    }
+    for (int k = 0; k < 15; ++k) s = __dadd_rn(s, __dmul_rn(v[k], z[ip + off[k]]));
     res[i] = __dsub_rn(r[i], s);
   }
 }
 
-// y = M x for a CSR block in global memory (x, y shared), sums from +0
-__device__ void tail_spmv(int rows, const int* rp, const int* ci, const double* val, int xo, int yo, bool add) {
+// y = M x for a CSR block in global memory (x, y shared; xL / yL > 0: that vector is
+// padded for a side-L lattice), sums from +0; four rows in flight per thread
+__device__ void tail_spmv(int rows, const int* rp, const int* ci, const double* val, int xo, int xL, int yo, int yL,
+                          bool add) {
   const double* x = tail_sm + xo;
   double* y = tail_sm + yo;
-  for (int i = threadIdx.x; i < rows; i += kTailNT) {
-    double s = 0.0;
-    for (int k = __ldg(rp + i); k < __ldg(rp + i + 1); ++k) s = __dadd_rn(s, __dmul_rn(__ldg(val + k), x[__ldg(ci + k)]));
-    y[i] = add ? __dadd_rn(y[i], s) : s;
+  constexpr int U = 4;
+  for (int i0 = threadIdx.x; i0 < rows; i0 += kTailNT * U) {
+    int b[U], e[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * kTailNT;
+      b[u] = i < rows ? __ldg(rp + i) : 0;
+      e[u] = i < rows ? __ldg(rp + i + 1) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * kTailNT;
+      if (i >= rows) break;
+      double s = 0.0;
+      for (int k = b[u]; k < e[u]; ++k) {
+        const int c = __ldg(ci + k);
+        s = __dadd_rn(s, __dmul_rn(__ldg(val + k), x[xL ? padof(c, xL) : c]));
+      }
+      const int yi = yL ? padof(i, yL) : i;
+      y[yi] = add ? __dadd_rn(y[yi], s) : s;
+    }
   }
 }
 
+// the coarsest LLT substitutions (the order of llt_solve_kernel) by warp 0 alone:
+// lane l keeps rows l, l+32, ... in registers, the pivot's quotient is broadcast by
+// shuffle, divisions on the diagonal's precomputed reciprocal (exact fallback)
+__device__ void tail_llt(int n, const double* Lm, const double* rcp, double* rc) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  constexpr int R = 4;  // n <= 128
+  double v[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) v[j] = lane + 32 * j < n ? rc[lane + 32 * j] : 0.0;
+  auto quot = [&](double sk, int k) {
+    const double d = Lm[k * n + k], y = rcp[k];
+    double q = div_fast(sk, d, y);
+    if (!(sk == 0.0 || div_is_fast(sk, d, q))) q = __ddiv_rn(sk, d);
+    return sk == 0.0 ? __dmul_rn(sk, y) : q;
+  };
+  for (int k = 0; k < n; ++k) {
+    const int ow = k & 31, oj = k >> 5;
+    double sk = 0.0;
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (j == oj) sk = v[j];
+    sk = __shfl_sync(0xffffffffu, sk, ow);
+    const double yk = quot(sk, k);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int i = lane + 32 * j;
+      if (i == k) v[j] = yk;
+      if (i > k && i < n) v[j] = __dsub_rn(v[j], __dmul_rn(Lm[i * n + k], yk));
+    }
+  }
+  for (int k = n - 1; k >= 0; --k) {
+    const int ow = k & 31, oj = k >> 5;
+    double sk = 0.0;
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (j == oj) sk = v[j];
+    sk = __shfl_sync(0xffffffffu, sk, ow);
+    const double xk = quot(sk, k);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int i = lane + 32 * j;
+      if (i == k) v[j] = xk;
+      if (i < k) v[j] = __dsub_rn(v[j], __dmul_rn(Lm[k * n + i], xk));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if (lane + 32 * j < n) rc[lane + 32 * j] = v[j];
+}
+
 __global__ void __launch_bounds__(kTailNT, 1) coarse_tail_kernel(TailParams p) {
-  // layout (element offsets into tail_sm): per level k: r_k, z_k; then res, rc, Lc
+  // layout (element offsets into tail_sm): per level k: r_k (n_k), z_k ((L_k+2)^3, padded);
+  // then res, rc, the coarsest factor and its diagonal reciprocals, the class rows
+  auto zlen = [&](int k) { return (p.lv[k].L + 2) * (p.lv[k].L + 2) * (p.lv[k].L + 2); };
   auto ro = [&](int k) {
     int o = 0;
-    for (int j = 0; j < k; ++j) o += 2 * p.lv[j].n;
+    for (int j = 0; j < k; ++j) o += p.lv[j].n + zlen(j);
     return o;
   };
   auto zo = [&](int k) { return ro(k) + p.lv[k].n; };
   int maxn = 0;
   for (int k = 0; k < p.nlev; ++k) maxn = max(maxn, p.lv[k].n);
-  const int reso = ro(p.nlev), rco = reso + maxn, lo = rco + p.nc;
-  auto tbo = [&](int k) { return ((lo + p.nc * p.nc + 1) & ~1) + k * 64 * 16; };  // class rows (16-B aligned)
+  const int reso = ro(p.nlev), rco = reso + maxn, lo = rco + p.nc, dro = lo + p.nc * p.nc;
+  auto tbo = [&](int k) { return ((dro + p.nc + 1) & ~1) + k * 64 * 16; };  // class rows (16-B aligned)
   double* Rc = tail_sm + rco;
-  const double* Lm = tail_sm + lo;
   const int tid = threadIdx.x;
   int ck = 0;
   auto mark = [&]() {
@@ -173,8 +241,7 @@ __global__ void __launch_bounds__(kTailNT, 1) coarse_tail_kernel(TailParams p) {
     ++ck;
   };
   mark();
-  // pull every level's row values and P / P^T into L2 first: between V-cycles the
-  // fine-level streams evict them, and a step is far shorter than an HBM miss
+  // pull P / P^T into L2 first: between V-cycles the fine-level streams evict them
   if (tid >= 32 && tid - 32 < p.nlev) {
     const TailLev& lv = p.lv[tid - 32];
     const unsigned np = (unsigned)lv.prp[lv.n];  // nnz(P) = nnz(P^T)
@@ -186,12 +253,14 @@ __global__ void __launch_bounds__(kTailNT, 1) coarse_tail_kernel(TailParams p) {
   for (int i = tid; i < p.lv[0].n; i += kTailNT) tail_sm[i] = p.r[i];
   for (int k = 0; k < p.nlev; ++k)
     for (int i = tid; i < 64 * 16; i += kTailNT) tail_sm[tbo(k) + i] = __ldg(p.lv[k].table + i);
+  for (int i = tid; i < p.nc * p.nc; i += kTailNT) tail_sm[lo + i] = __ldg(p.Lc + i);
+  for (int i = tid; i < p.nc; i += kTailNT) tail_sm[dro + i] = div_recip(__ldg(p.Lc + i * p.nc + i));
   __syncthreads();
   mark();
   // ---- down: pre-smooth from zero, residual, restrict
   for (int k = 0; k < p.nlev; ++k) {
     const TailLev& lv = p.lv[k];
-    for (int i = tid; i < lv.n; i += kTailNT) tail_sm[zo(k) + i] = 0.0;
+    for (int i = tid; i < zlen(k); i += kTailNT) tail_sm[zo(k) + i] = 0.0;  // +0, halo included
     __syncthreads();
     for (int s = 0; s < p.m; ++s) {
       tail_sweep<true>(lv, ro(k), zo(k), tbo(k), p.err);
@@ -201,34 +270,20 @@ __global__ void __launch_bounds__(kTailNT, 1) coarse_tail_kernel(TailParams p) {
     tail_residual(lv, ro(k), zo(k), reso, tbo(k));
     __syncthreads();
     mark();
-    tail_spmv(k + 1 < p.nlev ? p.lv[k + 1].n : p.nc, lv.trp, lv.tci, lv.tv, reso, k + 1 < p.nlev ? ro(k + 1) : rco,
-              false);
+    tail_spmv(k + 1 < p.nlev ? p.lv[k + 1].n : p.nc, lv.trp, lv.tci, lv.tv, reso, 0, k + 1 < p.nlev ? ro(k + 1) : rco,
+              0, false);
     __syncthreads();
     mark();
   }
-  // ---- coarsest: L y = r, L^T x = y in place on rc (the order of llt_solve_kernel)
-  for (int i = tid; i < p.nc * p.nc; i += kTailNT) tail_sm[lo + i] = __ldg(p.Lc + i);
+  // ---- coarsest: L y = r, L^T x = y in place on rc
+  tail_llt(p.nc, tail_sm + lo, tail_sm + dro, Rc);
   __syncthreads();
-  const int n = p.nc;
-  for (int k = 0; k < n; ++k) {
-    const double yk = __ddiv_rn(Rc[k], Lm[k * n + k]);
-    __syncthreads();
-    if (tid == 0) Rc[k] = yk;
-    for (int i = k + 1 + tid; i < n; i += kTailNT) Rc[i] = __dsub_rn(Rc[i], __dmul_rn(Lm[i * n + k], yk));
-    __syncthreads();
-  }
-  for (int k = n - 1; k >= 0; --k) {
-    const double xk = __ddiv_rn(Rc[k], Lm[k * n + k]);
-    __syncthreads();
-    if (tid == 0) Rc[k] = xk;
-    for (int i = tid; i < k; i += kTailNT) Rc[i] = __dsub_rn(Rc[i], __dmul_rn(Lm[k * n + i], xk));
-    __syncthreads();
-  }
   mark();
   // ---- up: prolongate, post-smooth
   for (int k = p.nlev - 1; k >= 0; --k) {
     const TailLev& lv = p.lv[k];
-    tail_spmv(lv.n, lv.prp, lv.pci, lv.pv, k + 1 < p.nlev ? zo(k + 1) : rco, zo(k), true);
+    const bool fromc = k + 1 == p.nlev;
+    tail_spmv(lv.n, lv.prp, lv.pci, lv.pv, fromc ? rco : zo(k + 1), fromc ? 0 : p.lv[k + 1].L, zo(k), lv.L, true);
     __syncthreads();
     mark();
     for (int s = 0; s < p.m; ++s) {
@@ -237,7 +292,7 @@ __global__ void __launch_bounds__(kTailNT, 1) coarse_tail_kernel(TailParams p) {
     }
     mark();
   }
-  for (int i = tid; i < p.lv[0].n; i += kTailNT) p.z[i] = tail_sm[zo(0) + i];
+  for (int i = tid; i < p.lv[0].n; i += kTailNT) p.z[i] = tail_sm[zo(0) + padof(i, p.lv[0].L)];
 }
 
 // the 64 class rows of a verified lattice level: slot values of a representative
@@ -282,10 +337,12 @@ __global__ void tail_check_kernel(int L, const int* __restrict__ rp, const doubl
 size_t tail_smem(const Hierarchy& h, int c0) {
   size_t d = 0, maxn = 0;
   for (size_t l = c0; l + 1 < h.levels.size(); ++l) {
-    d += 2 * (size_t)h.levels[l].A.rows;
+    const size_t Q = (size_t)h.levels[l].A.lat.lx + 2;
+    d += (size_t)h.levels[l].A.rows + Q * Q * Q;
     maxn = std::max(maxn, (size_t)h.levels[l].A.rows);
   }
-  d += maxn + (size_t)h.nc + (size_t)h.nc * h.nc + 1 + (size_t)(h.levels.size() - 1 - c0) * 64 * 16;
+  if (h.nc > 128) return SIZE_MAX;  // tail_llt keeps at most 4 rows per lane
+  d += maxn + 2 * (size_t)h.nc + (size_t)h.nc * h.nc + 1 + (size_t)(h.levels.size() - 1 - c0) * 64 * 16;
   return d * sizeof(double);
 }
 
