@@ -137,7 +137,8 @@ const rd_csr* rd_gpu_amg_level_matrix(const rd_amg* h, int level, int which);
 /* coarse_flag of level l (1 = C), host buffer of rows(A_l) bytes */
 int rd_gpu_amg_level_flags(const rd_amg* h, int level, uint8_t* flags);
 /* level l's smoother: 0 generic, 1 structured lattice kernel streaming the packed stencil,
- * 2 structured with the uniform stencil held in registers (every row = the centre row) */
+ * 2 structured with the uniform stencil held in registers (every row = the centre row),
+ * 3 structured with the 64 position-class rows in shared memory                          */
 int rd_gpu_amg_level_structured(const rd_amg* h, int level);
 /* replaces rd::amg_apply(h, r) / amg_precond(h)          amg.hpp:39-42, amg.cpp:119-145 */
 int rd_gpu_amg_apply(rd_amg* h, const double* r, double* z);

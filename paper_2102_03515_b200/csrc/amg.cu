@@ -857,10 +857,10 @@ bool build_levels(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, boo
   coarse_tail_prepare(c, h, tail_bad.p);
   int tail_bad_h = 0;
   RDG_CUDA(cudaMemcpyAsync(&tail_bad_h, tail_bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  std::vector<int> uni(h.levels.size(), -1);  // smoother stencil uniformity, read with the same sync
+  std::vector<int> uni(2 * h.levels.size(), -1);  // smoother stencil uniformity, read with the same sync
   for (size_t l = 0; l < h.levels.size(); ++l)
     if (h.levels[l].A.lat_uni_state == -2)
-      RDG_CUDA(cudaMemcpyAsync(&uni[l], h.levels[l].A.lat_uni_flag.p, sizeof(int), cudaMemcpyDeviceToHost,
+      RDG_CUDA(cudaMemcpyAsync(&uni[2 * l], h.levels[l].A.lat_uni_flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost,
                                c.stream));
   RDG_CUDA(cudaStreamSynchronize(c.stream));
   for (int l = 0; l < nlat; ++l)
@@ -871,7 +871,7 @@ bool build_levels(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, boo
     if (f[kMaxLat + l]) throw Error(RD_ERUNTIME, "lattice smoother: pattern/layout mismatch");
   }
   for (size_t l = 0; l < h.levels.size(); ++l)
-    if (uni[l] >= 0) lattice_resolve(c, h.levels[l].A, uni[l]);  // packs only for non-uniform levels
+    if (uni[2 * l] >= 0) lattice_resolve(c, h.levels[l].A, &uni[2 * l]);  // packs only where needed
   if (tail_bad_h) h.tail_level = -1;
   return true;
 }

@@ -448,7 +448,7 @@ int rd_gpu_amg_level_flags(const rd_amg* h, int level, uint8_t* flags) {
 int rd_gpu_amg_level_structured(const rd_amg* h, int level) {
   if (!h || level < 0 || level >= (int)h->h.levels.size()) return -1;
   const DCsr& A = h->h.levels[level].A;
-  return A.lat.ok ? (A.lat_uni_state == 1 ? 2 : 1) : 0;
+  return A.lat.ok ? (A.lat_uni_state == 1 ? 2 : (A.lat_uni_state == 2 ? 3 : 1)) : 0;
 }
 
 int rd_gpu_amg_apply(rd_amg* h, const double* r, double* z) {

@@ -62,9 +62,6 @@ __device__ __forceinline__ void l2_prefetch(const void* src, unsigned bytes) {
   if (bytes >= 16) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes & ~15u) : "memory");
 }
 
-// position class of a lattice coordinate: 0 first, 3 last, 2 second-to-last, 1 interior.
-// Every level's rows are equal within a class triple (checked at setup).
-__device__ __forceinline__ int pos_class(int t, int L) { return t == 0 ? 0 : t == L - 1 ? 3 : t == L - 2 ? 2 : 1; }
 
 
 extern __shared__ __align__(16) double tail_sm[];  // every vector of the tail (offsets below)

@@ -36,9 +36,13 @@ struct DCsr {
   mutable unsigned lat_epoch = 0;
   // uniform stencil: every row equals the box-centre row slot by slot (absent slots
   // aside) -- then the smoother keeps the row in registers and streams no values.
-  // state: -1 not prepared, -2 check pending on the device, 0 packed, 1 uniform
+  // class-uniform stencil: every row equals its position class's row (64 classes,
+  // pos_class of each coordinate) -- the smoother reads rows from an 8 KB table.
+  // state: -1 not prepared, -2 checks pending on the device, 0 packed, 1 uniform, 2 class
   mutable DBuf<double> lat_uni;     // 15 slot values + the diagonal's division reciprocal
-  mutable DBuf<int> lat_uni_flag;   // device: 1 = some row differs
+  mutable DBuf<int> lat_uni_flag;   // device: [0] 1 = some row differs from the centre row,
+                                    //         [1] 1 = some row differs from its class row
+  mutable DBuf<double> lat_cls;     // [64][16] class rows (slot order, absent +0, reciprocal in 15)
   mutable int lat_uni_state = -1;
 };
 
@@ -75,16 +79,17 @@ void gs_pass(Ctx& c, const DCsr& A, const double* f, const double* xin, double* 
 // setup-time layout for the structured smoother (no-op unless A.lat.ok); with
 // err_dev the layout check is left on the device (1 mismatch, 2 zero diagonal)
 void lattice_prepare(Ctx& c, const DCsr& A, int* err_dev = nullptr);
-// after lattice_prepare: uniform_flag = the host copy of lat_uni_flag (-1: read it here);
+// after lattice_prepare: flags_host = the host copy of lat_uni_flag[0..1] (null: read it here);
 // builds the packed layout for a non-uniform level when build_packs
-void lattice_resolve(Ctx& c, const DCsr& A, int uniform_flag = -1, bool build_packs = true);
+void lattice_resolve(Ctx& c, const DCsr& A, const int* flags_host = nullptr, bool build_packs = true);
 
 // distributed z-slab smoother (dist.cu): one rank's planes [zlo, zhi) of a lattice
 // level; local vectors hold planes [g0, g1) (the slab plus one ghost plane per side)
 struct SlabSmoother {
   int L = 0, zlo = 0, zhi = 0, g0 = 0, g1 = 0, ntz = 0;
   DBuf<double> pack[2];            // fwd, bwd step-major packed stencil of the slab's tiles
-  DBuf<double> uni;                // or the uniform stencil row (then no packs)
+  DBuf<double> uni;                // or the stencil on chip (then no packs): the uniform row
+  int vm = 0;                      // (vm 1) or the 64 class rows (vm 2); 0 packed
   // tagged cells {value, tag} of planes [g0, g1): plain cudaMalloc, so a peer
   // process can map them (cudaIpcGetMemHandle) for the pipelined hand-off
   unsigned long long* cells = nullptr;

@@ -499,6 +499,10 @@ class AmgHierarchy:
         """Level l's lattice stencil is the same in every row (kept in registers by the smoother)."""
         return lib().rd_gpu_amg_level_structured(self.h, int(l)) == 2
 
+    def stencil_source(self, l: int) -> str:
+        """How level l's smoother gets its stencil: generic / packed / uniform / class."""
+        return ["generic", "packed", "uniform", "class"][lib().rd_gpu_amg_level_structured(self.h, int(l))]
+
     def apply(self, r, z=None):
         """amg.hpp:39 amg_apply: one V-cycle, zero initial guess.  Host arrays in -> host array out;
         device buffers (torch tensors / pointers) are used in place and left stream-ordered."""

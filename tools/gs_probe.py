@@ -30,5 +30,5 @@ for l in range(h.num_levels - 1):
         h.level_sweep(l, True, f, x, y)
     b.record(stream)
     torch.cuda.synchronize()
-    out.append((l, A.rows, round(a.elapsed_time(b) / R * 1e3, 1), "uni" if h.uniform(l) else "packed"))
+    out.append((l, A.rows, round(a.elapsed_time(b) / R * 1e3, 1), h.stencil_source(l)))
 print(os.environ.get("RD_GS_DEBUG", "0"), json.dumps(out))
