@@ -123,3 +123,15 @@ def test_exact_slabs_c2_vcycle(mode, world):
     outs = _run_ranks(world, n, rho, "ball", mode, 262144, solve=False)
     assert outs[0]["G"] == 1 and outs[0]["cuts"][0] == 0 and outs[0]["cuts"][-1] == 127
     assert np.array_equal(outs[0]["z"], zref)
+
+
+def test_pipelined_slabs_c2_solve():
+    """C2 solved on 2 pipelined slabs: the single-GPU iteration count and solution (1e-10)."""
+    n, rho = 128, 2.0 ** -14
+    ref = _single(n, rho, "ball")
+    outs = _run_ranks(2, n, rho, "ball", "pipelined", 262144)
+    o0 = outs[0]
+    assert all(o["conv"] and o["it"] == ref["it"] for o in outs)
+    assert np.array_equal(o0["z"], ref["z"])
+    err = np.abs(o0["x"] - ref["x"]).max() / np.abs(ref["x"]).max()
+    assert err <= 1e-10, err

@@ -498,3 +498,20 @@ def test_degenerate_meshes(rd):  # test_bench.cpp:185-195: n=1 has no dofs
     assert ds.n_dofs == 1
     out = rd.solve_system_amg(ds.A, ds.f(), 1e-8)
     assert out.converged
+
+
+def test_c2_full_solve(rd, O):  # BASELINE config 2 at full size: n=128, rho=h^2, ball target
+    """The bench workload end to end against the oracle: A bit for bit, iteration count equal,
+    solution within 1e-10 relative, every smoothed level on a structured kernel."""
+    O.set_num_threads(8)
+    n, rho = 128, 2.0 ** -14
+    ds = rd.build_system(rd.build_structured_cube(n), rho, "ball")
+    os_ = O.build_system(O.build_structured_cube(n), rho, "ball")
+    assert_csr_equal(ds.A, os_.A, "A")
+    assert np.array_equal(ds.f(), os_.f)
+    out = rd.solve_system_amg(ds.A, ds.f(), 1e-8)
+    ref = O.solve_system_amg(os_, 1e-8)
+    assert out.converged and ref.converged and out.iterations == ref.iterations == 5
+    assert np.abs(out.u - ref.u).max() <= 1e-10 * np.abs(ref.u).max()
+    h = rd.build_amg(ds.A)
+    assert [h.stencil_source(l) for l in range(h.num_levels - 1)][:2] == ["uniform", "class"]
