@@ -382,6 +382,9 @@ def run_ours(args, rank, world, local_rank):
         bw = timed(lambda: h.level_sweep(l, False, fl, xl, yl))
         level_sweeps.append({"level": l, "rows": Al.rows, "nnz": Al.nnz, "fwd_ms": fw, "bwd_ms": bw})
     spmv_ms = timed(lambda: rd.lib().rd_gpu_spmv(ctx.h, s.A.h, rd._ptr(x), rd._ptr(y)))
+    # the V-cycle / PCG SpMV on the prepared level-0 matrix: the lattice stencil kernel (no CSR read)
+    A0 = h.level(0)
+    st_ms = timed(lambda: rd.lib().rd_gpu_spmv(ctx.h, A0.h, rd._ptr(x), rd._ptr(y)))
     structured = h.structured(0)
     uniform = h.uniform(0)
     # SURVEY.md 8(d) algorithmic bytes of a GS sweep (the CSR formulation: values, columns, row
@@ -434,6 +437,11 @@ def run_ours(args, rank, world, local_rank):
                  "frac": spmv_bytes / (spmv_ms * 1e-3) / 1e9 / peak, "traffic": traffic.get("spmv")},
         "gs_sweep_level0": {"bytes_per_launch": gs_bytes, "launch_ms": gs_ms, "achieved_gbs": gs_gbs,
                             "frac": gs_gbs / peak},
+        "spmv_stencil_level0": {"source": h.stencil_source(0), "launch_ms": st_ms,
+                                "moved_bytes_per_launch": 16 * N,
+                                "moved_gbs": 16 * N / (st_ms * 1e-3) / 1e9,
+                                "frac_moved": 16 * N / (st_ms * 1e-3) / 1e9 / peak,
+                                "csr_algorithmic_gbs": spmv_bytes / (st_ms * 1e-3) / 1e9},
         "levels": h.num_levels,
         "level_sweeps": level_sweeps,
         "structured_levels": [bool(h.structured(l)) for l in range(h.num_levels - 1)],

@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace rdg {
@@ -204,10 +206,57 @@ __global__ void __launch_bounds__(kSpmvNT) spmv_staged_kernel(int rows, const in
   }
 }
 
+// SpMV on a lattice level whose rows are known on chip (smoother_lattice.cu's checks):
+// uniform (tab = the 15-slot row) or class-uniform (tab = 64 class rows).  One block
+// per x-line, threads along x (coalesced neighbour reads); the row sum from +0 in slot
+// = ascending column order, absent slots adding +0 * x_i (exact: a running sum that
+// starts at +0 is never -0).  Reads x and writes y only: the CSR stays untouched.
+template <int MODE, bool CLS>
+__global__ void __launch_bounds__(128) stencil_spmv_kernel(int L, const double* __restrict__ tab,
+                                                           const double* __restrict__ x, double* __restrict__ y,
+                                                           const double* __restrict__ r) {
+  __shared__ __align__(16) double st[CLS ? 64 * 16 : 16];
+  for (int k = threadIdx.x; k < (CLS ? 64 * 16 : 16); k += blockDim.x) st[k] = __ldg(tab + k);
+  __syncthreads();
+  const int line = blockIdx.x;
+  const int yy = line % L, zz = line / L;
+  const long long P = (long long)L * L;
+  const bool ym = yy > 0, yp = yy < L - 1, zm = zz > 0, zp = zz < L - 1;
+  const int cyz = pos_class(yy, L) * 4 + pos_class(zz, L);
+  const long long off[15] = {-1 - L - P, -L - P, -1 - P, -P, -1 - L, -L, -1, 0, 1, L, 1 + L, P, 1 + P, L + P, 1 + L + P};
+  for (int a = threadIdx.x; a < L; a += blockDim.x) {
+    const long long i = (long long)line * L + a;
+    const bool am = a > 0, ap = a < L - 1;
+    const bool pr[15] = {am && ym && zm, ym && zm, am && zm, zm, am && ym, ym, am, true,
+                         ap, yp, ap && yp, zp, ap && zp, yp && zp, ap && yp && zp};
+    const double* v = CLS ? st + (pos_class(a, L) * 16 + cyz) * 16 : st;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 15; ++k) {
+      const double vk = pr[k] ? v[k] : 0.0;
+      acc = __dadd_rn(acc, __dmul_rn(vk, x[pr[k] ? i + off[k] : i]));
+    }
+    y[i] = MODE == kResidual ? __dsub_rn(r[i], acc) : acc;
+  }
+}
+
 template <int MODE>
 void launch_spmv(Ctx& c, const DCsr& A, const double* x, double* y, const double* r, double* dot_out) {
   if (A.rows == 0) {
     if (MODE == kDot) RDG_CUDA(cudaMemsetAsync(dot_out, 0, sizeof(double), c.stream));
+    return;
+  }
+  static const bool nostencil = getenv("RD_NO_STENCIL_SPMV") && atoi(getenv("RD_NO_STENCIL_SPMV")) != 0;
+  if (!nostencil && A.lat.ok && (A.lat_uni_state == 1 || A.lat_uni_state == 2) && A.lat.lx == A.lat.ly &&
+      A.lat.lx == A.lat.lz && (int64_t)A.lat.lx * A.lat.lx * A.lat.lx == A.rows && A.cols == A.rows) {
+    const int L = A.lat.lx;
+    const bool cls = A.lat_uni_state == 2;
+    constexpr int M = MODE == kResidual ? kResidual : kPlain;
+    auto* k = cls ? stencil_spmv_kernel<M, true> : stencil_spmv_kernel<M, false>;
+    k<<<L * L, 128, 0, c.stream>>>(L, cls ? A.lat_cls.p : A.lat_uni.p, x, y, r);
+    RDG_LAUNCH_CHECK();
+    ++c.launches;
+    if (MODE == kDot) dot(c, A.rows, x, y, dot_out);
     return;
   }
   const int nb = div_up(A.rows, kSpmvNT);

@@ -120,8 +120,13 @@ PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, do
   }
   RDG_CUDA(cudaMemcpyAsync(p.p, z.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
   const int g = vec_grid(c, n);
+  // the hierarchy's level 0 views A's arrays (its stencil facts feed the lattice SpMV)
+  const DCsr& As = (h && !h->levels.empty() && h->levels[0].A.v.p == A.v.p && h->levels[0].A.rp.p == A.rp.p &&
+                    h->levels[0].A.rows == A.rows)
+                       ? h->levels[0].A
+                       : A;
   for (int it = 1; it <= max_iter; ++it) {
-    spmv_dot(c, A, p.p, Ap.p, &st.p->pAp);
+    spmv_dot(c, As, p.p, Ap.p, &st.p->pAp);
     pcg_xr_kernel<<<g, 256, 0, c.stream>>>(n, st.p, p.p, Ap.p, x, r.p);
     RDG_LAUNCH_CHECK();
     ++c.launches;
