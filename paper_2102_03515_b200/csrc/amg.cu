@@ -873,6 +873,8 @@ bool build_levels(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, boo
   for (size_t l = 0; l < h.levels.size(); ++l)
     if (uni[2 * l] >= 0) lattice_resolve(c, h.levels[l].A, &uni[2 * l]);  // packs only where needed
   if (tail_bad_h) h.tail_level = -1;
+  if (getenv("RD_TAIL_CLOCKS"))
+    fprintf(stderr, "coarse tail: level %d (class check %s)\n", h.tail_level, tail_bad_h ? "failed" : "ok");
   return true;
 }
 }  // namespace

@@ -109,7 +109,7 @@ __device__ void tail_sweep(const TailLev& lv, int fo, int xo, int tbo, int* err)
       const double d = v[7];
       if (d == 0.0) atomicCAS(err, 0, RD_EZERODIAG);
       double q = div_fast(sum, d, v[15]);
-      if (!(sum == 0.0 || div_is_fast(sum, d, q))) q = __ddiv_rn(sum, d);
+      if (!(sum == 0.0 || div_is_fast(sum, d, q))) q = div_exact(sum, d);
       x[ip] = sum == 0.0 ? __dmul_rn(sum, v[15]) : q;
     }
     __syncthreads();
@@ -178,7 +178,7 @@ __device__ void tail_llt(int n, const double* Lm, const double* rcp, double* rc)
   auto quot = [&](double sk, int k) {
     const double d = Lm[k * n + k], y = rcp[k];
     double q = div_fast(sk, d, y);
-    if (!(sk == 0.0 || div_is_fast(sk, d, q))) q = __ddiv_rn(sk, d);
+    if (!(sk == 0.0 || div_is_fast(sk, d, q))) q = div_exact(sk, d);
     return sk == 0.0 ? __dmul_rn(sk, y) : q;
   };
   for (int k = 0; k < n; ++k) {
