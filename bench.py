@@ -350,6 +350,12 @@ def run_ours(args, rank, world, local_rank):
     if args.profile:
         return result
 
+    # ---------------- the BASELINE error gate on the solution just computed (assembly.cpp:312-331)
+    s_err = rd.build_system(mesh, rho, args.target)
+    result["errors"] = {"l2_u_minus_target": float(np.sqrt(rd.l2_error_target_squared(s_err, u_dev, args.target))),
+                        "rule": "64-point subdivision" if args.target in ("ball", "box") else "degree 5"}
+    del s_err
+
     # ---------------- dominant kernels, timed live with events on the library stream
     s = rd.build_system(mesh, rho, args.target)
     h = rd.build_amg(s.A)

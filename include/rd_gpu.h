@@ -179,6 +179,14 @@ int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, doubl
 int rd_gpu_error_norms(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs,
                        double rho, double* l2_error, double* h1_semi_error);
 
+/* replaces rd::l2_error_target_squared(sol, target)  assembly.hpp:62, assembly.cpp:312-331:
+ * the SQUARED L2 distance of the P1 field (interior coefficients `coeffs`, host or device)
+ * to the target field, with the target's own rule (rule_for: 64-point subdivision for the
+ * discontinuous box / ball, degree-5 otherwise).  The BASELINE error gate ||u_rho,h - u_bar||_L2
+ * for every target; ||grad(u - u_bar)|| of the smooth target is rd_gpu_error_norms(rho = 0). */
+int rd_gpu_l2_error_target_squared(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs,
+                                   const rd_target* target, double* err2);
+
 /* ------------------------------------------------------------ distributed (z-slab) pieces
  * SURVEY.md §8(e).  The reference has no distributed solver (its parallelism is
  * the thread pool of parallel.cpp:12-73); these calls are the per-rank device

@@ -95,6 +95,7 @@ def lib():
         "or_pipeline": (_I, [_I, _D, _I, C.c_uint64, _D, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I),
                              C.POINTER(_D), C.POINTER(_D), C.POINTER(_D)]),
         "or_l2_error_manufactured": (_I, [_P, _P, _pd, _D, C.POINTER(_D)]),
+        "or_l2_error_target_squared": (_I, [_P, _P, _pd, _I, _I, C.c_uint64, C.POINTER(_D)]),
         "or_h1_semi_error_manufactured": (_I, [_P, _P, _pd, _D, C.POINTER(_D)]),
     }
     for name, (res, args) in sig.items():
@@ -462,4 +463,12 @@ def h1_semi_error_manufactured(mesh: Mesh, sys: FemSystem, coeffs, rho_exact: fl
     out = _D()
     _check(lib().or_h1_semi_error_manufactured(mesh._h.h, sys._h.h, np.ascontiguousarray(coeffs, np.float64),
                                                float(rho_exact), C.byref(out)))
+    return out.value
+
+
+def l2_error_target_squared(mesh: Mesh, sys: FemSystem, coeffs, target: str, n: int = 0, seed: int = 0) -> float:
+    """assembly.cpp:312-331: squared L2 distance of the P1 field to the target, the target's rule."""
+    out = _D()
+    _check(lib().or_l2_error_target_squared(mesh._h.h, sys._h.h, np.ascontiguousarray(coeffs, np.float64),
+                                            TARGETS[target], int(n), int(seed), C.byref(out)))
     return out.value

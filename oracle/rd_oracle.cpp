@@ -1103,6 +1103,31 @@ double h1_semi_error(const Mesh& m, const DofMap& dm, const double* coeffs, cons
   return std::sqrt(err2);
 }
 
+// assembly.cpp:312-331: the squared L2 distance to the TARGET field with the target's
+// own rule (rule_for, assembly.cpp:140-144), target minus fe_value
+double l2_error_target_squared(const Mesh& m, const DofMap& dm, const double* coeffs, const Target& tg) {
+  const auto nodal = nodal_field(m, dm, coeffs);
+  const Rule& rule = rule_for(tg);
+  return parallel_reduce(m.nt(), [&](int64_t b, int64_t e) {
+    double s = 0.0;
+    for (int64_t t = b; t < e; ++t) {
+      const auto verts = tet_vertices(m, static_cast<int>(t));
+      const auto& tet = m.tets[static_cast<size_t>(t)];
+      double acc = 0.0;
+      for (int q = 0; q < rule.size(); ++q) {
+        const auto& lam = rule.pts[static_cast<size_t>(q)];
+        const V3 x = physical_point(lam, verts);
+        double u = 0.0;
+        for (int i = 0; i < 4; ++i) u += lam[static_cast<size_t>(i)] * nodal[static_cast<size_t>(tet[static_cast<size_t>(i)])];
+        const double d = tg(x) - u;
+        acc += rule.w[static_cast<size_t>(q)] * d * d;
+      }
+      s += tet_volume(m, static_cast<int>(t)) * acc;
+    }
+    return s;
+  });
+}
+
 template <class F>
 int guard(F&& fn) {
   try {
@@ -1428,6 +1453,10 @@ int or_pipeline(int n, double rho, int kind, uint64_t seed, double tol, int* ite
 
 int or_l2_error_manufactured(const or_mesh* m, const or_system* s, const double* coeffs, double rho, double* out) {
   return guard([&] { *out = l2_error(m->m, s->s.dm, coeffs, manufactured_exact(rho)); });
+}
+int or_l2_error_target_squared(const or_mesh* m, const or_system* s, const double* coeffs, int kind, int n,
+                               uint64_t seed, double* out) {
+  return guard([&] { *out = l2_error_target_squared(m->m, s->s.dm, coeffs, make_target(kind, n, seed)); });
 }
 int or_h1_semi_error_manufactured(const or_mesh* m, const or_system* s, const double* coeffs, double rho,
                                   double* out) {

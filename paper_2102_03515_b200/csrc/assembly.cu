@@ -1013,6 +1013,66 @@ __global__ void __launch_bounds__(kErrNT) error_norm_kernel(int nt, const int* _
   finish_reduction<kErrNT>(partials, counter, sh, [&](double tot) { *out = tot; });
 }
 
+// assembly.cpp:312-331 on the device: per tet the target's rule (NQ = 14 or 64),
+// d = target(x_q) - u_h(x_q), acc += (w d) d, vol * acc; fixed-order block sums
+template <int NQ>
+__global__ void __launch_bounds__(kErrNT) error_target_kernel(int nt, const int* __restrict__ tets,
+                                                            const double* __restrict__ xyz,
+                                                            const int* __restrict__ v2d,
+                                                            const double* __restrict__ coeffs, int kind,
+                                                            const double* __restrict__ nodal, int n,
+                                                            double* partials, unsigned* counter, double* out) {
+  __shared__ double sh[kErrNT / 32];
+  const int t = blockIdx.x * kErrNT + threadIdx.x;
+  double contrib = 0.0;
+  if (t < nt) {
+    const int4 t4 = reinterpret_cast<const int4*>(tets)[t];
+    const int tv[4] = {t4.x, t4.y, t4.z, t4.w};
+    double V[4][3], nod[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) V[k][c] = xyz[3 * (int64_t)tv[k] + c];
+      const int d = v2d[tv[k]];
+      nod[k] = d >= 0 ? coeffs[d] : 0.0;
+    }
+    double a[3], b[3], e[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      a[c] = __dsub_rn(V[1][c], V[0][c]);
+      b[c] = __dsub_rn(V[2][c], V[0][c]);
+      e[c] = __dsub_rn(V[3][c], V[0][c]);
+    }
+    const double x0 = __dsub_rn(__dmul_rn(a[1], b[2]), __dmul_rn(a[2], b[1]));
+    const double x1 = __dsub_rn(__dmul_rn(a[2], b[0]), __dmul_rn(a[0], b[2]));
+    const double x2 = __dsub_rn(__dmul_rn(a[0], b[1]), __dmul_rn(a[1], b[0]));
+    const double dt = __dadd_rn(__dadd_rn(__dmul_rn(x0, e[0]), __dmul_rn(x1, e[1])), __dmul_rn(x2, e[2]));
+    const double vol = __ddiv_rn(fabs(dt), 6.0);  // mesh.cpp:188-191
+    double acc = 0.0;
+    for (int q = 0; q < NQ; ++q) {
+      const double* lam = NQ == 14 ? c_rules.p14[q] : c_rules.p64[q];
+      const double w = NQ == 14 ? c_rules.w14[q] : c_rules.w64[q];
+      double X[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s = __dadd_rn(s, __dmul_rn(lam[k], V[k][c]));
+        X[c] = s;
+      }
+      double u = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) u = __dadd_rn(u, __dmul_rn(lam[k], nod[k]));
+      const double d = __dsub_rn(target_eval(kind, X[0], X[1], X[2], nodal, n), u);
+      acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w, d), d));
+    }
+    contrib = __dmul_rn(vol, acc);
+  }
+  const double bsum = block_sum_fixed<kErrNT>(contrib, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = bsum;
+  finish_reduction<kErrNT>(partials, counter, sh, [&](double tot) { *out = tot; });
+}
+
 int read_flag(Ctx& c, const int* d) {
   int h = 0;
   RDG_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -1217,6 +1277,42 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
     c.launches += 2;
   }
   RDG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+double l2_error_target_squared(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, int kind,
+                               uint64_t seed) {
+  if (kind < 0 || kind > RD_TARGET_QUADRATIC) throw Error(RD_EINVAL, "l2_error_target: unknown target kind");
+  if (kind == RD_TARGET_SINE_RANDOM && m.lattice_n < 1)
+    throw Error(RD_EINVAL, "l2_error_target: the sine+random target needs a build_structured_cube mesh");
+  upload_rules(c);
+  const int nt = m.nt, n = m.lattice_n;
+  const int nb = std::max(div_up(nt, kErrNT), 1);
+  DBuf<double> partials(nb, c.stream), outv(1, c.stream), nodal;
+  DBuf<unsigned> counter(1, c.stream);
+  RDG_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), c.stream));
+  RDG_CUDA(cudaMemsetAsync(outv.p, 0, sizeof(double), c.stream));
+  if (kind == RD_TARGET_SINE_RANDOM) {
+    const int64_t nv = (int64_t)(n + 1) * (n + 1) * (n + 1);
+    nodal.alloc(nv, c.stream);
+    random_nodal_kernel<<<div_up(nv, 256), 256, 0, c.stream>>>(n, seed, nodal.p);
+    RDG_LAUNCH_CHECK();
+    ++c.launches;
+  }
+  if (nt > 0) {
+    const bool disc = kind == RD_TARGET_BOX || kind == RD_TARGET_BALL;  // rule_for: Smoothness::discontinuous
+    if (disc)
+      error_target_kernel<64><<<nb, kErrNT, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, s.v2d.p, coeffs, kind, nodal.p, n,
+                                                           partials.p, counter.p, outv.p);
+    else
+      error_target_kernel<14><<<nb, kErrNT, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, s.v2d.p, coeffs, kind, nodal.p, n,
+                                                           partials.p, counter.p, outv.p);
+    RDG_LAUNCH_CHECK();
+    ++c.launches;
+  }
+  double h = 0.0;
+  RDG_CUDA(cudaMemcpyAsync(&h, outv.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  RDG_CUDA(cudaStreamSynchronize(c.stream));
+  return h;
 }
 
 void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, double rho, double* l2,

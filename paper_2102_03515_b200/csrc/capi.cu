@@ -560,4 +560,16 @@ int rd_gpu_error_norms(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, c
   });
 }
 
+int rd_gpu_l2_error_target_squared(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs,
+                                   const rd_target* target, double* err2) {
+  return guard(ctx, [&] {
+    require(mesh && sys && coeffs && target && err2, "l2_error_target_squared: null argument");
+    require(sys->s.nv == mesh->m.nv, "l2_error_target_squared: system does not belong to the mesh");
+    Ctx& c = ctx->c;
+    DBuf<double> tc;
+    const double* cd = in_dev(c, coeffs, sys->s.n_dofs, tc);
+    *err2 = l2_error_target_squared(c, mesh->m, sys->s, cd, target->kind, target->seed);
+  });
+}
+
 }  // extern "C"

@@ -184,6 +184,9 @@ void detect_cube_lattice(Ctx& c, DMesh& m);
 void build_system(Ctx& c, const DMesh& m, double rho, int target_kind, uint64_t seed, DSystem& s);
 // l2 / h1-semi error of the P1 field `coeffs` (device, n_dofs) vs the manufactured exact solution
 void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, double rho, double* l2, double* h1);
+// assembly.cpp:312-331: squared L2 distance of the P1 field to the target (the target's rule)
+double l2_error_target_squared(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, int kind,
+                               uint64_t seed);
 
 }  // namespace rdg
 

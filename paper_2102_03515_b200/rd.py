@@ -129,6 +129,7 @@ def lib():
         "rd_gpu_pcg": (_I, [_P, _P, _P, _P, _D, _I, _P, _P, _P]),
         "rd_gpu_solve_system_amg": (_I, [_P, _P, _P, _D, _P, _P]),
         "rd_gpu_error_norms": (_I, [_P, _P, _P, _P, _D, C.POINTER(_D), C.POINTER(_D)]),
+        "rd_gpu_l2_error_target_squared": (_I, [_P, _P, _P, _P, _P, C.POINTER(_D)]),
         # distributed (z-slab) pieces, dist.py
         "rd_gpu_ctx_set_exact_sweeps": (_I, [_P, _I]),
         "rd_gpu_csr_rowblock": (_I, [_P, _P, _I, _I, _I, _I, C.POINTER(_P)]),
@@ -417,6 +418,21 @@ def error_norms(sys: FemSystem, coeffs, rho_exact: float):
     ctx.check(lib().rd_gpu_error_norms(ctx.h, sys.mesh.h, sys.h, _ptr(coeffs) if sys.n_dofs else None,
                                        float(rho_exact), C.byref(l2), C.byref(h1)))
     return l2.value, h1.value
+
+
+def l2_error_target_squared(sys: FemSystem, coeffs, target: str, seed: int = 0) -> float:
+    """assembly.hpp:62 / assembly.cpp:312-331 on the device: squared L2 distance of the P1 field
+    with interior coefficients `coeffs` to the target field (the target's own quadrature rule)."""
+    ctx = sys.ctx
+    if isinstance(coeffs, np.ndarray) or isinstance(coeffs, (list, tuple)):
+        coeffs = np.ascontiguousarray(coeffs, np.float64)
+        if coeffs.size != sys.n_dofs:
+            raise RdInvalidArgument("l2_error_target_squared: coefficient vector size mismatch")
+    t = _Target(TARGETS[target], int(seed))
+    out = _D()
+    ctx.check(lib().rd_gpu_l2_error_target_squared(ctx.h, sys.mesh.h, sys.h, _ptr(coeffs) if sys.n_dofs else None,
+                                                   C.byref(t), C.byref(out)))
+    return out.value
 
 
 # ------------------------------------------------------------------ kernels

@@ -515,3 +515,20 @@ def test_c2_full_solve(rd, O):  # BASELINE config 2 at full size: n=128, rho=h^2
     assert np.abs(out.u - ref.u).max() <= 1e-10 * np.abs(ref.u).max()
     h = rd.build_amg(ds.A)
     assert [h.stencil_source(l) for l in range(h.num_levels - 1)][:2] == ["uniform", "class"]
+
+
+@pytest.mark.parametrize("n,rho,target", [(16, 2.0 ** -8, "ball"), (16, 1e-2, "sine_random"), (16, 2.0 ** -8, "smooth"),
+                                          (12, 1.0, "box"), (8, 1.0, "quadratic")])
+def test_l2_error_target_squared(rd, O, n, rho, target):
+    """assembly.cpp:312-331 on the device (the BASELINE error gate ||u - u_bar||_L2 for every
+    target) against the oracle on the oracle's converged solution: 1e-12 relative."""
+    om = O.build_structured_cube(n)
+    os_ = O.build_system(om, rho, target)
+    ref = O.solve_system_amg(os_, 1e-10)
+    want = O.l2_error_target_squared(om, os_, ref.u, target, n)
+    ds = rd.build_system(rd.build_structured_cube(n), rho, target)
+    got = rd.l2_error_target_squared(ds, ref.u, target)
+    assert abs(got - want) <= 1e-12 * want, (got, want)
+    z = np.zeros(ds.n_dofs)
+    assert abs(rd.l2_error_target_squared(ds, z, target) - O.l2_error_target_squared(om, os_, z, target, n)) <= \
+        1e-12 * O.l2_error_target_squared(om, os_, z, target, n)

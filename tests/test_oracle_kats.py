@@ -484,3 +484,16 @@ def test_appendix_a_hierarchy(O):  # SURVEY.md Appendix A table (n = 32)
     a, b, c = idx % m, (idx // m) % m, idx // (m * m)
     even = ((a % 2 == 0) & (b % 2 == 0) & (c % 2 == 0)).astype(np.uint8)
     assert np.array_equal(h.flags(0), even)
+
+
+def test_l2_error_target_squared_kats(O):
+    """assembly.cpp:312-331 restated: exact integrals of the target against the zero field."""
+    n = 4
+    m = O.build_structured_cube(n)
+    for target, want in [("zero", 0.0), ("one", 1.0), ("quadratic", 35.0 / 18.0)]:
+        s = O.build_system(m, 1.0, target)
+        got = O.l2_error_target_squared(m, s, np.zeros(s.n_dofs), target)
+        assert abs(got - want) <= 1e-13 * max(1.0, want), (target, got, want)
+    # the P1 interpolant of a linear field is exact: zero distance up to rounding
+    s = O.build_system(m, 1.0, "one")
+    assert O.l2_error_target_squared(m, s, np.ones(s.n_dofs), "one") > 0.0  # boundary nodes are 0
