@@ -187,6 +187,12 @@ int rd_gpu_error_norms(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, c
 int rd_gpu_l2_error_target_squared(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs,
                                    const rd_target* target, double* err2);
 
+/* replaces the rho-coupled table's target_dual_norm(sys, sol)  bench.cpp:55-63 with
+ * target_residual (assembly.cpp:354-356) and hminus1_norm[_with] (assembly.cpp:333-352):
+ * r = f - M u, w = K^-1 r (dense LLT for n <= 2000, else AMG(K)-PCG to 1e-11), sqrt(r . w).
+ * RD_ERUNTIME on a negative pairing, RD_ENOTSPD if K is not SPD.                      */
+int rd_gpu_target_dual_norm(rd_ctx* ctx, const rd_system* sys, const double* coeffs, double* out);
+
 /* ------------------------------------------------------------ distributed (z-slab) pieces
  * SURVEY.md §8(e).  The reference has no distributed solver (its parallelism is
  * the thread pool of parallel.cpp:12-73); these calls are the per-rank device

@@ -96,6 +96,7 @@ def lib():
                              C.POINTER(_D), C.POINTER(_D), C.POINTER(_D)]),
         "or_l2_error_manufactured": (_I, [_P, _P, _pd, _D, C.POINTER(_D)]),
         "or_l2_error_target_squared": (_I, [_P, _P, _pd, _I, _I, C.c_uint64, C.POINTER(_D)]),
+        "or_target_dual_norm": (_I, [_P, _pd, C.POINTER(_D)]),
         "or_h1_semi_error_manufactured": (_I, [_P, _P, _pd, _D, C.POINTER(_D)]),
     }
     for name, (res, args) in sig.items():
@@ -471,4 +472,11 @@ def l2_error_target_squared(mesh: Mesh, sys: FemSystem, coeffs, target: str, n: 
     out = _D()
     _check(lib().or_l2_error_target_squared(mesh._h.h, sys._h.h, np.ascontiguousarray(coeffs, np.float64),
                                             TARGETS[target], int(n), int(seed), C.byref(out)))
+    return out.value
+
+
+def target_dual_norm(sys: FemSystem, coeffs) -> float:
+    """bench.cpp:55-63: ||f - M u||_{H^-1} via K (dense LLT for n <= 2000, else AMG-PCG at 1e-11)."""
+    out = _D()
+    _check(lib().or_target_dual_norm(sys._h.h, np.ascontiguousarray(coeffs, np.float64), C.byref(out)))
     return out.value

@@ -1128,6 +1128,29 @@ double l2_error_target_squared(const Mesh& m, const DofMap& dm, const double* co
   });
 }
 
+// bench.cpp:55-63 target_dual_norm with target_residual (assembly.cpp:354-356) and
+// hminus1_norm[_with] (assembly.cpp:333-352): r = f - M u, w = K^-1 r, sqrt(r . w)
+double target_dual_norm(const System& s, const double* coeffs) {
+  const int n = s.dm.n_dofs();
+  const Vec u(coeffs, coeffs + n);
+  const Vec Mu = spmv(s.M, u);
+  Vec r(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) r[static_cast<size_t>(i)] = s.f[static_cast<size_t>(i)] - Mu[static_cast<size_t>(i)];
+  Vec w;
+  if (n <= 2000) {
+    const Llt f = llt_compute(n, to_dense(s.K));
+    if (!f.ok) throw std::runtime_error("dense_cholesky_solve: matrix not positive definite");
+    w = llt_solve(f, r);
+  } else {
+    const Amg hk = build_amg(s.K, 64, 1);
+    w = pcg([&](const Vec& x) { return spmv(s.K, x); }, [&](const Vec& x) { return amg_apply(hk, x); }, r, 1e-11, 500)
+            .x;
+  }
+  const double rw = dot(r, w);
+  if (rw < 0.0) throw std::runtime_error("hminus1_norm: negative dual pairing");
+  return std::sqrt(rw);
+}
+
 template <class F>
 int guard(F&& fn) {
   try {
@@ -1453,6 +1476,9 @@ int or_pipeline(int n, double rho, int kind, uint64_t seed, double tol, int* ite
 
 int or_l2_error_manufactured(const or_mesh* m, const or_system* s, const double* coeffs, double rho, double* out) {
   return guard([&] { *out = l2_error(m->m, s->s.dm, coeffs, manufactured_exact(rho)); });
+}
+int or_target_dual_norm(const or_system* s, const double* coeffs, double* out) {
+  return guard([&] { *out = target_dual_norm(s->s, coeffs); });
 }
 int or_l2_error_target_squared(const or_mesh* m, const or_system* s, const double* coeffs, int kind, int n,
                                uint64_t seed, double* out) {

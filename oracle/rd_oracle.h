@@ -109,6 +109,7 @@ int or_pipeline(int n, double rho, int target_kind, uint64_t seed, double tol, i
 /* assembly.cpp:265-310 error norms against the closed form (manufactured_exact) */
 int or_l2_error_manufactured(const or_mesh* m, const or_system* s, const double* coeffs,
                              double rho_exact, double* out);
+int or_target_dual_norm(const or_system* s, const double* coeffs, double* out);
 int or_l2_error_target_squared(const or_mesh* m, const or_system* s, const double* coeffs, int kind, int n,
                                uint64_t seed, double* out);
 int or_h1_semi_error_manufactured(const or_mesh* m, const or_system* s,

@@ -883,6 +883,13 @@ void build_hierarchy(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, 
   if (!build_levels(c, A, threshold, m, h, borrow, /*direct=*/true)) build_levels(c, A, threshold, m, h, borrow, false);
 }
 
+void dense_llt_solve(Ctx& c, int n, const double* L, const double* b, double* x) {
+  if (n == 0) return;
+  llt_solve_kernel<<<1, kCoarseNT, sizeof(double) * n, c.stream>>>(n, L, b, x);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+}
+
 void coarse_solve(Ctx& c, Hierarchy& h, const double* r, double* z) {
   const int n = h.nc;
   if (n == 0) return;

@@ -2,6 +2,7 @@
 //
 // Each function converts rdg::Error into the status code that maps onto the
 // reference's exception type and leaves the message in rd_gpu_last_error().
+#include <cmath>
 #include <cstdlib>
 #include <chrono>
 #include <cstring>
@@ -557,6 +558,40 @@ int rd_gpu_error_norms(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, c
     DBuf<double> tc;
     const double* cd = in_dev(c, coeffs, sys->s.n_dofs, tc);
     error_norms(c, mesh->m, sys->s, cd, rho, l2, h1);
+  });
+}
+
+int rd_gpu_target_dual_norm(rd_ctx* ctx, const rd_system* sys, const double* coeffs, double* out) {
+  return guard(ctx, [&] {
+    require(sys && coeffs && out, "target_dual_norm: null argument");
+    Ctx& c = ctx->c;
+    const DSystem& S = sys->s;
+    const int n = S.n_dofs;
+    if (n == 0) {
+      *out = 0.0;
+      return;
+    }
+    DBuf<double> tc, r(n, c.stream), w(n, c.stream), rw(1, c.stream);
+    const double* u = in_dev(c, coeffs, n, tc);
+    residual(c, S.M, S.f.p, u, r.p);  // target_residual: f - M u (assembly.cpp:354-356)
+    exact_retry(c, [&] {
+      if (n <= 2000) {  // hminus1_norm's dense branch (assembly.cpp:342-347)
+        DBuf<double> Lk;
+        dense_llt(c, S.K, Lk);
+        dense_llt_solve(c, n, Lk.p, r.p, w.p);
+      } else {  // bench.cpp:58-61: AMG on K, PCG to 1e-11 from zero
+        Hierarchy hk;
+        build_hierarchy(c, S.K, 64, 1, hk);
+        pcg_device(c, S.K, &hk, r.p, 1e-11, 500, w.p, nullptr);
+      }
+      sync_and_raise(c);
+    });
+    dot(c, n, r.p, w.p, rw.p);
+    double h = 0.0;
+    RDG_CUDA(cudaMemcpyAsync(&h, rw.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    if (h < 0.0) throw Error(RD_ERUNTIME, "hminus1_norm: negative dual pairing");
+    *out = std::sqrt(h);
   });
 }
 

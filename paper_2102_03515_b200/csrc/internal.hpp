@@ -151,6 +151,8 @@ void build_hierarchy(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, 
 void vcycle(Ctx& c, Hierarchy& h, const double* r, double* z, double* dot_out, int l0 = 0);
 // throws RD_ENOTSPD, or (err_dev) leaves the failure flag on the device
 void dense_llt(Ctx& c, const DCsr& A, DBuf<double>& L, int* err_dev = nullptr);
+// x = L^-T L^-1 b with the dense factor of dense_llt (llt_solve_kernel's order), device vectors
+void dense_llt_solve(Ctx& c, int n, const double* L, const double* b, double* x);
 
 // ---------------------------------------------------------------- pcg.cu
 struct PcgResultDev {

@@ -130,6 +130,7 @@ def lib():
         "rd_gpu_solve_system_amg": (_I, [_P, _P, _P, _D, _P, _P]),
         "rd_gpu_error_norms": (_I, [_P, _P, _P, _P, _D, C.POINTER(_D), C.POINTER(_D)]),
         "rd_gpu_l2_error_target_squared": (_I, [_P, _P, _P, _P, _P, C.POINTER(_D)]),
+        "rd_gpu_target_dual_norm": (_I, [_P, _P, _P, C.POINTER(_D)]),
         # distributed (z-slab) pieces, dist.py
         "rd_gpu_ctx_set_exact_sweeps": (_I, [_P, _I]),
         "rd_gpu_csr_rowblock": (_I, [_P, _P, _I, _I, _I, _I, C.POINTER(_P)]),
@@ -432,6 +433,18 @@ def l2_error_target_squared(sys: FemSystem, coeffs, target: str, seed: int = 0) 
     out = _D()
     ctx.check(lib().rd_gpu_l2_error_target_squared(ctx.h, sys.mesh.h, sys.h, _ptr(coeffs) if sys.n_dofs else None,
                                                    C.byref(t), C.byref(out)))
+    return out.value
+
+
+def target_dual_norm(sys: FemSystem, coeffs) -> float:
+    """bench.cpp:55-63 on the device: ||f - M u||_{H^-1} = sqrt(r . K^-1 r)."""
+    ctx = sys.ctx
+    if isinstance(coeffs, np.ndarray) or isinstance(coeffs, (list, tuple)):
+        coeffs = np.ascontiguousarray(coeffs, np.float64)
+        if coeffs.size != sys.n_dofs:
+            raise RdInvalidArgument("target_dual_norm: coefficient vector size mismatch")
+    out = _D()
+    ctx.check(lib().rd_gpu_target_dual_norm(ctx.h, sys.h, _ptr(coeffs) if sys.n_dofs else None, C.byref(out)))
     return out.value
 
 

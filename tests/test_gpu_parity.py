@@ -532,3 +532,18 @@ def test_l2_error_target_squared(rd, O, n, rho, target):
     z = np.zeros(ds.n_dofs)
     assert abs(rd.l2_error_target_squared(ds, z, target) - O.l2_error_target_squared(om, os_, z, target, n)) <= \
         1e-12 * O.l2_error_target_squared(om, os_, z, target, n)
+
+
+@pytest.mark.parametrize("n,rho,target", [(8, 1e-2, "smooth"), (8, 1.0, "ball"), (16, 2.0 ** -8, "ball"),
+                                          (16, 1e-4, "sine_random")])
+def test_target_dual_norm(rd, O, n, rho, target):
+    """bench.cpp:55-63 on the device: dense LLT of K for n_dofs <= 2000 (n=8: agreement to
+    rounding), AMG(K)-PCG to 1e-11 above (n=16: the generic, non-lattice K hierarchy)."""
+    om = O.build_structured_cube(n)
+    os_ = O.build_system(om, rho, target)
+    u = O.solve_system_amg(os_, 1e-10).u
+    want = O.target_dual_norm(os_, u)
+    ds = rd.build_system(rd.build_structured_cube(n), rho, target)
+    got = rd.target_dual_norm(ds, u)
+    tol = 1e-12 if (n - 1) ** 3 <= 2000 else 1e-8
+    assert abs(got - want) <= tol * want, (got, want)
