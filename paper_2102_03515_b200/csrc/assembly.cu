@@ -19,6 +19,8 @@
 #include <cmath>
 #include <utility>
 
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace rdg {
@@ -572,6 +574,49 @@ __device__ __forceinline__ void lat_row_all(std::integer_sequence<int, E...>, in
   (lat_row_tet<E>(v, nv, xyz, K, M, ok), ...);
 }
 
+// Uniform geometry: every cell's six Kuhn tets have, bit for bit, the edge vectors
+// v1-v0, v2-v0, v3-v0 of cell (0,0,0)'s (exact for n = 2^k, coordinates i/n).  Then
+// local_geom -- a function of those vectors only -- and so every row's 24 tet terms,
+// summed in the same order, equal the reference row's: one row is computed, the
+// others copy it.  Checked per cell on the device; any mismatch keeps the per-row sums.
+__global__ void lat_geom_check_kernel(int n, const double* __restrict__ xyz, int* nonuni) {
+  const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= (int64_t)n * n * n) return;
+  const int nv = n + 1;
+  const int ci = (int)(cell % n), cj = (int)((cell / n) % n), ck = (int)(cell / ((int64_t)n * n));
+  const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};  // mesh.cpp:46-47
+  bool same = true;
+  for (int p = 0; p < 6 && same; ++p) {
+    int c[3] = {ci, cj, ck}, r[3] = {0, 0, 0};
+    const int64_t a0 = ((int64_t)c[2] * nv + c[1]) * nv + c[0], b0 = ((int64_t)r[2] * nv + r[1]) * nv + r[0];
+    for (int e = 0; e < 3 && same; ++e) {
+      c[perms[p][e]] += 1;
+      r[perms[p][e]] += 1;
+      const int64_t a = ((int64_t)c[2] * nv + c[1]) * nv + c[0], b = ((int64_t)r[2] * nv + r[1]) * nv + r[0];
+      for (int d = 0; d < 3; ++d)
+        same = same && __double_as_longlong(__dsub_rn(xyz[3 * a + d], xyz[3 * a0 + d])) ==
+                           __double_as_longlong(__dsub_rn(xyz[3 * b + d], xyz[3 * b0 + d]));
+    }
+  }
+  if (!same) *nonuni = 1;
+}
+
+// the reference row (vertex at the cube's centre: all 24 incident tets exist): km = K[15], M[15]
+__global__ void lat_row_ref_kernel(int n, const double* __restrict__ xyz, double* km, int* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int nv = n + 1, c = n / 2;
+  const int v = (c * nv + c) * nv + c;
+  double K[15], M[15];
+  for (int s = 0; s < 15; ++s) K[s] = M[s] = 0.0;
+  bool ok = true;
+  lat_row_all(std::make_integer_sequence<int, 24>{}, v, nv, xyz, K, M, ok);
+  if (!ok) atomicExch(err, RD_EDEGENERATE);
+  for (int s = 0; s < 15; ++s) {
+    km[s] = K[s];
+    km[15 + s] = M[s];
+  }
+}
+
 // Row r: 15 K and M slots (slot-major, padded [15][nd]), the interior-column
 // mask, and the pruned counts of K, M and A = K u M.
 constexpr int kLatNT = 128;
@@ -579,7 +624,8 @@ __global__ void __launch_bounds__(kLatNT) lat_values_kernel(int nd, int n, const
                                                            const int* __restrict__ v2d,
                                                            const double* __restrict__ xyz, double* Kp, double* Mp,
                                                            unsigned short* mask, int* kc, int* mc, int* ac,
-                                                           int* err) {
+                                                           int* err, const int* __restrict__ geo_nonuni,
+                                                           const double* __restrict__ km) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nd) return;
   const int nv = n + 1;
@@ -593,7 +639,15 @@ __global__ void __launch_bounds__(kLatNT) lat_values_kernel(int nd, int n, const
 #pragma unroll
   for (int s = 0; s < 15; ++s) K[s] = M[s] = 0.0;
   bool ok = true;
-  lat_row_all(std::make_integer_sequence<int, 24>{}, v, nv, xyz, K, M, ok);
+  if (*geo_nonuni == 0) {  // uniform geometry: the reference row's sums
+#pragma unroll
+    for (int s = 0; s < 15; ++s) {
+      K[s] = km[s];
+      M[s] = km[15 + s];
+    }
+  } else {
+    lat_row_all(std::make_integer_sequence<int, 24>{}, v, nv, xyz, K, M, ok);
+  }
   if (!ok) atomicExch(err, RD_EDEGENERATE);
   unsigned m = 0;
   int a = 0, b = 0, u = 0;
@@ -1153,8 +1207,20 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
     DBuf<double> Kp((size_t)15 * nd, c.stream), Mp((size_t)15 * nd, c.stream);
     DBuf<unsigned short> mask(nd, c.stream);
     DBuf<int> kc(nd, c.stream), mc(nd, c.stream), ac(nd, c.stream);
+    DBuf<int> geo(1, c.stream);
+    DBuf<double> km(30, c.stream);
+    static const bool nogeo = getenv("RD_NO_UNIFORM_GEOMETRY") && atoi(getenv("RD_NO_UNIFORM_GEOMETRY")) != 0;
+    const int geo0 = nogeo ? 1 : 0;
+    RDG_CUDA(cudaMemcpyAsync(geo.p, &geo0, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    if (!nogeo) {
+      lat_geom_check_kernel<<<div_up((int64_t)n * n * n, 256), 256, 0, c.stream>>>(n, m.xyz.p, geo.p);
+      RDG_LAUNCH_CHECK();
+      lat_row_ref_kernel<<<1, 32, 0, c.stream>>>(n, m.xyz.p, km.p, err.p);
+      RDG_LAUNCH_CHECK();
+      c.launches += 2;
+    }
     lat_values_kernel<<<div_up(nd, kLatNT), kLatNT, 0, c.stream>>>(nd, n, s.d2v.p, s.v2d.p, m.xyz.p, Kp.p, Mp.p,
-                                                                  mask.p, kc.p, mc.p, ac.p, err.p);
+                                                                  mask.p, kc.p, mc.p, ac.p, err.p, geo.p, km.p);
     RDG_LAUNCH_CHECK();
     ++c.launches;
     const int e = read_flag(c, err.p);
