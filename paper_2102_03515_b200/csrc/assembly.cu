@@ -659,8 +659,10 @@ __global__ void __launch_bounds__(kLatNT) lat_values_kernel(int nd, int n, const
     a += kk;
     b += mm;
     u += (kk || mm);
-    Kp[(int64_t)s * nd + r] = K[s];
-    Mp[(int64_t)s * nd + r] = M[s];
+    if (*geo_nonuni != 0) {  // uniform geometry: lat_split reads the reference row instead
+      Kp[(int64_t)s * nd + r] = K[s];
+      Mp[(int64_t)s * nd + r] = M[s];
+    }
   }
   mask[r] = (unsigned short)m;
   kc[r] = a;
@@ -679,7 +681,9 @@ __global__ void __launch_bounds__(kLatNT) lat_split_kernel(int nd, int n, double
                                                           const unsigned short* __restrict__ mask,
                                                           const int* __restrict__ krp, int* kci, double* kv,
                                                           const int* __restrict__ mrp, int* mci, double* mv,
-                                                          const int* __restrict__ arp, int* aci, double* av) {
+                                                          const int* __restrict__ arp, int* aci, double* av,
+                                                          const int* __restrict__ geo_nonuni,
+                                                          const double* __restrict__ km) {
   __shared__ int scol[kLatNT / 32][32 * 15];
   __shared__ double sval[kLatNT / 32][32 * 15];
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
@@ -691,14 +695,15 @@ __global__ void __launch_bounds__(kLatNT) lat_split_kernel(int nd, int n, double
   const int nv = n + 1;
   const int v = row ? d2v[r] : 0;
   const unsigned m = row ? mask[r] : 0u;
+  const bool uni = *geo_nonuni == 0;
   int col[15];
   double kq[15], mq[15];
 #pragma unroll
   for (int s = 0; s < 15; ++s) {
     const bool on = (m >> s) & 1u;
     col[s] = on ? v2d[v + lat_code_off(c_lat_tab.sten[s], nv)] : 0;
-    kq[s] = on ? Kp[(int64_t)s * nd + r] : 0.0;
-    mq[s] = on ? Mp[(int64_t)s * nd + r] : 0.0;
+    kq[s] = on ? (uni ? km[s] : Kp[(int64_t)s * nd + r]) : 0.0;
+    mq[s] = on ? (uni ? km[15 + s] : Mp[(int64_t)s * nd + r]) : 0.0;
   }
   int* sc = scol[wq];
   double* sv = sval[wq];
@@ -1230,7 +1235,7 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
       alloc_split(cnts);
       lat_split_kernel<<<div_up(nd, kLatNT), kLatNT, 0, c.stream>>>(
           nd, n, rho, s.d2v.p, s.v2d.p, Kp.p, Mp.p, mask.p, s.K.rp.p, s.K.ci.p, s.K.v.p, s.M.rp.p, s.M.ci.p,
-          s.M.v.p, s.A.rp.p, s.A.ci.p, s.A.v.p);
+          s.M.v.p, s.A.rp.p, s.A.ci.p, s.A.v.p, geo.p, km.p);
       RDG_LAUNCH_CHECK();
       ++c.launches;
       if ((int64_t)nd == (int64_t)(n - 1) * (n - 1) * (n - 1)) {
