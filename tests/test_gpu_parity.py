@@ -7,6 +7,9 @@ Bars (BASELINE.json north star):
   * PCG: iteration counts equal, solutions within 1e-10 relative (dot products are
     reduced in a different -- deterministic -- order than Eigen's SSE2 dot).
 """
+import math
+import os
+
 import numpy as np
 import pytest
 
@@ -547,3 +550,30 @@ def test_target_dual_norm(rd, O, n, rho, target):
     got = rd.target_dual_norm(ds, u)
     tol = 1e-12 if (n - 1) ** 3 <= 2000 else 1e-8
     assert abs(got - want) <= tol * want, (got, want)
+
+
+def _goldens():
+    import json as _json
+    return _json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                        "baseline_configs.json")))["cases"]
+
+
+@pytest.mark.parametrize("case", _goldens(), ids=lambda c: c["name"])
+def test_baseline_config_goldens(rd, case):
+    """BASELINE configs C1, C2 and the C3 rho sweep against the committed oracle goldens
+    (tools/make_goldens.py): iteration count equal, residual history / solution / error gates
+    within the north star's 1e-10."""
+    n, rho, target = case["n"], case["rho"], case["target"]
+    ds = rd.build_system(rd.build_structured_cube(n), rho, target)
+    out = rd.pcg(ds.A, "amg", ds.f(), 1e-8, 500)
+    assert out.converged and out.iterations == case["iterations"]
+    assert np.allclose(out.residual_history, case["residual_history"], rtol=1e-9, atol=0)
+    u = out.x
+    assert abs(np.linalg.norm(u) - case["u_norm2"]) <= 1e-10 * case["u_norm2"]
+    for i, v in case["u_samples"].items():
+        assert abs(u[int(i)] - v) <= 1e-10 * np.abs(u).max()
+    l2 = math.sqrt(rd.l2_error_target_squared(ds, u, target))
+    assert abs(l2 - case["l2_u_minus_target"]) <= 1e-10 * case["l2_u_minus_target"]
+    if "h1_u_minus_target" in case:
+        _, h1 = rd.error_norms(ds, u, 0.0)
+        assert abs(h1 - case["h1_u_minus_target"]) <= 1e-10 * case["h1_u_minus_target"]

@@ -497,3 +497,17 @@ def test_l2_error_target_squared_kats(O):
     # the P1 interpolant of a linear field is exact: zero distance up to rounding
     s = O.build_system(m, 1.0, "one")
     assert O.l2_error_target_squared(m, s, np.ones(s.n_dofs), "one") > 0.0  # boundary nodes are 0
+
+
+def test_oracle_reproduces_c1_golden(O):
+    """The committed goldens (tools/make_goldens.py) are the oracle's own answers: C1 re-run."""
+    g = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                    "baseline_configs.json")))["cases"]
+    c1 = next(c for c in g if c["name"] == "C1")
+    m = O.build_structured_cube(c1["n"])
+    s = O.build_system(m, c1["rho"], c1["target"])
+    r = O.pcg(s.A, "amg", s.f, 1e-8, 500)
+    assert r.iterations == c1["iterations"]
+    assert [float(v) for v in r.residual_history] == c1["residual_history"]
+    assert float(np.linalg.norm(r.x)) == c1["u_norm2"]
+    assert math.sqrt(O.l2_error_target_squared(m, s, r.x, "smooth")) == c1["l2_u_minus_target"]
