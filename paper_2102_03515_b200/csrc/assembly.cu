@@ -1157,7 +1157,9 @@ void detect_cube_lattice(Ctx& c, DMesh& m) {
 void build_structured_cube(Ctx& c, int n, DMesh& m) {
   if (n < 1) throw Error(RD_EINVAL, "build_structured_cube: n must be >= 1");
   const int64_t nv = (int64_t)(n + 1) * (n + 1) * (n + 1), nt = (int64_t)n * n * n * 6;
-  if (nt * 4 > 0x7fffffffLL) throw Error(RD_EINVAL, "build_structured_cube: n too large for int32 tet ids");
+  // tet and vertex ids are int32 (mesh.hpp:13-24); the lattice assembly never forms the
+  // 4*nt vertex-tet incidence list (the generic path checks its own int32 limit)
+  if (nt > 0x7fffffffLL || nv > 0x7fffffffLL) throw Error(RD_EINVAL, "build_structured_cube: n too large for int32 ids");
   m.nv = (int)nv;
   m.nt = (int)nt;
   m.lattice_n = n;
@@ -1255,6 +1257,8 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
   DBuf<int> vto, vt;
   if (!lattice) {
     DBuf<int> vcnt(nv + 1, c.stream);
+    if ((int64_t)nt * 4 > 0x7fffffffLL)
+      throw Error(RD_EINVAL, "build_system: more than 2^31 vertex-tet incidences on a non-lattice mesh");
     vto.alloc(nv + 1, c.stream);
     vt.alloc(std::max<int64_t>((int64_t)nt * 4, 1), c.stream);
     RDG_CUDA(cudaMemsetAsync(vcnt.p, 0, sizeof(int) * (nv + 1), c.stream));

@@ -577,3 +577,32 @@ def test_baseline_config_goldens(rd, case):
     if "h1_u_minus_target" in case:
         _, h1 = rd.error_norms(ds, u, 0.0)
         assert abs(h1 - case["h1_u_minus_target"]) <= 1e-10 * case["h1_u_minus_target"]
+
+
+@pytest.mark.parametrize("n,target", [(256, "smooth"), (512, "ball")])
+def test_full_size_properties(rd, n, target):
+    """C4 (n=256) and C5 (n=512, 133M dofs) on one B200, where the oracle cannot follow:
+    size-independent properties -- convergence to rtol 1e-8 in the C2-like iteration count, a
+    true residual ||f - A u|| consistent with it, every smoothed level structured, and for the
+    smooth target the O(h^2) error decay against the C1 golden."""
+    rho = 1.0 / n ** 2
+    mesh = rd.build_structured_cube(n)
+    ds = rd.build_system(mesh, rho, target)
+    import torch
+    u = torch.empty(ds.n_dofs, dtype=torch.float64, device="cuda")
+    out = rd.solve_system_amg(ds.A, ds.f_ptr, 1e-8, u=u)
+    assert out.converged and 2 <= out.iterations <= 8
+    f = torch.empty_like(u)
+    rd.lib().rd_gpu_copy(ds.ctx.h, rd._ptr(f), rd.C.c_void_p(ds.f_ptr), 8 * ds.n_dofs)
+    Au = torch.empty_like(u)
+    ds.ctx.check(rd.lib().rd_gpu_spmv(ds.ctx.h, ds.A.h, rd._ptr(u), rd._ptr(Au)))
+    ds.ctx.synchronize()
+    rel = float(torch.linalg.norm(f - Au) / torch.linalg.norm(f))
+    assert rel < 1e-6, rel
+    l2 = math.sqrt(rd.l2_error_target_squared(ds, u, target))
+    if target == "smooth":
+        c1 = next(c for c in _goldens() if c["name"] == "C1")
+        ratio = c1["l2_u_minus_target"] / l2
+        assert 30 < ratio < 130, ratio  # h: 1/32 -> 1/256, rho = h^2 coupled: ~(h1/h2)^2 = 64
+    else:
+        assert 0.0 < l2 < 0.1
