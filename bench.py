@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--target", default=TARGET)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-extra", action="store_true", help="skip the C4 / C5 single-GPU runs")
     p.add_argument("--profile", action="store_true", help="short run for ncu: 1 step, no extras")
     p.add_argument("--mode", default="pipelined", choices=["pipelined", "exact", "block"],
                    help="N > 1: smoother hand-off between slabs: pipelined = the sweep kernels write the "
@@ -494,10 +495,48 @@ def run_ours(args, rank, world, local_rank):
                          "path": "rd_gpu_mesh_create(pinned host TetMesh) -> rd_gpu_build_system -> "
                                  "rd_gpu_solve_system_amg(u -> pinned host)"}
 
+    # ---------------- the other BASELINE sizes on this GPU (C4 n=256, C5 n=512 = 133M dofs):
+    # one timed solve each after a warm-up, same path; reported beside the C2 headline
+    if rank == 0 and world == 1 and not args.no_extra:
+        result["other_configs"] = other_configs(ctx, stream)
     # ---------------- CPU baseline (rank 0, N = 1): the oracle port on the host cores
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(n, args.target)
     return result
+
+
+def other_configs(ctx, stream):
+    import torch
+
+    from paper_2102_03515_b200 import rd
+
+    out = []
+    for name, n, target in (("C4", 256, "smooth"), ("C5", 512, "ball")):
+        try:
+            rho = rho_for(n)
+            mesh = rd.build_structured_cube(n, ctx)
+            u = None
+            for rep in range(2):  # warm-up, then the timed step
+                ctx.synchronize()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                s = rd.build_system(mesh, rho, target)
+                if u is None:
+                    u = torch.empty(s.n_dofs, dtype=torch.float64, device=stream.device)
+                o = rd.solve_system_amg(s.A, s.f_ptr, TOL, u=u)
+                b.record(stream)
+                torch.cuda.synchronize()
+                ms = a.elapsed_time(b)
+                nd = s.n_dofs
+                del s
+            out.append({"config": name, "n": n, "n_dofs": nd, "target": target, "rho": rho, "iterations": o.iterations,
+                        "ms_per_step": ms, "value": nd * o.iterations / (ms / 1e3), "unit": UNIT,
+                        "phases_ms": {"setup": 1e3 * o.setup_seconds, "pcg": 1e3 * o.solve_seconds}})
+            del mesh, u
+        except Exception as e:  # reported, never fatal for the headline line
+            out.append({"config": name, "error": str(e)[:200]})
+    return out
 
 
 def host_threads():
