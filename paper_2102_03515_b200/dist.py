@@ -127,9 +127,14 @@ class TorchComm:
     def link_slabs(self, ops, G):
         """Map the neighbours' slab cell buffers (CUDA IPC over NVLink) for the pipelined hand-off."""
         for l in range(G):
-            mine = (ops.ipc_handle(l), ops.slab_g0(l))
+            try:  # every rank reaches the collective, even when its own export fails
+                mine = (ops.ipc_handle(l), ops.slab_g0(l))
+            except Exception:  # noqa: BLE001
+                mine = None
             allh = [None] * self.world
             self.dist.all_gather_object(allh, mine, group=self.group)
+            if any(h is None for h in allh):
+                raise RuntimeError("slab cell buffers could not be exported for CUDA IPC")
             if self.rank + 1 < self.world:
                 ops.open_peer(l, 0, *allh[self.rank + 1])
             if self.rank > 0:
@@ -440,7 +445,16 @@ class DistSolver:
         self.G = G
         ops.localize(self.plan, self.rank)
         if mode == "pipelined":
-            comm.link_slabs(ops, G)
+            # peer mapping of the neighbours' cell buffers; if any rank cannot map (no P2P
+            # path, IPC unavailable) every rank falls back to the NCCL plane hand-off
+            ok = 1
+            try:
+                comm.link_slabs(ops, G)
+            except Exception as e:  # noqa: BLE001 -- reported through the fallback
+                self.link_error = repr(e)
+                ok = 0
+            if not all(comm.allgather_int(ok)):
+                self.mode = "exact"
         R = self.rank
         pl = self.plan
         self.r = [None] + [ops.vec(l) for l in range(1, G + 1)]
