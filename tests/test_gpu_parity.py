@@ -606,3 +606,16 @@ def test_full_size_properties(rd, n, target):
         assert 30 < ratio < 130, ratio  # h: 1/32 -> 1/256, rho = h^2 coupled: ~(h1/h2)^2 = 64
     else:
         assert 0.0 < l2 < 0.1
+
+
+@pytest.mark.parametrize("n,thr,m", [(16, 64, 2), (32, 64, 3), (32, 512, 2), (33, 64, 2), (64, 64, 0)])
+def test_amg_apply_smoothing_steps(rd, O, n, thr, m):
+    """build_amg(A, threshold, m) with m != 1 (amg.cpp:90-132: m symmetric sweeps before and
+    after the coarse correction; m = 0 skips smoothing): the structured levels, the one-CTA
+    coarse tail and the generic path (n = 33: side 32 levels) against the oracle, bit for bit."""
+    os_ = O.build_system(O.build_structured_cube(n), 1.0 / n ** 2, "ball")
+    oh = O.build_amg(os_.A, thr, m)
+    ds = rd.build_system(rd.build_structured_cube(n), 1.0 / n ** 2, "ball")
+    dh = rd.build_amg(ds.A, thr, m)
+    r = O.pseudo_random_vec(os_.A.rows, 5)
+    assert np.array_equal(dh.apply(r), oh.apply(r))
