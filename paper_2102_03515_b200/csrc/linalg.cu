@@ -143,7 +143,13 @@ int64_t exclusive_scan(Ctx& c, const int* counts, int* offsets, int64_t n, const
 namespace {
 constexpr int kSpmvWarps = 8;
 constexpr int kSpmvNT = kSpmvWarps * 32;
-constexpr int kSpmvCap = 512;  // staged nnz per warp per chunk
+#ifndef RD_SPMV_CAP
+#define RD_SPMV_CAP 512
+#endif
+#ifndef RD_SPMV_BATCH
+#define RD_SPMV_BATCH 0
+#endif
+constexpr int kSpmvCap = RD_SPMV_CAP;  // staged nnz per warp per chunk
 
 enum SpmvMode { kPlain = 0, kDot = 1, kResidual = 2 };
 
@@ -153,7 +159,7 @@ struct SpmvSmem {
   double red[kSpmvWarps];
 };
 
-template <int MODE>
+template <int MODE, bool ASYNC = true>
 __global__ void __launch_bounds__(kSpmvNT) spmv_staged_kernel(int rows, const int* __restrict__ rp,
                                                               const int* __restrict__ ci,
                                                               const double* __restrict__ val,
@@ -183,11 +189,37 @@ __global__ void __launch_bounds__(kSpmvNT) spmv_staged_kernel(int rows, const in
       const int4* gi = reinterpret_cast<const int4*>(ci + ia);
       double2* sv = reinterpret_cast<double2*>(sm.v[warp]);
       int4* si = reinterpret_cast<int4*>(sm.ci[warp]);
-      for (int t = lane; t < nv2; t += 32) sv[t] = __ldg(gv + t);
-      for (int t = lane; t < ni4; t += 32) si[t] = __ldg(gi + t);
+      if (ASYNC) {
+        // every 16-byte piece of the block in flight at once (cp.async), then one wait:
+        // a load -> shared store per iteration would serialise the DRAM round trips
+        for (int t = lane; t < nv2; t += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(sv + t)),
+                       "l"(gv + t)
+                       : "memory");
+        for (int t = lane; t < ni4; t += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(si + t)),
+                       "l"(gi + t)
+                       : "memory");
+        asm volatile("cp.async.wait_all;" ::: "memory");
+      } else {
+        for (int t = lane; t < nv2; t += 32) sv[t] = __ldg(gv + t);
+        for (int t = lane; t < ni4; t += 32) si[t] = __ldg(gi + t);
+      }
       __syncwarp();
       const int kb = max(rs, cb), ke = min(re, ce);
+#if RD_SPMV_BATCH
+      // the row's x gathers issued RD_SPMV_BATCH at a time, then summed in column order
+      for (int k0 = kb; k0 < ke; k0 += RD_SPMV_BATCH) {
+        double xv[RD_SPMV_BATCH];
+#pragma unroll
+        for (int u = 0; u < RD_SPMV_BATCH; ++u) xv[u] = k0 + u < ke ? __ldg(x + sm.ci[warp][k0 + u - ia]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < RD_SPMV_BATCH; ++u)
+          if (k0 + u < ke) sum = __dadd_rn(sum, __dmul_rn(sm.v[warp][k0 + u - va], xv[u]));
+      }
+#else
       for (int k = kb; k < ke; ++k) sum = __dadd_rn(sum, __dmul_rn(sm.v[warp][k - va], __ldg(x + sm.ci[warp][k - ia])));
+#endif
       __syncwarp();
     }
     if (lane < nr) {
@@ -260,24 +292,27 @@ void launch_spmv(Ctx& c, const DCsr& A, const double* x, double* y, const double
     return;
   }
   const int nb = div_up(A.rows, kSpmvNT);
+  // A/B timing only: staging through registers instead of cp.async
+  static const bool syncstage = getenv("RD_SPMV_SYNCSTAGE") && atoi(getenv("RD_SPMV_SYNCSTAGE")) != 0;
   static bool attr = false;
   const size_t smem = sizeof(SpmvSmem);
   if (!attr) {
-    RDG_CUDA(cudaFuncSetAttribute(spmv_staged_kernel<kPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    RDG_CUDA(cudaFuncSetAttribute(spmv_staged_kernel<kDot>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    RDG_CUDA(cudaFuncSetAttribute(spmv_staged_kernel<kResidual>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    for (auto* k : {spmv_staged_kernel<kPlain, true>, spmv_staged_kernel<kDot, true>, spmv_staged_kernel<kResidual, true>,
+                    spmv_staged_kernel<kPlain, false>, spmv_staged_kernel<kDot, false>,
+                    spmv_staged_kernel<kResidual, false>})
+      RDG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   if (MODE == kDot && nb > Ctx::kMaxPartials) {
     // too many blocks for one partials array: plain SpMV then a separate dot
-    spmv_staged_kernel<kPlain><<<nb, kSpmvNT, smem, c.stream>>>(A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, nullptr,
+    (syncstage ? spmv_staged_kernel<kPlain, false> : spmv_staged_kernel<kPlain, true>)<<<nb, kSpmvNT, smem, c.stream>>>(A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, nullptr,
                                                                nullptr, nullptr);
     RDG_LAUNCH_CHECK();
     ++c.launches;
     dot(c, A.rows, x, y, dot_out);
     return;
   }
-  spmv_staged_kernel<MODE><<<nb, kSpmvNT, smem, c.stream>>>(A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, c.d_partials,
+  (syncstage ? spmv_staged_kernel<MODE, false> : spmv_staged_kernel<MODE, true>)<<<nb, kSpmvNT, smem, c.stream>>>(A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, c.d_partials,
                                                            c.d_counter, dot_out);
   RDG_LAUNCH_CHECK();
   ++c.launches;

@@ -196,6 +196,11 @@ class ThreadComm:
                 if ev is not None:
                     torch.cuda.current_stream().wait_event(ev)
                 t.copy_(buf)
+                if buf.is_cuda:
+                    # buf was allocated on the sender's stream: without this the caching
+                    # allocator hands the block back to the sender's stream as soon as buf
+                    # is dropped here, before this stream's copy has run
+                    buf.record_stream(torch.cuda.current_stream())
 
     def _allgather(self, v):
         self.hub.vals[self.rank] = v

@@ -31,7 +31,19 @@ while i < len(lines):
     hdr = lines[i].split()
     L, nty, ntz, ns = int(hdr[1]), int(hdr[3]), int(hdr[5]), int(hdr[7])
     T = np.array([[int(v) for v in lines[i + 1 + t].split()] for t in range(nty * ntz)], dtype=np.int64)
-    i += 1 + nty * ntz
+    H = np.array([[int(v) for v in lines[i + 1 + nty * ntz + t].split()] for t in range(nty * ntz)], dtype=np.int64)
+    i += 1 + 2 * nty * ntz
+    if nty > 1:
+        # y crossing tile 0 -> tile 1: upstream step v+16 (lane (0,0) clock), helper commit of v, downstream step v
+        v = np.arange(4, ns - 20)
+        up, hc, dn = T[0, 2 + v + 16], H[1, 2 + v], T[1, 2 + v]
+        print(f"   y crossing 0->1 (ns): upstream step -> halo commit {np.median(hc - up):.0f}, "
+              f"commit -> downstream step {np.median(dn - hc):.0f}")
+    if ntz > 1:
+        v = np.arange(4, ns - 12)
+        up, hc, dn = T[0, 2 + v + 8], H[nty, 2 + v], T[nty, 2 + v]
+        print(f"   z crossing 0->{nty} (ns): upstream step -> halo commit {np.median(hc - up):.0f}, "
+              f"commit -> downstream step {np.median(dn - hc):.0f}")
     t0 = T[:, 0].min()
     start = (T[:, 0] - t0) / 1e3
     steps = (T[:, 2:] - t0) / 1e3
