@@ -125,11 +125,19 @@ PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, do
                     h->levels[0].A.rows == A.rows)
                        ? h->levels[0].A
                        : A;
-  for (int it = 1; it <= max_iter; ++it) {
+  // A p and the x / r update of iteration it are enqueued before the host waits on the
+  // convergence check of iteration it - 1, so the GPU never idles across that round trip;
+  // once converged they are no-ops (pcg_xr_kernel reads st->done; Ap and pAp are scratch)
+  auto enqueue_ap_xr = [&]() {
     spmv_dot(c, As, p.p, Ap.p, &st.p->pAp);
     pcg_xr_kernel<<<g, 256, 0, c.stream>>>(n, st.p, p.p, Ap.p, x, r.p);
     RDG_LAUNCH_CHECK();
     ++c.launches;
+  };
+  static_assert(sizeof(PcgState) <= 8 * sizeof(double), "PcgState overlaps the pinned scratch");
+  int* herr = reinterpret_cast<int*>(c.h_pinned + 10);
+  enqueue_ap_xr();
+  for (int it = 1; it <= max_iter; ++it) {
     precond(&st.p->rz_next);
     pcg_check_kernel<<<1, 1, 0, c.stream>>>(st.p, tol, hist_dev, max_iter);
     RDG_LAUNCH_CHECK();
@@ -137,9 +145,10 @@ PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, do
     RDG_LAUNCH_CHECK();
     c.launches += 2;
     RDG_CUDA(cudaMemcpyAsync(hs, st.p, sizeof(PcgState), cudaMemcpyDeviceToHost, c.stream));
+    RDG_CUDA(cudaMemcpyAsync(herr, c.d_err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    if (it < max_iter) enqueue_ap_xr();
     RDG_CUDA(cudaStreamSynchronize(c.stream));
-    int derr = 0;
-    RDG_CUDA(cudaMemcpy(&derr, c.d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    const int derr = *herr;
     if (derr) {
       RDG_CUDA(cudaMemset(c.d_err, 0, sizeof(int)));
       throw Error(derr, derr == RD_EZERODIAG ? "sgs_sweep: zero diagonal" : "device error");
