@@ -171,6 +171,18 @@ typedef struct {
 int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, double tol, double* u,
                             rd_solve_outcome* out);
 
+/* The bench-precond row end to end from a host TetMesh (mesh.hpp:13-24 arrays, as for
+ * rd_gpu_mesh_create) in one call: upload, rd::build_system (assembly.cpp:225-238), then
+ * solve_system's AMG branch (bench.cpp:185-225) with u (n_dofs doubles, host or device) read
+ * back.  The host arrays need only live for the call, so for a mesh of Kuhn-lattice size the
+ * tet array uploads on a second stream while the lattice path (which reads no tets) assembles
+ * and solves; the uploaded tets are then checked against the Kuhn enumeration and a mismatch
+ * reruns the work on the generic path.  Same results, errors and timing split as
+ * rd_gpu_build_system + rd_gpu_solve_system_amg.  n_dofs_out may be NULL. */
+int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const int32_t* tets, const uint8_t* bnd,
+                           double rho, const rd_target* target, double tol, double* u, int* n_dofs_out,
+                           rd_solve_outcome* out);
+
 /* replaces rd::l2_error / rd::h1_semi_error (assembly.hpp:59-61, assembly.cpp:265-310) for the
  * manufactured exact solution u = c sin(pi x) sin(pi y) sin(pi z), c = 1/(3 rho pi^2 + 1)
  * (rd::manufactured_exact(rho), target.cpp:45-58): the P1 field with interior coefficients

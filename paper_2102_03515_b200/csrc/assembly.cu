@@ -142,9 +142,8 @@ __global__ void cube_vertices_kernel(int n, double* xyz, uint8_t* bnd) {
   bnd[v] = on_unit_boundary(x, y, z) ? 1 : 0;
 }
 
-__global__ void cube_tets_kernel(int n, int* tets) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)n * n * n * 6) return;
+// tet t of build_structured_cube(n): cell t / 6, chain p = t % 6 (mesh.cpp:46-58)
+__device__ __forceinline__ int4 kuhn_tet(int n, int64_t t) {
   const int nv = n + 1;
   const int p = (int)(t % 6);
   const int64_t cell = t / 6;
@@ -158,7 +157,13 @@ __global__ void cube_tets_kernel(int n, int* tets) {
   out.z = (c[2] * nv + c[1]) * nv + c[0];
   c[perms[p][2]] += 1;
   out.w = (c[2] * nv + c[1]) * nv + c[0];
-  reinterpret_cast<int4*>(tets)[t] = out;
+  return out;
+}
+
+__global__ void cube_tets_kernel(int n, int* tets) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * n * n * 6) return;
+  reinterpret_cast<int4*>(tets)[t] = kuhn_tet(n, t);
 }
 
 // ---------------------------------------------------------------- dof map, adjacency
@@ -885,7 +890,8 @@ __global__ void load_tet_kernel(int nt, const int* __restrict__ tets, const doub
                                 const double* __restrict__ nodal, int n, double* tacc, double* tvol) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nt) return;
-  const int4 t4 = reinterpret_cast<const int4*>(tets)[t];
+  // tets == null: a Kuhn-lattice mesh, its tets by formula (the same ids the check compared)
+  const int4 t4 = tets ? reinterpret_cast<const int4*>(tets)[t] : kuhn_tet(n, t);
   const int tv[4] = {t4.x, t4.y, t4.z, t4.w};
   double V[4][3];
 #pragma unroll
@@ -1141,6 +1147,19 @@ int read_flag(Ctx& c, const int* d) {
 
 }  // namespace
 
+int cube_lattice_candidate(int nv, int nt) {
+  if (nt < 6 || nt % 6) return -1;
+  const int n = (int)std::llround(std::cbrt((double)(nt / 6)));
+  if ((int64_t)6 * n * n * n != nt || (int64_t)(n + 1) * (n + 1) * (n + 1) != nv) return -1;
+  return n;
+}
+
+void launch_lattice_tets_check(Ctx& c, cudaStream_t st, int n, const int* tets, int nt, int* bad) {
+  lattice_tets_check_kernel<<<div_up(nt, 256), 256, 0, st>>>(n, tets, bad);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+}
+
 void detect_cube_lattice(Ctx& c, DMesh& m) {
   m.lattice_n = -1;
   if (m.nt < 6 || m.nt % 6) return;
@@ -1255,6 +1274,8 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
   }
   // ---- vertex -> tet CSR, ascending tets (assembly.cpp:14-31)
   DBuf<int> vto, vt;
+  // a mesh whose tets are still uploading on another stream (rd_gpu_solve_host_mesh)
+  if (!lattice && m.tets_ready) RDG_CUDA(cudaStreamWaitEvent(c.stream, m.tets_ready, 0));
   if (!lattice) {
     DBuf<int> vcnt(nv + 1, c.stream);
     if ((int64_t)nt * 4 > 0x7fffffffLL)
@@ -1336,12 +1357,11 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
     }
     DBuf<double> tacc((size_t)nt * 4, c.stream), tvol(nt, c.stream);
     const bool disc = kind == RD_TARGET_BOX || kind == RD_TARGET_BALL;  // Smoothness::discontinuous
+    const int* tp = lattice ? nullptr : m.tets.p;  // the lattice path reads no tets
     if (disc)
-      load_tet_kernel<64><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, kind, nodal.p, n, tacc.p,
-                                                                 tvol.p);
+      load_tet_kernel<64><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, tp, m.xyz.p, kind, nodal.p, n, tacc.p, tvol.p);
     else
-      load_tet_kernel<14><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, kind, nodal.p, n, tacc.p,
-                                                                 tvol.p);
+      load_tet_kernel<14><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, tp, m.xyz.p, kind, nodal.p, n, tacc.p, tvol.p);
     RDG_LAUNCH_CHECK();
     if (lattice)
       lat_load_gather_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, n, s.d2v.p, tacc.p, tvol.p, s.f.p);

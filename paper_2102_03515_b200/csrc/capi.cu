@@ -549,6 +549,106 @@ int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, doubl
   });
 }
 
+int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const int32_t* tets, const uint8_t* bnd,
+                           double rho, const rd_target* target, double tol, double* u, int* n_dofs_out,
+                           rd_solve_outcome* out) {
+  return guard(ctx, [&] {
+    require(nv >= 0 && nt >= 0, "rd_gpu_solve_host_mesh: negative size");
+    require(target && out && (nv == 0 || (xyz && bnd)) && (nt == 0 || tets), "rd_gpu_solve_host_mesh: null argument");
+    Ctx& c = ctx->c;
+    *out = rd_solve_outcome{0, 0, 0.0, 0.0};
+    DMesh m;
+    m.nv = nv;
+    m.nt = nt;
+    m.lattice_n = -1;
+    m.xyz.alloc((size_t)nv * 3, c.stream);
+    m.tets.alloc((size_t)nt * 4, c.stream);
+    m.boundary.alloc(nv, c.stream);
+    if (nv) RDG_CUDA(cudaMemcpyAsync(m.xyz.p, xyz, sizeof(double) * 3 * nv, cudaMemcpyDefault, c.stream));
+    if (nv) RDG_CUDA(cudaMemcpyAsync(m.boundary.p, bnd, nv, cudaMemcpyDefault, c.stream));
+    // A mesh of Kuhn-lattice size is assembled and solved by the lattice path (which reads
+    // no tets) while its tets upload on a second stream and are checked against the Kuhn
+    // enumeration there; the check gates the result.  The host arrays live for this call.
+    const int cand = cube_lattice_candidate(nv, nt);
+    cudaStream_t up = nullptr;
+    cudaEvent_t ev_alloc = nullptr, ev_done = nullptr;
+    DBuf<int> bad(1, c.stream);
+    RDG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
+    bool pending = false;
+    if (cand > 0 && nt > 0) {
+      RDG_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+      RDG_CUDA(cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming));
+      RDG_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+      RDG_CUDA(cudaEventRecord(ev_alloc, c.stream));  // the allocations and the flag reset
+      RDG_CUDA(cudaStreamWaitEvent(up, ev_alloc, 0));
+      RDG_CUDA(cudaMemcpyAsync(m.tets.p, tets, sizeof(int) * 4 * (size_t)nt, cudaMemcpyDefault, up));
+      launch_lattice_tets_check(c, up, cand, m.tets.p, nt, bad.p);
+      RDG_CUDA(cudaEventRecord(ev_done, up));
+      m.lattice_n = cand;  // provisional until ev_done
+      m.tets_ready = ev_done;
+      pending = true;
+    } else {
+      if (nt) RDG_CUDA(cudaMemcpyAsync(m.tets.p, tets, sizeof(int) * 4 * (size_t)nt, cudaMemcpyDefault, c.stream));
+      detect_cube_lattice(c, m);
+    }
+    // the upload stream's work is done (and checked) before anything here is freed
+    int verdict = pending ? -1 : 1;  // -1: the tets check has not been read yet
+    auto resolve = [&]() -> bool {   // true: the provisional lattice path stands
+      if (verdict < 0) {
+        int hb = 1;
+        if (cudaEventSynchronize(ev_done) == cudaSuccess)
+          cudaMemcpy(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost);
+        cudaEventDestroy(ev_alloc);
+        cudaEventDestroy(ev_done);
+        cudaStreamDestroy(up);
+        m.tets_ready = nullptr;
+        verdict = hb ? 0 : 1;
+        if (hb) m.lattice_n = -1;
+      }
+      return verdict == 1;
+    };
+    auto run = [&](bool final) {
+      using clk = std::chrono::steady_clock;
+      DSystem sys;
+      build_system(c, m, rho, target->kind, target->seed, sys);
+      const DCsr& A = sys.A;
+      const int n = A.rows;
+      if (n_dofs_out) *n_dofs_out = n;
+      *out = rd_solve_outcome{0, 0, 0.0, 0.0};
+      if (n == 0) {  // bench.cpp:187-191
+        out->converged = 1;
+        return;
+      }
+      OutVec<double> uo(c, u, n);
+      RDG_CUDA(cudaStreamSynchronize(c.stream));
+      const auto t0 = clk::now();
+      Hierarchy h;
+      build_hierarchy(c, A, 64, 1, h, /*borrow=*/true);
+      RDG_CUDA(cudaStreamSynchronize(c.stream));
+      const auto t1 = clk::now();
+      PcgResultDev r;
+      exact_retry(c, [&] {
+        r = pcg_device(c, A, &h, sys.f.p, tol, 500, uo.dev(), nullptr);
+        RDG_CUDA(cudaStreamSynchronize(c.stream));
+        sync_and_raise(c);
+      });
+      const auto t2 = clk::now();
+      if (final || resolve()) uo.finish();  // a mismatch reruns below; u is written by that run
+      sync_and_raise(c);
+      out->iterations = r.iterations;
+      out->converged = r.converged ? 1 : 0;
+      out->setup_seconds = std::chrono::duration<double>(t1 - t0).count();
+      out->solve_seconds = std::chrono::duration<double>(t2 - t1).count();
+    };
+    try {
+      run(false);
+    } catch (...) {
+      if (resolve()) throw;  // an error of the provisional path stands only for lattice tets
+    }
+    if (!resolve()) run(true);  // the generic path (lattice_n = -1), tets already on the device
+  });
+}
+
 int rd_gpu_error_norms(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs, double rho,
                        double* l2, double* h1) {
   return guard(ctx, [&] {

@@ -166,6 +166,9 @@ PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, do
 // ---------------------------------------------------------------- assembly.cu
 struct DMesh {
   int nv = 0, nt = 0, lattice_n = -1;
+  // set while the tets upload on another stream (rd_gpu_solve_host_mesh): the generic
+  // assembly path waits on it before reading tets; the lattice path reads none
+  cudaEvent_t tets_ready = nullptr;
   DBuf<double> xyz;
   DBuf<int> tets;
   DBuf<uint8_t> boundary;
@@ -183,6 +186,10 @@ struct DSystem {
 void build_structured_cube(Ctx& c, int n, DMesh& m);
 // sets m.lattice_n when the tets are exactly the build_structured_cube enumeration
 void detect_cube_lattice(Ctx& c, DMesh& m);
+// n when (nv, nt) are the sizes of build_structured_cube(n), else -1 (no check of the tets)
+int cube_lattice_candidate(int nv, int nt);
+// bad[0] = 1 unless tets[0, nt) is the Kuhn enumeration of build_structured_cube(n); on stream st
+void launch_lattice_tets_check(Ctx& c, cudaStream_t st, int n, const int* tets, int nt, int* bad);
 void build_system(Ctx& c, const DMesh& m, double rho, int target_kind, uint64_t seed, DSystem& s);
 // l2 / h1-semi error of the P1 field `coeffs` (device, n_dofs) vs the manufactured exact solution
 void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, double rho, double* l2, double* h1);

@@ -159,7 +159,7 @@ struct SpmvSmem {
   double red[kSpmvWarps];
 };
 
-template <int MODE, bool ASYNC = true>
+template <int MODE>
 __global__ void __launch_bounds__(kSpmvNT) spmv_staged_kernel(int rows, const int* __restrict__ rp,
                                                               const int* __restrict__ ci,
                                                               const double* __restrict__ val,
@@ -189,22 +189,17 @@ __global__ void __launch_bounds__(kSpmvNT) spmv_staged_kernel(int rows, const in
       const int4* gi = reinterpret_cast<const int4*>(ci + ia);
       double2* sv = reinterpret_cast<double2*>(sm.v[warp]);
       int4* si = reinterpret_cast<int4*>(sm.ci[warp]);
-      if (ASYNC) {
-        // every 16-byte piece of the block in flight at once (cp.async), then one wait:
-        // a load -> shared store per iteration would serialise the DRAM round trips
-        for (int t = lane; t < nv2; t += 32)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(sv + t)),
-                       "l"(gv + t)
-                       : "memory");
-        for (int t = lane; t < ni4; t += 32)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(si + t)),
-                       "l"(gi + t)
-                       : "memory");
-        asm volatile("cp.async.wait_all;" ::: "memory");
-      } else {
-        for (int t = lane; t < nv2; t += 32) sv[t] = __ldg(gv + t);
-        for (int t = lane; t < ni4; t += 32) si[t] = __ldg(gi + t);
-      }
+      // every 16-byte piece of the block in flight at once (cp.async), then one wait:
+      // a load -> shared store per iteration would serialise the DRAM round trips
+      for (int t = lane; t < nv2; t += 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(sv + t)),
+                     "l"(gv + t)
+                     : "memory");
+      for (int t = lane; t < ni4; t += 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(si + t)),
+                     "l"(gi + t)
+                     : "memory");
+      asm volatile("cp.async.wait_all;" ::: "memory");
       __syncwarp();
       const int kb = max(rs, cb), ke = min(re, ce);
 #if RD_SPMV_BATCH
@@ -292,27 +287,23 @@ void launch_spmv(Ctx& c, const DCsr& A, const double* x, double* y, const double
     return;
   }
   const int nb = div_up(A.rows, kSpmvNT);
-  // A/B timing only: staging through registers instead of cp.async
-  static const bool syncstage = getenv("RD_SPMV_SYNCSTAGE") && atoi(getenv("RD_SPMV_SYNCSTAGE")) != 0;
   static bool attr = false;
   const size_t smem = sizeof(SpmvSmem);
   if (!attr) {
-    for (auto* k : {spmv_staged_kernel<kPlain, true>, spmv_staged_kernel<kDot, true>, spmv_staged_kernel<kResidual, true>,
-                    spmv_staged_kernel<kPlain, false>, spmv_staged_kernel<kDot, false>,
-                    spmv_staged_kernel<kResidual, false>})
+    for (auto* k : {spmv_staged_kernel<kPlain>, spmv_staged_kernel<kDot>, spmv_staged_kernel<kResidual>})
       RDG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   if (MODE == kDot && nb > Ctx::kMaxPartials) {
     // too many blocks for one partials array: plain SpMV then a separate dot
-    (syncstage ? spmv_staged_kernel<kPlain, false> : spmv_staged_kernel<kPlain, true>)<<<nb, kSpmvNT, smem, c.stream>>>(A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, nullptr,
+    spmv_staged_kernel<kPlain><<<nb, kSpmvNT, smem, c.stream>>>(A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, nullptr,
                                                                nullptr, nullptr);
     RDG_LAUNCH_CHECK();
     ++c.launches;
     dot(c, A.rows, x, y, dot_out);
     return;
   }
-  (syncstage ? spmv_staged_kernel<MODE, false> : spmv_staged_kernel<MODE, true>)<<<nb, kSpmvNT, smem, c.stream>>>(A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, c.d_partials,
+  spmv_staged_kernel<MODE><<<nb, kSpmvNT, smem, c.stream>>>(A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, c.d_partials,
                                                            c.d_counter, dot_out);
   RDG_LAUNCH_CHECK();
   ++c.launches;

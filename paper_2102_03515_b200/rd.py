@@ -128,6 +128,7 @@ def lib():
         "rd_gpu_amg_level_sweep": (_I, [_P, _I, _I, _P, _P, _P]),
         "rd_gpu_pcg": (_I, [_P, _P, _P, _P, _D, _I, _P, _P, _P]),
         "rd_gpu_solve_system_amg": (_I, [_P, _P, _P, _D, _P, _P]),
+        "rd_gpu_solve_host_mesh": (_I, [_P, _I, _P, _I, _P, _P, _D, _P, _D, _P, _P, _P]),
         "rd_gpu_error_norms": (_I, [_P, _P, _P, _P, _D, C.POINTER(_D), C.POINTER(_D)]),
         "rd_gpu_l2_error_target_squared": (_I, [_P, _P, _P, _P, _P, C.POINTER(_D)]),
         "rd_gpu_target_dual_norm": (_I, [_P, _P, _P, C.POINTER(_D)]),
@@ -594,6 +595,27 @@ class SolveOutcome:
     converged: bool
     setup_seconds: float
     solve_seconds: float
+
+
+def solve_host_mesh(xyz, tets, boundary, rho: float, target: str = "smooth", tol: float = 1e-8, u=None,
+                    seed: int = 0, ctx: Context | None = None) -> SolveOutcome:
+    """mesh upload + build_system + solve_system(..., PrecondKind::amg) in one call
+    (rd_gpu_solve_host_mesh: the tets upload overlaps the lattice-path solve).  `u`: an
+    output array or device pointer of n_dofs doubles; None allocates a host array."""
+    ctx = ctx or default_context()
+    xyz = np.ascontiguousarray(xyz, np.float64)
+    tets = np.ascontiguousarray(tets, np.int32)
+    boundary = np.ascontiguousarray(boundary, np.uint8)
+    host = u is None
+    if host:
+        u = np.zeros(max(int((boundary == 0).sum()), 1))
+    t = _Target(TARGETS[target], int(seed))
+    out = _SolveOutcome()
+    nd = C.c_int(0)
+    ctx.check(lib().rd_gpu_solve_host_mesh(ctx.h, xyz.shape[0], _ptr(xyz), tets.shape[0], _ptr(tets), _ptr(boundary),
+                                           float(rho), C.byref(t), float(tol), _ptr(u), C.byref(nd), C.byref(out)))
+    return SolveOutcome(u[: nd.value] if host else u, out.iterations, bool(out.converged), out.setup_seconds,
+                        out.solve_seconds)
 
 
 def solve_system_amg(A: Csr, f, tol: float = 1e-8, u=None) -> SolveOutcome:

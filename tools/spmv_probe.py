@@ -1,6 +1,6 @@
 """CSR SpMV timing probe (C2 level-0 A and the level-0 restriction Pt) through the C-ABI
 with CUDA events on the library stream.  RD_NO_STENCIL_SPMV=1 forces the CSR kernel on A;
-RD_SPMV_SYNCSTAGE=1 stages through registers (A/B)."""
+the staged kernel is the cp.async one."""
 import json
 import os
 import sys
