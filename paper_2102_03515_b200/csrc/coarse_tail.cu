@@ -87,30 +87,56 @@ __device__ void tail_sweep(const TailLev& lv, int fo, int xo, int tbo, int* err)
   const int yo = FWD ? y : L - 1 - y, zo = FWD ? z : L - 1 - z;
   const int base = (zo * L + yo) * L, pbase = padi(0, yo, zo, L);
   const int cyz = pos_class(yo, L) * 4 + pos_class(zo, L);
-  const int off[15] = {-1 - Q - QQ, -Q - QQ, -1 - QQ, -QQ, -1 - Q, -Q, -1, 0, 1, Q, 1 + Q, QQ, 1 + QQ, Q + QQ, 1 + Q + QQ};
+  // Neighbour values by sweep-direction offset (the 15-point set is centrally symmetric,
+  // so both directions see the same offsets): per step 7 loads -- the three fresh rows of
+  // the y-1 / z-1 / yz-1 lines, the old a+1 rows of this and the +y / +z / +yz lines --
+  // and the rest from the previous step's registers (row a-1 fresh, row a old).  The
+  // thread runs the loads from row -1 (padding), so the first row starts from them.
+  const int sg = FWD ? 1 : -1;
+  const int oXp = sg, oY0 = -sg * Q, oZ0 = -sg * QQ, oD0 = -sg * (Q + QQ);
+  const int oYp = sg * (1 + Q), oZp = sg * (1 + QQ), oYZp = sg * (1 + Q + QQ);
+  double X1 = 0.0, Y1 = 0.0, Z1 = 0.0, D1 = 0.0;  // row a-1 of this / y-1 / z-1 / yz-1 lines (fresh)
+  double Yp0 = 0.0, Zp0 = 0.0, YZp0 = 0.0;         // row a of the +y / +z / +yz lines (old)
   const int steps = 3 * (L - 1) + 1;
-  for (int s = 0; s < steps; ++s) {
+  for (int s = -1; s < steps; ++s) {
     const int a = s - y - z;
-    if (has && a >= 0 && a < L) {
+    if (has && a >= -1 && a < L) {
       const int ao = FWD ? a : L - 1 - a;
       const int ip = pbase + ao;
-      const double2* row = reinterpret_cast<const double2*>(tb + (pos_class(ao, L) * 16 + cyz) * 16);
-      double v[16];
+      const double Xp = x[ip + oXp], Y0 = x[ip + oY0], Z0 = x[ip + oZ0], D0 = x[ip + oD0];
+      const double Yp1 = x[ip + oYp], Zp1 = x[ip + oZp], YZp1 = x[ip + oYZp];
+      double xn = 0.0;
+      if (a >= 0) {
+        const double2* row = reinterpret_cast<const double2*>(tb + (pos_class(ao, L) * 16 + cyz) * 16);
+        double v[16];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double2 t = row[k];
-        v[2 * k] = t.x;
-        v[2 * k + 1] = t.y;
+        for (int k = 0; k < 8; ++k) {
+          const double2 t = row[k];
+          v[2 * k] = t.x;
+          v[2 * k + 1] = t.y;
+        }
+        // ascending original column order: the sweep-offset slots in the reference's order
+        const double nf[15] = {D1, D0, Z1, Z0, Y1, Y0, X1, 0.0, Xp, Yp0, Yp1, Zp0, Zp1, YZp0, YZp1};
+        const double nr[15] = {YZp1, YZp0, Zp1, Zp0, Yp1, Yp0, Xp, 0.0, X1, Y0, Y1, Z0, Z1, D0, D1};
+        const double(&nb)[15] = FWD ? nf : nr;
+        double sum = f[base + ao];
+#pragma unroll
+        for (int k = 0; k < 15; ++k)
+          if (k != 7) sum = __dsub_rn(sum, __dmul_rn(v[k], nb[k]));
+        const double d = v[7];
+        if (d == 0.0) atomicCAS(err, 0, RD_EZERODIAG);
+        double q = div_fast(sum, d, v[15]);
+        if (!(sum == 0.0 || div_is_fast(sum, d, q))) q = div_exact(sum, d);
+        xn = sum == 0.0 ? __dmul_rn(sum, v[15]) : q;
+        x[ip] = xn;
       }
-      double sum = f[base + ao];
-#pragma unroll
-      for (int k = 0; k < 15; ++k)
-        if (k != 7) sum = __dsub_rn(sum, __dmul_rn(v[k], x[ip + off[k]]));
-      const double d = v[7];
-      if (d == 0.0) atomicCAS(err, 0, RD_EZERODIAG);
-      double q = div_fast(sum, d, v[15]);
-      if (!(sum == 0.0 || div_is_fast(sum, d, q))) q = div_exact(sum, d);
-      x[ip] = sum == 0.0 ? __dmul_rn(sum, v[15]) : q;
+      X1 = xn;  // row -1: the padding's +0
+      Y1 = Y0;
+      Z1 = Z0;
+      D1 = D0;
+      Yp0 = Yp1;
+      Zp0 = Zp1;
+      YZp0 = YZp1;
     }
     __syncthreads();
   }
