@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extra", action="store_true", help="skip the C4 / C5 single-GPU runs")
     p.add_argument("--profile", action="store_true", help="short run for ncu: 1 step, no extras")
-    p.add_argument("--mode", default="pipelined", choices=["pipelined", "exact", "block"],
+    p.add_argument("--mode", default="exact", choices=["pipelined", "exact", "block"],
                    help="N > 1: smoother hand-off between slabs: pipelined = the sweep kernels write the "
                         "boundary cells into the next GPU's memory (NVLink, CUDA IPC); exact = planes handed on "
                         "over NCCL between sweeps (both the single-GPU sweep bit for bit); block = concurrent "
@@ -127,8 +127,8 @@ class ClockSampler:
 
 def job_rate(elapsed_ms, work, world, device=None):
     """Whole-job throughput: the slowest rank's device time (MAX) over all ranks' work (SUM).
-    Ranks are independent replicas (the exact lexicographic GS does not
-    shard), so there is no data-path collective -- only this timing reduction."""
+    Used by the --replicas mode (independent solves per rank, no data-path collective);
+    the default N > 1 path is the slab-distributed solve of run_dist."""
     import torch
 
     t = torch.tensor([float(elapsed_ms)], dtype=torch.float64, device=device)
@@ -475,16 +475,16 @@ def run_ours(args, rank, world, local_rank):
             e2e_step()
         barrier()
         torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        if os.environ.get("RD_BENCH_VERBOSE"):
+        if os.environ.get("RD_BENCH_VERBOSE"):  # host-timed probe steps, outside the timed window
             for _ in range(2):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 e2e_step()
                 torch.cuda.synchronize()
                 print(f"e2e step {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr, flush=True)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
         e2e_its = [e2e_step() for _ in range(args.steps)]
         b.record(stream)
         torch.cuda.synchronize()

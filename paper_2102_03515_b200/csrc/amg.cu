@@ -758,13 +758,13 @@ void lattice_level(Ctx& c, Level& lv, DCsr& Ac, int* notlat_dev, bool direct) {
 }  // namespace
 
 namespace {
-// RD_SETUP_TRACE=1: synchronise after each setup phase and print its host time
-// (diagnostic only; the syncs it adds are not in the product path)
+// RD_PROBES builds (compile-time, diagnostics only): synchronise after each setup
+// phase and print its host time; compiled out of the shipped library
 struct SetupTrace {
   Ctx& c;
   bool on;
   std::chrono::steady_clock::time_point t0;
-  explicit SetupTrace(Ctx& cc) : c(cc), on(getenv("RD_SETUP_TRACE") && atoi(getenv("RD_SETUP_TRACE")) != 0) {
+  explicit SetupTrace(Ctx& cc) : c(cc), on(RD_PROBES != 0) {
     if (on) {
       cudaStreamSynchronize(c.stream);
       t0 = std::chrono::steady_clock::now();
@@ -873,7 +873,7 @@ bool build_levels(Ctx& c, const DCsr& A, int threshold, int m, Hierarchy& h, boo
   for (size_t l = 0; l < h.levels.size(); ++l)
     if (uni[2 * l] >= 0) lattice_resolve(c, h.levels[l].A, &uni[2 * l]);  // packs only where needed
   if (tail_bad_h) h.tail_level = -1;
-  if (getenv("RD_TAIL_CLOCKS"))
+  if (RD_PROBES)
     fprintf(stderr, "coarse tail: level %d (class check %s)\n", h.tail_level, tail_bad_h ? "failed" : "ok");
   return true;
 }

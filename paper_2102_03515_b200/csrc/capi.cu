@@ -6,10 +6,31 @@
 #include <cstdlib>
 #include <chrono>
 #include <cstring>
+#include <mutex>
 
 #include "internal.hpp"
 
 using namespace rdg;
+
+namespace rdg {
+cudaMemPool_t library_pool(int device) {
+  static std::mutex mu;
+  static std::vector<cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lock(mu);
+  if (device < 0) throw Error(RD_EINVAL, "bad device");
+  if ((size_t)device >= pools.size()) pools.resize(device + 1, nullptr);
+  if (!pools[device]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    RDG_CUDA(cudaMemPoolCreate(&pools[device], &props));
+    uint64_t thr = UINT64_MAX;  // the library's own pool keeps its memory between calls
+    RDG_CUDA(cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  return pools[device];
+}
+}  // namespace rdg
 
 namespace {
 
@@ -18,6 +39,7 @@ thread_local std::string g_noctx_err;
 template <class F>
 int guard(rd_ctx* ctx, F&& fn) {
   try {
+    PoolScope ps(ctx ? ctx->c.pool : current_pool());
     fn();
     return RD_OK;
   } catch (const Error& e) {
@@ -132,11 +154,8 @@ int rd_gpu_ctx_create(int device, void* stream, rd_ctx** out) {
     } else {
       RDG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     }
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
+    c.pool = library_pool(device);
+    PoolScope ps(c.pool);
     RDG_CUDA(cudaMalloc(&c.d_err, sizeof(int)));
     RDG_CUDA(cudaMalloc(&c.d_counter, 64 * sizeof(unsigned)));
     RDG_CUDA(cudaMalloc(&c.d_partials, Ctx::kMaxPartials * sizeof(double)));
@@ -473,13 +492,10 @@ int rd_gpu_amg_level_sweep(rd_amg* h, int level, int forward, const double* f, c
     require(level >= 0 && level < (int)h->h.levels.size(), "amg_level_sweep: bad level");
     require(is_device_ptr(f) && is_device_ptr(xout) && (!xin || is_device_ptr(xin)),
             "amg_level_sweep: device pointers required");
-    // asynchronous (no sync to check a speculation): exact sweeps.  RD_GS_LEVEL_SPEC=1
-    // (timing probes only) runs the V-cycle's speculative kernel and leaves any
-    // speculation flag unchecked.
+    // asynchronous (no sync to check a speculation): exact sweeps
     Ctx& c = h->ctx->c;
     const bool was = c.gs_exact;
-    static const bool spec = getenv("RD_GS_LEVEL_SPEC") && atoi(getenv("RD_GS_LEVEL_SPEC")) != 0;
-    c.gs_exact = !spec;
+    c.gs_exact = true;
     gs_pass(c, h->h.levels[level].A, f, xin, xout, forward != 0);
     c.gs_exact = was;
   });
@@ -570,22 +586,36 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
     // no tets) while its tets upload on a second stream and are checked against the Kuhn
     // enumeration there; the check gates the result.  The host arrays live for this call.
     const int cand = cube_lattice_candidate(nv, nt);
-    cudaStream_t up = nullptr;
-    cudaEvent_t ev_alloc = nullptr, ev_done = nullptr;
     DBuf<int> bad(1, c.stream);
     RDG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
+    // the upload stream and its events; declared after the buffers it writes, so on any
+    // exit (including a throw before the work below is resolved) the upload is waited
+    // for before m.tets and bad are freed
+    struct Upload {
+      cudaStream_t s = nullptr;
+      cudaEvent_t alloc = nullptr, done = nullptr;
+      void close() {
+        if (s) cudaStreamSynchronize(s);
+        if (alloc) cudaEventDestroy(alloc);
+        if (done) cudaEventDestroy(done);
+        if (s) cudaStreamDestroy(s);
+        s = nullptr;
+        alloc = done = nullptr;
+      }
+      ~Upload() { close(); }
+    } upl;
     bool pending = false;
     if (cand > 0 && nt > 0) {
-      RDG_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
-      RDG_CUDA(cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming));
-      RDG_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
-      RDG_CUDA(cudaEventRecord(ev_alloc, c.stream));  // the allocations and the flag reset
-      RDG_CUDA(cudaStreamWaitEvent(up, ev_alloc, 0));
-      RDG_CUDA(cudaMemcpyAsync(m.tets.p, tets, sizeof(int) * 4 * (size_t)nt, cudaMemcpyDefault, up));
-      launch_lattice_tets_check(c, up, cand, m.tets.p, nt, bad.p);
-      RDG_CUDA(cudaEventRecord(ev_done, up));
-      m.lattice_n = cand;  // provisional until ev_done
-      m.tets_ready = ev_done;
+      RDG_CUDA(cudaStreamCreateWithFlags(&upl.s, cudaStreamNonBlocking));
+      RDG_CUDA(cudaEventCreateWithFlags(&upl.alloc, cudaEventDisableTiming));
+      RDG_CUDA(cudaEventCreateWithFlags(&upl.done, cudaEventDisableTiming));
+      RDG_CUDA(cudaEventRecord(upl.alloc, c.stream));  // the allocations and the flag reset
+      RDG_CUDA(cudaStreamWaitEvent(upl.s, upl.alloc, 0));
+      RDG_CUDA(cudaMemcpyAsync(m.tets.p, tets, sizeof(int) * 4 * (size_t)nt, cudaMemcpyDefault, upl.s));
+      launch_lattice_tets_check(c, upl.s, cand, m.tets.p, nt, bad.p);
+      RDG_CUDA(cudaEventRecord(upl.done, upl.s));
+      m.lattice_n = cand;  // provisional until upl.done
+      m.tets_ready = upl.done;
       pending = true;
     } else {
       if (nt) RDG_CUDA(cudaMemcpyAsync(m.tets.p, tets, sizeof(int) * 4 * (size_t)nt, cudaMemcpyDefault, c.stream));
@@ -596,12 +626,10 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
     auto resolve = [&]() -> bool {   // true: the provisional lattice path stands
       if (verdict < 0) {
         int hb = 1;
-        if (cudaEventSynchronize(ev_done) == cudaSuccess)
+        if (cudaEventSynchronize(upl.done) == cudaSuccess)
           cudaMemcpy(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost);
-        cudaEventDestroy(ev_alloc);
-        cudaEventDestroy(ev_done);
-        cudaStreamDestroy(up);
         m.tets_ready = nullptr;
+        upl.close();
         verdict = hb ? 0 : 1;
         if (hb) m.lattice_n = -1;
       }

@@ -47,7 +47,7 @@ struct TailParams {
   double* z;
   int* err;
   int m;  // smoothing steps
-  long long* clk;  // RD_TAIL_CLOCKS probes only: phase timestamps of thread 0
+  long long* clk;  // RD_PROBES builds only: phase timestamps of thread 0 (else null)
 };
 
 __device__ __forceinline__ unsigned tail_mask(int a, int y, int z, int L) {
@@ -448,18 +448,19 @@ void coarse_tail(Ctx& c, Hierarchy& h, int c0, const double* r, double* z) {
   p.z = z;
   p.err = c.d_err;
   p.m = h.smoothing_steps;
-  static const bool probe = getenv("RD_TAIL_CLOCKS") != nullptr;
-  DBuf<long long> clk;
-  if (probe) {
-    clk.alloc(64, c.stream);
-    RDG_CUDA(cudaMemsetAsync(clk.p, 0, 64 * sizeof(long long), c.stream));
-    p.clk = clk.p;
-  }
+#if RD_PROBES  // compile-time diagnostic builds only: phase clocks of the tail kernel
+  DBuf<long long> clk(64, c.stream);
+  RDG_CUDA(cudaMemsetAsync(clk.p, 0, 64 * sizeof(long long), c.stream));
+  p.clk = clk.p;
+#else
+  p.clk = nullptr;
+#endif
 
   coarse_tail_kernel<<<1, kTailNT, tail_smem(h, c0), c.stream>>>(p);
   RDG_LAUNCH_CHECK();
   ++c.launches;
-  if (probe) {
+#if RD_PROBES
+  {
     long long hc[64];
     RDG_CUDA(cudaMemcpyAsync(hc, clk.p, sizeof(hc), cudaMemcpyDeviceToHost, c.stream));
     RDG_CUDA(cudaStreamSynchronize(c.stream));
@@ -467,6 +468,7 @@ void coarse_tail(Ctx& c, Hierarchy& h, int c0, const double* r, double* z) {
     for (int k = 1; k < 64 && hc[k]; ++k) fprintf(stderr, " %lld", hc[k] - hc[k - 1]);
     fprintf(stderr, "\n");
   }
+#endif
 }
 
 }  // namespace rdg

@@ -64,6 +64,7 @@ int vgrid(Ctx& c, int64_t n) {
 template <class F>
 int guard(rd_ctx* ctx, F&& fn) {
   try {
+    PoolScope ps(ctx->c.pool);
     fn();
     return RD_OK;
   } catch (const Error& e) {

@@ -136,7 +136,7 @@ PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, do
   };
   static_assert(sizeof(PcgState) <= 8 * sizeof(double), "PcgState overlaps the pinned scratch");
   int* herr = reinterpret_cast<int*>(c.h_pinned + 10);
-  enqueue_ap_xr();
+  if (max_iter >= 1) enqueue_ap_xr();  // max_iter <= 0: x stays 0 (linalg.cpp:66,77)
   for (int it = 1; it <= max_iter; ++it) {
     precond(&st.p->rz_next);
     pcg_check_kernel<<<1, 1, 0, c.stream>>>(st.p, tol, hist_dev, max_iter);

@@ -125,20 +125,31 @@ class TorchComm:
         return out.tolist()
 
     def link_slabs(self, ops, G):
-        """Map the neighbours' slab cell buffers (CUDA IPC over NVLink) for the pipelined hand-off."""
+        """Map the neighbours' slab cell buffers (CUDA IPC over NVLink) for the pipelined hand-off.
+
+        Every rank runs every level's collective whatever fails locally (an export or a
+        peer mapping), and the outcome is reduced once at the end, so a failure on some
+        ranks can never leave the others waiting in a different collective."""
+        ok = True
         for l in range(G):
-            try:  # every rank reaches the collective, even when its own export fails
+            try:
                 mine = (ops.ipc_handle(l), ops.slab_g0(l))
             except Exception:  # noqa: BLE001
                 mine = None
             allh = [None] * self.world
             self.dist.all_gather_object(allh, mine, group=self.group)
-            if any(h is None for h in allh):
-                raise RuntimeError("slab cell buffers could not be exported for CUDA IPC")
-            if self.rank + 1 < self.world:
-                ops.open_peer(l, 0, *allh[self.rank + 1])
-            if self.rank > 0:
-                ops.open_peer(l, 1, *allh[self.rank - 1])
+            if not ok or any(h is None for h in allh):
+                ok = False
+                continue
+            try:
+                if self.rank + 1 < self.world:
+                    ops.open_peer(l, 0, *allh[self.rank + 1])
+                if self.rank > 0:
+                    ops.open_peer(l, 1, *allh[self.rank - 1])
+            except Exception:  # noqa: BLE001
+                ok = False
+        if not all(self.allgather_int(1 if ok else 0)):
+            raise RuntimeError("slab cell buffers could not be mapped for the pipelined hand-off")
 
     def pipelined_sweep(self, ops, l, fwd, f, xin, xout):
         ops.sweep_pipelined(l, fwd, f, xin, xout)
@@ -390,10 +401,14 @@ class DeviceOps:
 
     def check(self) -> int:
         """Device errors of the asynchronous calls so far (0, or RD_GS_SPECULATION_MISS, ...)."""
-        rc = self.rd.lib().rd_gpu_synchronize(self.ctx.h)
+        rc = self.check_raw()
         if rc not in (0, self.rd.RD_GS_SPECULATION_MISS):
             self.ctx.check(rc)
         return rc
+
+    def check_raw(self) -> int:
+        """The status of rd_gpu_synchronize, never raised here (collective callers raise together)."""
+        return int(self.rd.lib().rd_gpu_synchronize(self.ctx.h))
 
 
 class _Slab:
@@ -602,8 +617,14 @@ class DistSolver:
             res = self._pcg(tol, max_iter)
         except NotSpdError as e:  # raised on every rank at once (the scalars are replicated)
             err = e
-        rc = self.ops.check()
-        if any(self.comm.allgather_int(1 if rc else 0)):
+        # the raw device status goes through the collective first, so a device error on
+        # one rank is raised on every rank together instead of stranding the others
+        rcs = self.comm.allgather_int(self.ops.check_raw())
+        miss = 0x5EC  # RD_GS_SPECULATION_MISS (rd.py): rerun with exact sweeps
+        bad = [c for c in rcs if c not in (0, miss)]
+        if bad:
+            raise RuntimeError(f"distributed pcg: device error {bad[0]} on rank {rcs.index(bad[0])}")
+        if any(rcs):
             # a speculative sweep somewhere left the division fast path (possibly behind the
             # error it caused): rerun the whole solve with exact sweeps on every rank
             self.ops.set_exact(True)

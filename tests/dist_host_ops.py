@@ -140,3 +140,6 @@ class HostOps:
 
     def check(self):
         return 0
+
+    def check_raw(self):
+        return 0

@@ -437,6 +437,17 @@ def test_pcg_hand_cases(rd, O):  # test_linalg.cpp:96-139
         rd.pcg(rd.from_triplets(2, 2, [(0, 0, 1.0), (1, 1, -1.0)]), "identity", np.ones(2), 1e-10, 10)
 
 
+@pytest.mark.parametrize("max_iter", [0, -3])
+@pytest.mark.parametrize("precond", ["identity", "amg"])
+def test_pcg_max_iter_nonpositive(rd, O, max_iter, precond):  # linalg.cpp:66,77: the loop never runs
+    ds = rd.build_system(rd.build_structured_cube(8), 1.0, "smooth")
+    os_ = O.build_system(O.build_structured_cube(8), 1.0, "smooth")
+    r = rd.pcg(ds.A, precond, ds.f(), 1e-8, max_iter)
+    ref = O.pcg(os_.A, precond, os_.f, 1e-8, max_iter)
+    assert r.iterations == ref.iterations == 0 and not r.converged and not ref.converged
+    assert np.all(r.x == 0.0) and np.all(ref.x == 0.0)
+
+
 @pytest.mark.parametrize("n,rho,target", [(8, 1.0, "smooth"), (8, 1e-12, "smooth"), (16, 2.0 ** -8, "ball"),
                                           (32, 2.0 ** -10, "smooth"), (32, 1e-2, "sine_random"),
                                           (32, 2.0 ** -10, "box")])
