@@ -199,6 +199,15 @@ int rd_gpu_error_norms(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, c
 int rd_gpu_l2_error_target_squared(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs,
                                    const rd_target* target, double* err2);
 
+/* replaces rd::l2_error(sol, target.evaluator) / rd::h1_semi_error(sol, grad u_bar)  (assembly.hpp:59-61,
+ * assembly.cpp:265-310) with the TARGET field u_bar as the exact function: l2 = ||u_h - u_bar||_L2,
+ * h1 = ||grad(u_h - u_bar)||_L2, degree-5 rule per tet.  grad u_bar: sin^3 as manufactured_exact(0)
+ * (smooth, nonzero_bc, and the sine part of sine+random), the P1 interpolant's gradient on the
+ * Kuhn tet its point location picks (sine+random), (y, x, 2) (quadratic), 0 a.e. (indicators,
+ * constants).  The BASELINE C3 gate ||grad(u_rho,h - u_bar)||.  Either output may be null. */
+int rd_gpu_error_norms_target(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs,
+                              const rd_target* target, double* l2_error, double* h1_semi_error);
+
 /* replaces the rho-coupled table's target_dual_norm(sys, sol)  bench.cpp:55-63 with
  * target_residual (assembly.cpp:354-356) and hminus1_norm[_with] (assembly.cpp:333-352):
  * r = f - M u, w = K^-1 r (dense LLT for n <= 2000, else AMG(K)-PCG to 1e-11), sqrt(r . w).

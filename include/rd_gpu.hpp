@@ -285,4 +285,17 @@ inline ErrorNorms error_norms(const TetMesh& mesh, const FemSystem& sys, const s
   return e;
 }
 
+// the same norms with a target field u_bar as the exact function (value and gradient):
+// ||u_h - u_bar||_L2 and ||grad(u_h - u_bar)||_L2, the BASELINE error gates
+inline ErrorNorms error_norms_target(const TetMesh& mesh, const FemSystem& sys, const std::vector<double>& coeffs,
+                                     Target target, uint64_t seed = 0) {
+  if ((int)coeffs.size() != sys.n_dofs()) throw std::invalid_argument("error_norms_target: coefficient size mismatch");
+  ErrorNorms e;
+  const rd_target t{static_cast<int>(target), seed};
+  check(rd_gpu_error_norms_target(mesh.context().get(), mesh.get(), sys.get(), coeffs.data(), &t, &e.l2,
+                                  &e.h1_semi),
+        mesh.context().get());
+  return e;
+}
+
 }  // namespace rd_gpu

@@ -98,6 +98,8 @@ def lib():
         "or_l2_error_target_squared": (_I, [_P, _P, _pd, _I, _I, C.c_uint64, C.POINTER(_D)]),
         "or_target_dual_norm": (_I, [_P, _pd, C.POINTER(_D)]),
         "or_h1_semi_error_manufactured": (_I, [_P, _P, _pd, _D, C.POINTER(_D)]),
+        "or_error_norms_target": (_I, [_P, _P, _pd, _I, _I, C.c_uint64, C.POINTER(_D), C.POINTER(_D)]),
+        "or_target_grad": (_I, [_I, _I, C.c_uint64, _I, _pd, _pd]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -473,6 +475,23 @@ def l2_error_target_squared(mesh: Mesh, sys: FemSystem, coeffs, target: str, n: 
     _check(lib().or_l2_error_target_squared(mesh._h.h, sys._h.h, np.ascontiguousarray(coeffs, np.float64),
                                             TARGETS[target], int(n), int(seed), C.byref(out)))
     return out.value
+
+
+def error_norms_target(mesh: Mesh, sys: FemSystem, coeffs, target: str, n: int = 0, seed: int = 0):
+    """assembly.cpp:265-310 with the target field as the exact function: (||u_h - u_bar||_L2,
+    ||grad(u_h - u_bar)||_L2), degree-5 rule; grad(u_bar) from Target::grad."""
+    l2, h1 = _D(), _D()
+    _check(lib().or_error_norms_target(mesh._h.h, sys._h.h, np.ascontiguousarray(coeffs, np.float64),
+                                       TARGETS[target], int(n), int(seed), C.byref(l2), C.byref(h1)))
+    return l2.value, h1.value
+
+
+def target_grad(kind: str, xyz, n: int = 0, seed: int = 0) -> np.ndarray:
+    """The exact gradient of a target field at points xyz [npts, 3]."""
+    xyz = np.ascontiguousarray(xyz, np.float64).reshape(-1, 3)
+    out = np.zeros_like(xyz)
+    _check(lib().or_target_grad(TARGETS[kind], int(n), int(seed), xyz.shape[0], xyz, out))
+    return out
 
 
 def target_dual_norm(sys: FemSystem, coeffs) -> float:

@@ -341,6 +341,68 @@ struct Target {
     return val;
   }
 
+  // gradient of the P1 interpolant at x, on the tet the point location of interp() picks:
+  // I_h r = r0 (1 - xi_a) + r1 (xi_a - xi_b) + r2 (xi_b - xi_c) + r3 xi_c with xi = n x - cell
+  // and (a, b, c) the chain, so d/dx_a = n (r1 - r0), d/dx_b = n (r2 - r1), d/dx_c = n (r3 - r2)
+  void interp_grad(const V3& x, double* g) const {
+    const int nv = n + 1;
+    int cell[3];
+    double xi[3];
+    for (int d = 0; d < 3; ++d) {
+      const double s = x.c[d] * static_cast<double>(n);
+      int ci = static_cast<int>(std::floor(s));
+      ci = std::min(std::max(ci, 0), n - 1);
+      cell[d] = ci;
+      xi[d] = s - static_cast<double>(ci);
+    }
+    constexpr int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    int p = 0;
+    for (; p < 5; ++p)
+      if (xi[perms[p][0]] >= xi[perms[p][1]] && xi[perms[p][1]] >= xi[perms[p][2]]) break;
+    const int* pm = perms[p];
+    int c[3] = {cell[0], cell[1], cell[2]};
+    double r[4];
+    r[0] = nodal[static_cast<size_t>((c[2] * nv + c[1]) * nv + c[0])];
+    for (int s = 0; s < 3; ++s) {
+      c[pm[s]] += 1;
+      r[s + 1] = nodal[static_cast<size_t>((c[2] * nv + c[1]) * nv + c[0])];
+    }
+    const double dn = static_cast<double>(n);
+    for (int s = 0; s < 3; ++s) g[pm[s]] = dn * (r[s + 1] - r[s]);
+  }
+
+  // the exact gradient of the target field (h1_semi_error's exact_grad for the error gate
+  // ||grad(u_h - u_bar)||): sin3 as manufactured_exact(0).grad_u (target.cpp:45-58), the
+  // random part piecewise constant (interp_grad), indicators zero almost everywhere
+  void grad(const V3& x, double* g) const {
+    g[0] = g[1] = g[2] = 0.0;
+    switch (kind) {
+      case OR_TARGET_SMOOTH:
+      case OR_TARGET_NONZERO_BC:
+      case OR_TARGET_SINE_RANDOM: {
+        const double sx = std::sin(kPi * x.c[0]), cx = std::cos(kPi * x.c[0]);
+        const double sy = std::sin(kPi * x.c[1]), cy = std::cos(kPi * x.c[1]);
+        const double sz = std::sin(kPi * x.c[2]), cz = std::cos(kPi * x.c[2]);
+        const double cp = 1.0 * kPi;
+        g[0] = cp * cx * sy * sz;
+        g[1] = cp * sx * cy * sz;
+        g[2] = cp * sx * sy * cz;
+        if (kind == OR_TARGET_SINE_RANDOM) {
+          double gr[3];
+          interp_grad(x, gr);
+          for (int d = 0; d < 3; ++d) g[d] = g[d] + 0.1 * gr[d];
+        }
+        return;
+      }
+      case OR_TARGET_QUADRATIC:  // x y + 2 z
+        g[0] = x.c[1];
+        g[1] = x.c[0];
+        g[2] = 2.0;
+        return;
+      default: return;  // box, ball, zero, one
+    }
+  }
+
   double operator()(const V3& x) const {
     switch (kind) {
       case OR_TARGET_SMOOTH: return sin3(x);  // target.cpp:17-23
@@ -1050,8 +1112,17 @@ Exact manufactured_exact(double rho) {
   return Exact{1.0 / (3.0 * rho * kPi * kPi + 1.0)};
 }
 
+// a target field as the exact function of l2_error / h1_semi_error (std::function callbacks
+// in the reference: exact = target.evaluator, exact_grad = its gradient)
+struct TargetExact {
+  const Target& t;
+  double u(const V3& x) const { return t(x); }
+  void grad(const V3& x, double* g) const { t.grad(x, g); }
+};
+
 // assembly.cpp:265-285
-double l2_error(const Mesh& m, const DofMap& dm, const double* coeffs, const Exact& ex) {
+template <class Ex>
+double l2_error(const Mesh& m, const DofMap& dm, const double* coeffs, const Ex& ex) {
   const auto nodal = nodal_field(m, dm, coeffs);
   const Rule& rule = rule_by_id(2);
   const double err2 = parallel_reduce(m.nt(), [&](int64_t b, int64_t e) {
@@ -1076,7 +1147,8 @@ double l2_error(const Mesh& m, const DofMap& dm, const double* coeffs, const Exa
 }
 
 // assembly.cpp:287-310
-double h1_semi_error(const Mesh& m, const DofMap& dm, const double* coeffs, const Exact& ex) {
+template <class Ex>
+double h1_semi_error(const Mesh& m, const DofMap& dm, const double* coeffs, const Ex& ex) {
   const auto nodal = nodal_field(m, dm, coeffs);
   const Rule& rule = rule_by_id(2);
   const double err2 = parallel_reduce(m.nt(), [&](int64_t b, int64_t e) {
@@ -1487,6 +1559,21 @@ int or_l2_error_target_squared(const or_mesh* m, const or_system* s, const doubl
 int or_h1_semi_error_manufactured(const or_mesh* m, const or_system* s, const double* coeffs, double rho,
                                   double* out) {
   return guard([&] { *out = h1_semi_error(m->m, s->s.dm, coeffs, manufactured_exact(rho)); });
+}
+int or_error_norms_target(const or_mesh* m, const or_system* s, const double* coeffs, int kind, int n,
+                          uint64_t seed, double* l2, double* h1) {
+  return guard([&] {
+    const Target t = make_target(kind, n, seed);
+    const TargetExact ex{t};
+    if (l2) *l2 = l2_error(m->m, s->s.dm, coeffs, ex);
+    if (h1) *h1 = h1_semi_error(m->m, s->s.dm, coeffs, ex);
+  });
+}
+int or_target_grad(int kind, int n, uint64_t seed, int npts, const double* xyz, double* g) {
+  return guard([&] {
+    const Target t = make_target(kind, n, seed);
+    for (int i = 0; i < npts; ++i) t.grad(V3{{xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]}}, g + 3 * i);
+  });
 }
 
 }  // extern "C"

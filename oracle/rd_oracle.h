@@ -114,6 +114,13 @@ int or_l2_error_target_squared(const or_mesh* m, const or_system* s, const doubl
                                uint64_t seed, double* out);
 int or_h1_semi_error_manufactured(const or_mesh* m, const or_system* s,
                                   const double* coeffs, double rho_exact, double* out);
+/* assembly.cpp:265-310 with the TARGET field as the exact function (value = target evaluator,
+ * gradient = Target::grad): l2 = ||u_h - u_bar||_L2, h1 = ||grad(u_h - u_bar)||_L2 (degree-5 rule;
+ * either output may be null) -- the BASELINE error gates for every target, C3 included */
+int or_error_norms_target(const or_mesh* m, const or_system* s, const double* coeffs, int kind, int n,
+                          uint64_t seed, double* l2, double* h1);
+/* the target's exact gradient at npts points (xyz [npts][3] -> g [npts][3]) */
+int or_target_grad(int kind, int n, uint64_t seed, int npts, const double* xyz, double* g);
 
 #ifdef __cplusplus
 }

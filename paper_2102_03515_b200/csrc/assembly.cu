@@ -800,6 +800,36 @@ __device__ double lattice_interp(const double* __restrict__ nodal, int n, double
   return val;
 }
 
+// gradient of the P1 interpolant on the tet lattice_interp locates (oracle Target::interp_grad):
+// d/dx_a = n (r1 - r0), d/dx_b = n (r2 - r1), d/dx_c = n (r3 - r2) along the chain (a, b, c)
+__device__ void lattice_interp_grad(const double* __restrict__ nodal, int n, double x, double y, double z,
+                                    double* g) {
+  const int nv = n + 1;
+  const double p[3] = {x, y, z};
+  int cell[3];
+  double xi[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double s = __dmul_rn(p[d], (double)n);
+    int c = (int)floor(s);
+    c = min(max(c, 0), n - 1);
+    cell[d] = c;
+    xi[d] = __dsub_rn(s, (double)c);
+  }
+  const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  int pi = 0;
+  for (; pi < 5; ++pi)
+    if (xi[perms[pi][0]] >= xi[perms[pi][1]] && xi[perms[pi][1]] >= xi[perms[pi][2]]) break;
+  int c[3] = {cell[0], cell[1], cell[2]};
+  double r[4];
+  r[0] = nodal[(c[2] * nv + c[1]) * nv + c[0]];
+  for (int k = 0; k < 3; ++k) {
+    c[perms[pi][k]] += 1;
+    r[k + 1] = nodal[(c[2] * nv + c[1]) * nv + c[0]];
+  }
+  for (int k = 0; k < 3; ++k) g[perms[pi][k]] = __dmul_rn((double)n, __dsub_rn(r[k + 1], r[k]));
+}
+
 __device__ __forceinline__ double target_eval(int kind, double x, double y, double z, const double* nodal, int n) {
   switch (kind) {
     case RD_TARGET_SMOOTH: return sin3(x, y, z);
@@ -983,6 +1013,45 @@ __global__ void lat_load_gather_kernel(int nd, int n, const int* __restrict__ d2
 }
 
 // ---------------------------------------------------------------- error norms
+// The exact function of l2_error / h1_semi_error (std::function callbacks in the reference,
+// assembly.hpp:59-61), restricted to what the device can evaluate: mode 0 the manufactured
+// solution c sin^3 (target.cpp:45-58), mode 1 a target field u_bar with its gradient (sin^3 as
+// manufactured_exact(0), the random part's piecewise-constant P1 gradient, indicators 0 a.e.)
+struct ExactField {
+  int mode;
+  double c;  // mode 0
+  int kind;  // mode 1
+  const double* nodal;
+  int n;
+};
+__device__ __forceinline__ double exact_u(const ExactField& e, double x, double y, double z) {
+  return e.mode == 0 ? __dmul_rn(e.c, sin3(x, y, z)) : target_eval(e.kind, x, y, z, e.nodal, e.n);
+}
+__device__ __forceinline__ void exact_grad(const ExactField& e, double x, double y, double z, double* g) {
+  g[0] = g[1] = g[2] = 0.0;
+  const bool trig = e.mode == 0 || e.kind == RD_TARGET_SMOOTH || e.kind == RD_TARGET_NONZERO_BC ||
+                    e.kind == RD_TARGET_SINE_RANDOM;
+  if (trig) {
+    const double cp = __dmul_rn(e.mode == 0 ? e.c : 1.0, kPi);
+    const double sx = sin(__dmul_rn(kPi, x)), cx = cos(__dmul_rn(kPi, x));
+    const double sy = sin(__dmul_rn(kPi, y)), cy = cos(__dmul_rn(kPi, y));
+    const double sz = sin(__dmul_rn(kPi, z)), cz = cos(__dmul_rn(kPi, z));
+    g[0] = __dmul_rn(__dmul_rn(__dmul_rn(cp, cx), sy), sz);
+    g[1] = __dmul_rn(__dmul_rn(__dmul_rn(cp, sx), cy), sz);
+    g[2] = __dmul_rn(__dmul_rn(__dmul_rn(cp, sx), sy), cz);
+    if (e.mode == 1 && e.kind == RD_TARGET_SINE_RANDOM) {
+      double gr[3];
+      lattice_interp_grad(e.nodal, e.n, x, y, z, gr);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) g[d] = __dadd_rn(g[d], __dmul_rn(0.1, gr[d]));
+    }
+  } else if (e.mode == 1 && e.kind == RD_TARGET_QUADRATIC) {  // x y + 2 z
+    g[0] = y;
+    g[1] = x;
+    g[2] = 2.0;
+  }
+}
+
 // assembly.cpp:265-310 against the manufactured exact solution: per tet the
 // degree-5 rule's sum (in the reference's operation order), then a fixed-order
 // block reduction (the reference sums tets sequentially; the order of the final
@@ -992,7 +1061,7 @@ template <bool H1>
 __global__ void __launch_bounds__(kErrNT) error_norm_kernel(int nt, const int* __restrict__ tets,
                                                           const double* __restrict__ xyz,
                                                           const int* __restrict__ v2d,
-                                                          const double* __restrict__ coeffs, double cexact,
+                                                          const double* __restrict__ coeffs, ExactField ex,
                                                           double* partials, unsigned* counter, double* out) {
   __shared__ double sh[kErrNT / 32];
   const int t = blockIdx.x * kErrNT + threadIdx.x;
@@ -1035,7 +1104,7 @@ __global__ void __launch_bounds__(kErrNT) error_norm_kernel(int nt, const int* _
         double u = 0.0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) u = __dadd_rn(u, __dmul_rn(lam[k], nod[k]));
-        const double d = __dsub_rn(u, __dmul_rn(cexact, sin3(X[0], X[1], X[2])));
+        const double d = __dsub_rn(u, exact_u(ex, X[0], X[1], X[2]));
         acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_rules.w14[q], d), d));
       }
       contrib = __dmul_rn(vol, acc);
@@ -1048,7 +1117,6 @@ __global__ void __launch_bounds__(kErrNT) error_norm_kernel(int nt, const int* _
 #pragma unroll
           for (int c = 0; c < 3; ++c) gu[c] = __dadd_rn(gu[c], __dmul_rn(nod[k], G.g[k][c]));
         double acc = 0.0;
-        const double cp = __dmul_rn(cexact, kPi);
         for (int q = 0; q < 14; ++q) {
           const double* lam = c_rules.p14[q];
           double X[3];
@@ -1059,13 +1127,9 @@ __global__ void __launch_bounds__(kErrNT) error_norm_kernel(int nt, const int* _
             for (int k = 0; k < 4; ++k) s = __dadd_rn(s, __dmul_rn(lam[k], V[k][c]));
             X[c] = s;
           }
-          const double sx = sin(__dmul_rn(kPi, X[0])), cx = cos(__dmul_rn(kPi, X[0]));
-          const double sy = sin(__dmul_rn(kPi, X[1])), cy = cos(__dmul_rn(kPi, X[1]));
-          const double sz = sin(__dmul_rn(kPi, X[2])), cz = cos(__dmul_rn(kPi, X[2]));
-          const double ge0 = __dmul_rn(__dmul_rn(__dmul_rn(cp, cx), sy), sz);
-          const double ge1 = __dmul_rn(__dmul_rn(__dmul_rn(cp, sx), cy), sz);
-          const double ge2 = __dmul_rn(__dmul_rn(__dmul_rn(cp, sx), sy), cz);
-          const double d0 = __dsub_rn(gu[0], ge0), d1 = __dsub_rn(gu[1], ge1), d2 = __dsub_rn(gu[2], ge2);
+          double ge[3];
+          exact_grad(ex, X[0], X[1], X[2], ge);
+          const double d0 = __dsub_rn(gu[0], ge[0]), d1 = __dsub_rn(gu[1], ge[1]), d2 = __dsub_rn(gu[2], ge[2]);
           const double sq = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
           acc = __dadd_rn(acc, __dmul_rn(c_rules.w14[q], sq));
         }
@@ -1410,11 +1474,10 @@ double l2_error_target_squared(Ctx& c, const DMesh& m, const DSystem& s, const d
   return h;
 }
 
-void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, double rho, double* l2,
-                 double* h1) {
-  if (!(rho >= 0.0)) throw Error(RD_EINVAL, "manufactured_exact: rho must be >= 0");
+namespace {
+void error_norms_field(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, ExactField ex, double* l2,
+                       double* h1) {
   upload_rules(c);
-  const double cexact = 1.0 / (3.0 * rho * kPi * kPi + 1.0);  // target.cpp:45-58
   const int nt = m.nt;
   const int nb = std::max(div_up(nt, kErrNT), 1);
   DBuf<double> partials(nb, c.stream), outv(2, c.stream);
@@ -1422,11 +1485,11 @@ void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs,
   RDG_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), c.stream));
   RDG_CUDA(cudaMemsetAsync(outv.p, 0, 2 * sizeof(double), c.stream));
   if (nt > 0) {
-    error_norm_kernel<false><<<nb, kErrNT, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, s.v2d.p, coeffs, cexact,
-                                                          partials.p, counter.p, outv.p);
+    error_norm_kernel<false><<<nb, kErrNT, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, s.v2d.p, coeffs, ex, partials.p,
+                                                          counter.p, outv.p);
     RDG_LAUNCH_CHECK();
-    error_norm_kernel<true><<<nb, kErrNT, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, s.v2d.p, coeffs, cexact,
-                                                         partials.p, counter.p, outv.p + 1);
+    error_norm_kernel<true><<<nb, kErrNT, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, s.v2d.p, coeffs, ex, partials.p,
+                                                         counter.p, outv.p + 1);
     RDG_LAUNCH_CHECK();
     c.launches += 2;
   }
@@ -1435,6 +1498,32 @@ void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs,
   RDG_CUDA(cudaStreamSynchronize(c.stream));
   if (l2) *l2 = std::sqrt(h[0]);
   if (h1) *h1 = std::sqrt(h[1]);
+}
+}  // namespace
+
+void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, double rho, double* l2,
+                 double* h1) {
+  if (!(rho >= 0.0)) throw Error(RD_EINVAL, "manufactured_exact: rho must be >= 0");
+  ExactField ex{0, 1.0 / (3.0 * rho * kPi * kPi + 1.0), 0, nullptr, 0};  // target.cpp:45-58
+  error_norms_field(c, m, s, coeffs, ex, l2, h1);
+}
+
+void error_norms_target(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, int kind, uint64_t seed,
+                        double* l2, double* h1) {
+  if (kind < 0 || kind > RD_TARGET_QUADRATIC) throw Error(RD_EINVAL, "error_norms_target: unknown target kind");
+  if (kind == RD_TARGET_SINE_RANDOM && m.lattice_n < 1)
+    throw Error(RD_EINVAL, "error_norms_target: the sine+random target needs a build_structured_cube mesh");
+  const int n = m.lattice_n;
+  DBuf<double> nodal;
+  if (kind == RD_TARGET_SINE_RANDOM) {
+    const int64_t nv = (int64_t)(n + 1) * (n + 1) * (n + 1);
+    nodal.alloc(nv, c.stream);
+    random_nodal_kernel<<<div_up(nv, 256), 256, 0, c.stream>>>(n, seed, nodal.p);
+    RDG_LAUNCH_CHECK();
+    ++c.launches;
+  }
+  ExactField ex{1, 1.0, kind, nodal.p, n};
+  error_norms_field(c, m, s, coeffs, ex, l2, h1);
 }
 
 }  // namespace rdg

@@ -689,6 +689,18 @@ int rd_gpu_error_norms(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, c
   });
 }
 
+int rd_gpu_error_norms_target(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs,
+                              const rd_target* target, double* l2, double* h1) {
+  return guard(ctx, [&] {
+    require(mesh && sys && target && (coeffs || sys->s.n_dofs == 0), "error_norms_target: null argument");
+    require(sys->s.nv == mesh->m.nv, "error_norms_target: system does not belong to the mesh");
+    Ctx& c = ctx->c;
+    DBuf<double> tc;
+    const double* cd = in_dev(c, coeffs, sys->s.n_dofs, tc);
+    error_norms_target(c, mesh->m, sys->s, cd, target->kind, target->seed, l2, h1);
+  });
+}
+
 int rd_gpu_target_dual_norm(rd_ctx* ctx, const rd_system* sys, const double* coeffs, double* out) {
   return guard(ctx, [&] {
     require(sys && coeffs && out, "target_dual_norm: null argument");

@@ -193,6 +193,9 @@ void launch_lattice_tets_check(Ctx& c, cudaStream_t st, int n, const int* tets, 
 void build_system(Ctx& c, const DMesh& m, double rho, int target_kind, uint64_t seed, DSystem& s);
 // l2 / h1-semi error of the P1 field `coeffs` (device, n_dofs) vs the manufactured exact solution
 void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, double rho, double* l2, double* h1);
+// l2 / h1-semi error of `coeffs` vs a target field u_bar (value and exact gradient)
+void error_norms_target(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, int kind, uint64_t seed,
+                        double* l2, double* h1);
 // assembly.cpp:312-331: squared L2 distance of the P1 field to the target (the target's rule)
 double l2_error_target_squared(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, int kind,
                                uint64_t seed);

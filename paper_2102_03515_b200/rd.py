@@ -131,6 +131,7 @@ def lib():
         "rd_gpu_solve_host_mesh": (_I, [_P, _I, _P, _I, _P, _P, _D, _P, _D, _P, _P, _P]),
         "rd_gpu_error_norms": (_I, [_P, _P, _P, _P, _D, C.POINTER(_D), C.POINTER(_D)]),
         "rd_gpu_l2_error_target_squared": (_I, [_P, _P, _P, _P, _P, C.POINTER(_D)]),
+        "rd_gpu_error_norms_target": (_I, [_P, _P, _P, _P, _P, C.POINTER(_D), C.POINTER(_D)]),
         "rd_gpu_target_dual_norm": (_I, [_P, _P, _P, C.POINTER(_D)]),
         # distributed (z-slab) pieces, dist.py
         "rd_gpu_ctx_set_exact_sweeps": (_I, [_P, _I]),
@@ -435,6 +436,21 @@ def l2_error_target_squared(sys: FemSystem, coeffs, target: str, seed: int = 0) 
     ctx.check(lib().rd_gpu_l2_error_target_squared(ctx.h, sys.mesh.h, sys.h, _ptr(coeffs) if sys.n_dofs else None,
                                                    C.byref(t), C.byref(out)))
     return out.value
+
+
+def error_norms_target(sys: FemSystem, coeffs, target: str, seed: int = 0):
+    """assembly.hpp:59-61 l2_error / h1_semi_error with the target field as the exact function
+    (value and gradient), on the device: (||u_h - u_bar||_L2, ||grad(u_h - u_bar)||_L2)."""
+    ctx = sys.ctx
+    if isinstance(coeffs, np.ndarray) or isinstance(coeffs, (list, tuple)):
+        coeffs = np.ascontiguousarray(coeffs, np.float64)
+        if coeffs.size != sys.n_dofs:
+            raise RdInvalidArgument("error_norms_target: coefficient vector size mismatch")
+    t = _Target(TARGETS[target], int(seed))
+    l2, h1 = _D(), _D()
+    ctx.check(lib().rd_gpu_error_norms_target(ctx.h, sys.mesh.h, sys.h, _ptr(coeffs) if sys.n_dofs else None,
+                                              C.byref(t), C.byref(l2), C.byref(h1)))
+    return l2.value, h1.value
 
 
 def target_dual_norm(sys: FemSystem, coeffs) -> float:

@@ -563,6 +563,24 @@ def test_target_dual_norm(rd, O, n, rho, target):
     assert abs(got - want) <= tol * want, (got, want)
 
 
+@pytest.mark.parametrize("target", ["smooth", "sine_random", "ball", "box", "quadratic", "nonzero_bc"])
+@pytest.mark.parametrize("n", [8, 13])
+def test_error_norms_target_parity(rd, O, n, target):
+    """assembly.cpp:265-310 with the target field as the exact function (value and gradient,
+    oracle Target::grad) on the device against the oracle, for the solution and for a
+    pseudo-random field; CUDA sin/cos vs glibc -> 1e-12 relative."""
+    rho = 1e-2
+    om = O.build_structured_cube(n)
+    os_ = O.build_system(om, rho, target)
+    u = O.solve_system_amg(os_, 1e-8).u
+    ds = rd.build_system(rd.build_structured_cube(n), rho, target)
+    for coeffs in (u, O.pseudo_random_vec(os_.n_dofs, 11)):
+        want = O.error_norms_target(om, os_, coeffs, target, n, 0)
+        got = rd.error_norms_target(ds, coeffs, target)
+        for g, w in zip(got, want):
+            assert abs(g - w) <= 1e-12 * max(w, 1e-300), (target, got, want)
+
+
 def _goldens():
     import json as _json
     return _json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
@@ -585,9 +603,13 @@ def test_baseline_config_goldens(rd, case):
         assert abs(u[int(i)] - v) <= 1e-10 * np.abs(u).max()
     l2 = math.sqrt(rd.l2_error_target_squared(ds, u, target))
     assert abs(l2 - case["l2_u_minus_target"]) <= 1e-10 * case["l2_u_minus_target"]
-    if "h1_u_minus_target" in case:
-        _, h1 = rd.error_norms(ds, u, 0.0)
-        assert abs(h1 - case["h1_u_minus_target"]) <= 1e-10 * case["h1_u_minus_target"]
+    # the gates with the target as the exact function: ||u - u_bar|| (degree 5), ||grad(u - u_bar)||
+    l2d5, h1 = rd.error_norms_target(ds, u, target)
+    assert abs(l2d5 - case["l2_deg5_u_minus_target"]) <= 1e-10 * case["l2_deg5_u_minus_target"]
+    assert abs(h1 - case["h1_u_minus_target"]) <= 1e-10 * case["h1_u_minus_target"]
+    if target == "smooth":  # the same gate through manufactured_exact(0)
+        _, h1m = rd.error_norms(ds, u, 0.0)
+        assert h1m == h1
 
 
 @pytest.mark.parametrize("n,target", [(256, "smooth"), (512, "ball")])

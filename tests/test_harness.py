@@ -1,0 +1,70 @@
+"""SURVEY.md §8(f)2 harness parity: include/rd_gpu_harness.hpp (the reference's ExperimentConfig,
+validate, config JSON, EocTable/CSV conventions, run_precond_bench, MatrixMarket I/O) and the
+rdbench bench-precond CLI (paper_2102_03515_b200/cli/rdbench.cpp) with the reference's exit codes
+(tools/rdbench.cpp:121-125, :186-190: 0 converged, 1 a row did not converge, 2 an exception)."""
+import csv
+import io
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2102_03515_b200")
+RDBENCH = os.path.join(PKG, "_build", "rdbench")
+HARNESS = os.path.join(ROOT, "tests", "cpp", "test_harness")
+
+
+def _built(path):
+    if not os.path.exists(path):
+        subprocess.run(["make", "-s", "-C", PKG], check=True)
+    return path
+
+
+def test_harness_host_checks(tmp_path):
+    out = subprocess.run([_built(HARNESS), str(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("args", [["bench-precond", "--rho", "-1"], ["bench-precond", "--n", "0"],
+                                  ["bench-precond", "--tol", "0"], ["bench-precond", "--precond", "jacobi"],
+                                  ["bench-precond", "--precond", "ilu"], ["bench-precond", "--example", "ball"],
+                                  ["bench-precond", "--bogus"], ["table-h"], ["adapt"], ["nope"], []])
+def test_rdbench_rejects_with_exit_2(args):
+    """Rejected configs raise std::invalid_argument before any device work: exit code 2 and an
+    'error:' line (rdbench.cpp:186-190); the other subcommands are outside the device path."""
+    out = subprocess.run([_built(RDBENCH)] + args, capture_output=True, text=True, timeout=60)
+    assert out.returncode == 2, (args, out.stdout, out.stderr)
+    assert out.stdout == ""
+
+
+@pytest.mark.gpu
+def test_rdbench_bench_precond_rows(O, tmp_path):
+    """bench-precond rows (bench.cpp:392-423) from the device: the reference's columns and
+    number formats, rho outer / n inner, iteration counts equal to the oracle's."""
+    path = tmp_path / "rows.csv"
+    out = subprocess.run([_built(RDBENCH), "bench-precond", "--rho", "1", "1e-4", "--n", "8", "12",
+                          "--out", str(path)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    text = path.read_text()
+    rows = list(csv.DictReader(io.StringIO(text)))
+    assert text.splitlines()[0] == "rho,n,dofs,iterations,converged,setup_seconds,solve_seconds"
+    assert [(r["rho"], r["n"]) for r in rows] == [("1.000000e+00", "8"), ("1.000000e+00", "12"),
+                                                  ("1.000000e-04", "8"), ("1.000000e-04", "12")]
+    for r in rows:
+        n, rho = int(r["n"]), float(r["rho"])
+        ref = O.solve_system_amg(O.build_system(O.build_structured_cube(n), rho, "smooth"), 1e-8)
+        assert int(r["dofs"]) == (n - 1) ** 3 and int(r["converged"]) == 1
+        assert int(r["iterations"]) == ref.iterations
+        assert float(r["setup_seconds"]) > 0 and float(r["solve_seconds"]) > 0
+
+
+@pytest.mark.gpu
+def test_rdbench_nonconverged_row_exit_1(tmp_path):
+    """A row that does not converge within pcg's 500 iterations still prints; exit code 1."""
+    out = subprocess.run([_built(RDBENCH), "bench-precond", "--rho", "1", "--n", "16", "--tol", "1e-300",
+                          "--gnuplot"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 1, out.stdout + out.stderr
+    assert out.stdout.startswith("# rho n dofs iterations converged setup_seconds solve_seconds\n# rho = ")
+    assert " 500 0 " in out.stdout and "1 row(s) did not converge" in out.stderr

@@ -511,3 +511,58 @@ def test_oracle_reproduces_c1_golden(O):
     assert [float(v) for v in r.residual_history] == c1["residual_history"]
     assert float(np.linalg.norm(r.x)) == c1["u_norm2"]
     assert math.sqrt(O.l2_error_target_squared(m, s, r.x, "smooth")) == c1["l2_u_minus_target"]
+    l2d5, h1 = O.error_norms_target(m, s, r.x, "smooth", c1["n"], 0)
+    assert l2d5 == c1["l2_deg5_u_minus_target"] and h1 == c1["h1_u_minus_target"]
+
+
+def _fd_grad(O, kind, pts, n, h=1e-7):
+    fd = np.zeros_like(pts)
+    for d in range(3):
+        e = np.zeros(3)
+        e[d] = h
+        fd[:, d] = (O.target_eval(kind, pts + e, n, 0) - O.target_eval(kind, pts - e, n, 0)) / (2 * h)
+    return fd
+
+
+@pytest.mark.parametrize("kind", ["smooth", "nonzero_bc", "sine_random", "quadratic", "ball", "one"])
+def test_target_gradient_matches_finite_differences(O, kind):
+    """The exact gradients behind the error gates (oracle Target::grad) against central
+    differences of the target evaluator, at points inside Kuhn tets (away from faces, where the
+    random part's P1 gradient jumps)."""
+    n = 8
+    rng = np.random.default_rng(3)
+    cells = rng.integers(0, n, (200, 3))
+    xi = rng.uniform(0.0, 1.0, (200, 3))
+    srt = -np.sort(-xi, axis=1)  # keep points 1e-3 away from every tet face of the cell
+    gaps = np.concatenate([1 - srt[:, :1], srt[:, :-1] - srt[:, 1:], srt[:, -1:]], axis=1)
+    keep = gaps.min(axis=1) > 1e-3
+    pts = ((cells + xi) / n)[keep]
+    g = O.target_grad(kind, pts, n)
+    fd = _fd_grad(O, kind, pts, n)
+    assert np.abs(g - fd).max() <= 1e-6 * max(1.0, np.abs(g).max())
+
+
+def test_error_norms_target_smooth_is_manufactured_zero(O):
+    """||grad(u - u_bar)|| of the smooth target is h1_semi_error with
+    manufactured_exact(0) (c = 1 exactly), and ||u - u_bar|| its l2_error -- bit for bit."""
+    m = O.build_structured_cube(8)
+    s = O.build_system(m, 1e-2, "smooth")
+    u = O.solve_system_amg(s, 1e-8).u
+    l2, h1 = O.error_norms_target(m, s, u, "smooth", 8, 0)
+    assert h1 == O.h1_semi_error_manufactured(m, s, u, 0.0)
+    assert l2 == O.l2_error_manufactured(m, s, u, 0.0)
+
+
+def test_error_norms_target_zero_field(O):
+    """Against the zero field the gates are the target's own norms: ||grad sin^3||_L2 =
+    pi sqrt(3/8) on the unit cube (degree-5 rule, so to quadrature accuracy), and the sine+random
+    target's differs by its random part's gradient."""
+    n = 8
+    m = O.build_structured_cube(n)
+    s_smooth = O.build_system(m, 1.0, "smooth")
+    l2s, h1s = O.error_norms_target(m, s_smooth, np.zeros(s_smooth.n_dofs), "smooth", n, 0)
+    assert abs(h1s - math.pi * math.sqrt(3.0 / 8.0)) < 1e-6
+    assert abs(l2s - math.sqrt(1.0 / 8.0)) < 1e-6
+    s = O.build_system(m, 1.0, "sine_random")
+    l2z, h1z = O.error_norms_target(m, s, np.zeros(s.n_dofs), "sine_random", n, 0)
+    assert h1z > 0 and abs(h1z - h1s) > 1e-3
