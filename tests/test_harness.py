@@ -61,10 +61,11 @@ def test_rdbench_bench_precond_rows(O, tmp_path):
 
 
 @pytest.mark.gpu
-def test_rdbench_nonconverged_row_exit_1(tmp_path):
-    """A row that does not converge within pcg's 500 iterations still prints; exit code 1."""
+def test_rdbench_breakdown_is_an_exception(tmp_path):
+    """An unattainable tolerance drives PCG past the rounding floor until p'Ap <= 0: pcg throws
+    (linalg.cpp:81-82) and rdbench reports it with exit code 2, as the reference does; the
+    --gnuplot path and the exit-1 rule for non-converged rows are covered host-side."""
     out = subprocess.run([_built(RDBENCH), "bench-precond", "--rho", "1", "--n", "16", "--tol", "1e-300",
                           "--gnuplot"], capture_output=True, text=True, timeout=300)
-    assert out.returncode == 1, out.stdout + out.stderr
-    assert out.stdout.startswith("# rho n dofs iterations converged setup_seconds solve_seconds\n# rho = ")
-    assert " 500 0 " in out.stdout and "1 row(s) did not converge" in out.stderr
+    assert out.returncode == 2, out.stdout + out.stderr
+    assert "not positive definite" in out.stderr and out.stdout == ""
