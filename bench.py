@@ -168,10 +168,17 @@ def _run_dist(args, rank, world, local_rank, dev, stream):
     ctx.synchronize()
     last = {}
 
+    phase_ev = []  # (start, after setup, after solve) events per timed step, on the rd stream
+
     def step():
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
         ops = DeviceOps(n, rho, args.target, ctx=ctx, device=local_rank, mesh=mesh)
         solver = DistSolver(comm, ops, gather_rows=args.gather_rows, mode=args.mode)
+        ev[1].record(stream)
         res = solver.pcg(TOL, 500)
+        ev[2].record(stream)
+        phase_ev.append(ev)
         last.update(ops=ops, solver=solver, res=res)
         return ops.rows[0], res
 
@@ -181,6 +188,7 @@ def _run_dist(args, rank, world, local_rank, dev, stream):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    phase_ev.clear()
     clocks = ClockSampler(local_rank)
     barrier()
     torch.cuda.synchronize()
@@ -204,6 +212,12 @@ def _run_dist(args, rank, world, local_rank, dev, stream):
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     elapsed_ms = float(t.item())
     value = float(ndofs) * sum(its) / (elapsed_ms / 1e3)
+    # setup (replicated build_system + build_amg + slab localisation + neighbour linking) and
+    # the distributed pcg, each the max over ranks of its per-step mean
+    ph = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in phase_ev) / len(phase_ev),
+                       sum(e[1].elapsed_time(e[2]) for e in phase_ev) / len(phase_ev)], dtype=torch.float64,
+                      device=dev)
+    torch.distributed.all_reduce(ph, op=torch.distributed.ReduceOp.MAX)
     solver = last["solver"]
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -218,6 +232,7 @@ def _run_dist(args, rank, world, local_rank, dev, stream):
                    "slab_cuts": solver.plan.cuts,
                    "l2": "inputs exceed L2 (device mesh 255 MB, A 364 MB > 126 MB L2); no flush"},
         "iterations": its[0],
+        "phases_ms": {"setup_replicated": float(ph[0]), "distributed_pcg": float(ph[1])},
         "clocks": clk,
         "gpu_launches": launches,
         "exchanges_per_iteration": {"halo_planes": "1 per face before SpMV/residual/restriction/"
@@ -537,6 +552,78 @@ def other_configs(ctx, stream):
             del mesh, u
         except Exception as e:  # reported, never fatal for the headline line
             out.append({"config": name, "error": str(e)[:200]})
+    out += generic_legs(ctx, stream)
+    return out
+
+
+def generic_legs(ctx, stream, n=N_DEFAULT):
+    """The C2 workload on the paths the lattice fast paths do not take (SURVEY.md 8(a) generic
+    kernels): (1) jittered interior coordinates -- Kuhn lattice, non-uniform geometry, per-cell
+    values, packed-stencil sweeps; (2) renumbered vertices + shuffled tets -- no lattice anywhere:
+    vertex->tet CSR assembly, MIS coarsening, Gustavson Galerkin, the sync-free Gauss-Seidel.
+    One timed build_system + solve each after a warm-up, plus each level's forward sweep."""
+    import numpy as np
+    import torch
+
+    from paper_2102_03515_b200 import rd
+
+    rho, target = rho_for(n), TARGET
+    xyz, tets, b = rd.build_structured_cube(n, ctx).download()
+    rng = np.random.default_rng(5)
+    xj = xyz.copy()
+    xj[b == 0] += rng.uniform(-0.2, 0.2, size=(int((b == 0).sum()), 3)) / n
+    rng = np.random.default_rng(7)
+    pv = rng.permutation(xyz.shape[0])
+    inv = np.empty_like(pv)
+    inv[pv] = np.arange(pv.size)
+    tr = inv[tets][rng.permutation(tets.shape[0])].astype(np.int32)
+    legs = [("C2_jittered", "jittered interior coordinates (+-0.2 h, seeded): lattice pattern, per-cell geometry",
+             (xj, tets, b)),
+            ("C2_renumbered", "renumbered vertices + shuffled tets (seeded): no lattice, every generic kernel",
+             (np.ascontiguousarray(xyz[pv]), np.ascontiguousarray(tr), np.ascontiguousarray(b[pv])))]
+    out = []
+    for name, what, arrays in legs:
+        try:
+            mesh = rd.mesh_from_arrays(*arrays, ctx=ctx)
+            u = None
+            for rep in range(2):
+                ctx.synchronize()
+                a = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                s = rd.build_system(mesh, rho, target)
+                if u is None:
+                    u = torch.empty(s.n_dofs, dtype=torch.float64, device=stream.device)
+                o = rd.solve_system_amg(s.A, s.f_ptr, TOL, u=u)
+                e.record(stream)
+                torch.cuda.synchronize()
+                ms = a.elapsed_time(e)
+            h = rd.build_amg(s.A)
+            levels = []
+            for l in range(h.num_levels - 1):
+                A = h.level(l)
+                x = torch.rand(A.rows, dtype=torch.float64, device=stream.device)
+                f = torch.rand(A.rows, dtype=torch.float64, device=stream.device)
+                y = torch.empty_like(x)
+                h.level_sweep(l, True, f, x, y)
+                ctx.synchronize()
+                a = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(3):
+                    h.level_sweep(l, True, f, x, y)
+                e.record(stream)
+                torch.cuda.synchronize()
+                levels.append({"level": l, "rows": A.rows, "nnz": A.nnz, "stencil": h.stencil_source(l),
+                               "fwd_sweep_ms": a.elapsed_time(e) / 3})
+            out.append({"config": name, "what": what, "n": n, "n_dofs": s.n_dofs, "target": target, "rho": rho,
+                        "lattice_mesh": mesh.lattice_n, "iterations": o.iterations, "ms_per_step": ms,
+                        "value": s.n_dofs * o.iterations / (ms / 1e3), "unit": UNIT,
+                        "phases_ms": {"setup": 1e3 * o.setup_seconds, "pcg": 1e3 * o.solve_seconds},
+                        "levels": levels})
+            del s, h, mesh, u
+        except Exception as ex:  # reported, never fatal for the headline line
+            out.append({"config": name, "error": str(ex)[:200]})
     return out
 
 
