@@ -60,6 +60,14 @@ def parse():
     return p.parse_args()
 
 
+def workload_config(n, n_dofs, target):
+    """The workload both arms name (identical dicts, so the driver's same-config check holds)."""
+    return {"workload": f"C2: build_system + build_amg + pcg, n={n} ({n_dofs} dofs), rho=h^2, {target} target, "
+                        f"rtol {TOL}",
+            "n": n, "n_dofs": n_dofs, "rho": rho_for(n), "target": target, "tol": TOL,
+            "l2": "inputs exceed L2 (device mesh 255 MB, A 364 MB > 126 MB L2 at n=128); no flush"}
+
+
 def rho_for(n):
     return 1.0 / (n * n)
 
@@ -224,13 +232,10 @@ def _run_dist(args, rank, world, local_rank, dev, stream):
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated Kuhn lattice, ball target, seeded)",
-        "config": {"workload": f"C2 cut into {world} z-slabs: build_system + build_amg (replicated) + "
-                               f"distributed pcg, n={n} ({ndofs} dofs), rho=h^2, {args.target} target, rtol {TOL}",
-                   "n": n, "n_dofs": ndofs, "rho": rho, "target": args.target, "tol": TOL,
-                   "parallelism": f"z-slabs x{world} ({args.mode} smoother hand-off), "
-                                  f"{solver.G} distributed level(s), coarse tail on rank 0",
-                   "slab_cuts": solver.plan.cuts,
-                   "l2": "inputs exceed L2 (device mesh 255 MB, A 364 MB > 126 MB L2); no flush"},
+        "config": workload_config(n, ndofs, args.target),
+        "parallelism": f"z-slabs x{world} ({args.mode} smoother hand-off), {solver.G} distributed level(s), "
+                       f"coarse tail on rank 0; setup replicated on every rank",
+        "slab_cuts": solver.plan.cuts,
         "iterations": its[0],
         "phases_ms": {"setup_replicated": float(ph[0]), "distributed_pcg": float(ph[1])},
         "clocks": clk,
@@ -352,11 +357,8 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated Kuhn lattice, ball target, seeded)",
-        "config": {"workload": f"C2: build_system + build_amg + pcg, n={n} ({ndofs} dofs), rho=2^{-2 * int(np.log2(n))}"
-                               f" (h^2), {args.target} target, rtol {TOL}",
-                   "n": n, "n_dofs": ndofs, "rho": rho, "target": args.target, "tol": TOL,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs exceed L2 (device mesh 255 MB, A 364 MB > 126 MB L2); no flush"},
+        "config": workload_config(n, ndofs, args.target),
+        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
         "iterations": its[0],
         "phases_ms": {"setup_host_clock": 1e3 * statistics.mean(setup_s), "pcg_host_clock": 1e3 * statistics.mean(solve_s)},
         "pcg_dof_iters_per_s": float(ndofs) * statistics.mean(its) / statistics.mean(solve_s),
@@ -627,6 +629,23 @@ def generic_legs(ctx, stream, n=N_DEFAULT):
     return out
 
 
+def host_info():
+    """CPU model and RAM of the host the CPU baseline ran on."""
+    model, mem_gb = None, None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                mem_gb = round(int(line.split()[1]) / 2 ** 20, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "ram_gib": mem_gb}
+
+
 def host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -645,7 +664,8 @@ def cpu_baseline(n, target):
     out = {"value": r["n_dofs"] * r["iterations"] / r["total_s"], "unit": UNIT, "cores": cores, "kind": "port",
            "sample": f"one full C2 step on the CPU oracle (n={n}: build_system + build_amg + pcg, "
                      f"{r['iterations']} iterations), {r['total_s']:.1f} s; SGS/setup serial as in the reference",
-           "phases_s": {"build": r["build_s"], "setup": r["setup_s"], "solve": r["solve_s"]}}
+           "phases_s": {"build": r["build_s"], "setup": r["setup_s"], "solve": r["solve_s"]},
+           "host": host_info()}
     if cores > 1 and not os.environ.get("RD_BENCH_NO_CPU1"):  # threads = 1 as well
         O.set_num_threads(1)
         r1 = O.pipeline(n, rho_for(n), target, 0, TOL)
@@ -678,12 +698,12 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated Kuhn lattice, ball target, seeded)",
-        "config": {"workload": f"C2: build_system + build_amg + pcg, n={n}, rho=h^2, {args.target} target, rtol {TOL}",
-                   "n": n, "n_dofs": runs[0]["n_dofs"], "rho": rho_for(n), "target": args.target, "tol": TOL},
+        "config": workload_config(n, runs[0]["n_dofs"], args.target),
         "iterations": runs[0]["iterations"],
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{args.steps} full C2 steps (reference rdsolve not buildable here: no Eigen; "
-                                   f"the oracle/ C++ port with -O3 -ffp-contract=off, {cores} threads)"},
+                                   f"the oracle/ C++ port with -O3 -ffp-contract=off, {cores} threads)",
+                         "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "phases_s": {k: statistics.mean(r[k] for r in runs) for k in ("build_s", "setup_s", "solve_s")},
     }

@@ -267,6 +267,84 @@ __global__ void __launch_bounds__(128) stencil_spmv_kernel(int L, const double* 
   }
 }
 
+// The same product, 2.5-D blocked: a block owns a 32 (x) x 8 (y) column of rows and marches
+// up ZC planes in z, the x values of planes z-1 .. z+2 (with a one-line halo in x and y,
+// zero outside the box) staged in a 4-plane shared-memory ring, so each x value is read
+// from L2 / HBM about once instead of nine times (one line per block above).  A row sums
+// its 15 slots from +0 in ascending column order; absent slots read x = +0 (finite coefficient
+// * +0 = +-0, and a running sum from +0 never becomes -0), so the result is the CSR row sum.
+constexpr int kStTX = 32, kStTY = 8, kStZC = 8;
+constexpr int kStPX = kStTX + 2, kStPY = kStTY + 2, kStPlane = kStPX * kStPY;
+template <int MODE, bool CLS>
+__global__ void __launch_bounds__(kStTX* kStTY) stencil_spmv_tiled_kernel(int L, const double* __restrict__ tab,
+                                                                         const double* __restrict__ x,
+                                                                         double* __restrict__ y,
+                                                                         const double* __restrict__ r) {
+  __shared__ __align__(16) double st[CLS ? 64 * 16 : 16];
+  __shared__ double pl[4][kStPlane];
+  const int tid = threadIdx.x, tx = tid % kStTX, ty = tid / kStTX;
+  for (int k = tid; k < (CLS ? 64 * 16 : 16); k += kStTX * kStTY) st[k] = __ldg(tab + k);
+  const int a0 = blockIdx.x * kStTX, y0 = blockIdx.y * kStTY, z0 = blockIdx.z * kStZC;
+  const int z1 = min(z0 + kStZC, L);
+  const long long P = (long long)L * L;
+  // this thread's staging elements of a plane (kStPlane = 340 <= 2 * 256)
+  auto stage = [&](int z, double (&v)[2]) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int e = tid + q * kStTX * kStTY;
+      v[q] = 0.0;
+      if (e < kStPlane) {
+        const int aa = a0 - 1 + e % kStPX, yy = y0 - 1 + e / kStPX;
+        if (z >= 0 && z < L && aa >= 0 && aa < L && yy >= 0 && yy < L) v[q] = __ldg(x + (z * P + (long long)yy * L + aa));
+      }
+    }
+  };
+  auto put = [&](int z, const double (&v)[2]) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int e = tid + q * kStTX * kStTY;
+      if (e < kStPlane) pl[(z + 4) & 3][e] = v[q];
+    }
+  };
+  double v0[2], v1[2], v2[2];
+  stage(z0 - 1, v0);
+  stage(z0, v1);
+  stage(z0 + 1, v2);
+  put(z0 - 1, v0);
+  put(z0, v1);
+  put(z0 + 1, v2);
+  __syncthreads();
+  const int a = a0 + tx, yy = y0 + ty;
+  const bool valid = a < L && yy < L;
+  const int cay = CLS ? (pos_class(a < L ? a : 0, L) * 16 + pos_class(yy < L ? yy : 0, L) * 4) : 0;
+  double U[15];
+  if (!CLS) {
+#pragma unroll
+    for (int k = 0; k < 15; ++k) U[k] = st[k];
+  }
+  const int c0 = (ty + 1) * kStPX + tx + 1;  // this row's cell in a staged plane
+  for (int z = z0; z < z1; ++z) {
+    double nv[2];
+    stage(z + 2, nv);  // in flight while this plane's rows are summed
+    const double* pm = pl[(z - 1 + 4) & 3];
+    const double* p0 = pl[z & 3];
+    const double* pp = pl[(z + 1) & 3];
+    const double* v = CLS ? st + (cay + pos_class(z, L)) * 16 : U;
+    const double xs[15] = {pm[c0 - kStPX - 1], pm[c0 - kStPX], pm[c0 - 1], pm[c0],
+                           p0[c0 - kStPX - 1], p0[c0 - kStPX], p0[c0 - 1], p0[c0], p0[c0 + 1], p0[c0 + kStPX],
+                           p0[c0 + kStPX + 1], pp[c0], pp[c0 + 1], pp[c0 + kStPX], pp[c0 + kStPX + 1]};
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 15; ++k) acc = __dadd_rn(acc, __dmul_rn(v[k], xs[k]));
+    if (valid) {
+      const long long i = z * P + (long long)yy * L + a;
+      y[i] = MODE == kResidual ? __dsub_rn(r[i], acc) : acc;
+    }
+    put(z + 2, nv);
+    __syncthreads();
+  }
+}
+
 template <int MODE>
 void launch_spmv(Ctx& c, const DCsr& A, const double* x, double* y, const double* r, double* dot_out) {
   if (A.rows == 0) {
@@ -279,8 +357,9 @@ void launch_spmv(Ctx& c, const DCsr& A, const double* x, double* y, const double
     const int L = A.lat.lx;
     const bool cls = A.lat_uni_state == 2;
     constexpr int M = MODE == kResidual ? kResidual : kPlain;
-    auto* k = cls ? stencil_spmv_kernel<M, true> : stencil_spmv_kernel<M, false>;
-    k<<<L * L, 128, 0, c.stream>>>(L, cls ? A.lat_cls.p : A.lat_uni.p, x, y, r);
+    auto* k = cls ? stencil_spmv_tiled_kernel<M, true> : stencil_spmv_tiled_kernel<M, false>;
+    const dim3 grid(div_up(L, kStTX), div_up(L, kStTY), div_up(L, kStZC));
+    k<<<grid, kStTX * kStTY, 0, c.stream>>>(L, cls ? A.lat_cls.p : A.lat_uni.p, x, y, r);
     RDG_LAUNCH_CHECK();
     ++c.launches;
     if (MODE == kDot) dot(c, A.rows, x, y, dot_out);
