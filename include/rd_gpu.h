@@ -240,6 +240,27 @@ int rd_gpu_dot_async(rd_ctx* ctx, int n, const double* a, const double* b, doubl
 int rd_gpu_pcg_update_xr(rd_ctx* ctx, int64_t n, double alpha, const double* p, const double* ap, double* x,
                          double* r);
 int rd_gpu_pcg_update_p(rd_ctx* ctx, int64_t n, double beta, const double* z, double* p);
+
+/* The distributed PCG's scalars on the device (linalg.cpp:64-102 split across ranks): every
+ * rank all-gathers its local dot partials into `parts` [world] (NCCL, on the stream) and these
+ * calls sum them in rank order -- the same bits on every rank -- and keep rz, alpha, beta,
+ * the relative residual and the convergence / SPD status in a device-resident rd_pcg_state,
+ * so no scalar crosses to the host inside the loop; the host reads the 64-byte state once
+ * per iteration.  After done or a status, alpha / xr / check / p calls are no-ops.
+ *   status 1: p'Ap <= 0 (runtime_error "pcg: operator not positive definite (p'Ap <= 0)")
+ *   status 2: r'z < 0   (runtime_error "pcg: preconditioner not positive definite")       */
+typedef struct rd_pcg_state {
+  double rz, rz0, pap, rz_next, alpha, beta, rel, reserved;
+  int32_t done, status, iterations, reserved2;
+} rd_pcg_state;
+int rd_gpu_pcg_dist_begin(rd_ctx* ctx, int world, const double* parts, rd_pcg_state* st);   /* rz0 = sum */
+int rd_gpu_pcg_dist_alpha(rd_ctx* ctx, int world, const double* parts, rd_pcg_state* st);   /* pAp, alpha */
+int rd_gpu_pcg_dist_xr(rd_ctx* ctx, int64_t n, const rd_pcg_state* st, const double* p, const double* ap, double* x,
+                       double* r);
+/* rz_next = sum, history[it-1] = rel = sqrt(rz_next / rz0), done if rel <= tol, else beta */
+int rd_gpu_pcg_dist_check(rd_ctx* ctx, int world, const double* parts, rd_pcg_state* st, double tol, double* history,
+                          int history_cap);
+int rd_gpu_pcg_dist_p(rd_ctx* ctx, int64_t n, const rd_pcg_state* st, const double* z, double* p);
 /* the V-cycle of the sub-hierarchy from `level` (amg.cpp:121-132 entered at level l):
  * r, z of rows(A_level); the coarse tail of a distributed V-cycle, on rank 0   */
 int rd_gpu_amg_apply_from(rd_amg* h, int level, const double* r, double* z);

@@ -57,6 +57,71 @@ __global__ void dist_p_kernel(int64_t n, double beta, const double* __restrict__
     p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
 }
 
+// ---- device-resident distributed PCG scalars (rd_pcg_state): rank-ordered sums of the
+// all-gathered partials, so every rank computes the same bits
+__device__ __forceinline__ double rank_sum(int world, const double* __restrict__ parts) {
+  double s = 0.0;
+  for (int k = 0; k < world; ++k) s = __dadd_rn(s, parts[k]);
+  return s;
+}
+__global__ void dpcg_begin_kernel(int world, const double* parts, rd_pcg_state* st) {
+  const double rz = rank_sum(world, parts);
+  st->rz = rz;
+  st->rz0 = rz;
+  st->done = 0;
+  st->status = 0;
+  st->iterations = 0;
+  if (rz < 0.0) st->status = 2;  // linalg.cpp:71
+  else if (rz == 0.0) st->done = 1;  // linalg.cpp:73-76
+}
+__global__ void dpcg_alpha_kernel(int world, const double* parts, rd_pcg_state* st) {
+  if (st->done || st->status) return;
+  const double pAp = rank_sum(world, parts);
+  st->pap = pAp;
+  if (!(pAp > 0.0)) {  // linalg.cpp:80-82
+    st->status = 1;
+    return;
+  }
+  st->alpha = __ddiv_rn(st->rz, pAp);
+}
+__global__ void dpcg_xr_kernel(int64_t n, const rd_pcg_state* st, const double* __restrict__ p,
+                               const double* __restrict__ Ap, double* __restrict__ x, double* __restrict__ r) {
+  if (st->done || st->status) return;
+  const double alpha = st->alpha;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    r[i] = __dsub_rn(r[i], __dmul_rn(alpha, Ap[i]));
+  }
+}
+__global__ void dpcg_check_kernel(int world, const double* parts, rd_pcg_state* st, double tol, double* hist,
+                                  int cap) {
+  if (st->done || st->status) return;
+  const double rzn = rank_sum(world, parts);
+  st->rz_next = rzn;
+  if (rzn < 0.0) {  // linalg.cpp:87-89
+    st->status = 2;
+    return;
+  }
+  const double rel = __dsqrt_rn(__ddiv_rn(rzn, st->rz0));
+  const int it = st->iterations + 1;
+  st->iterations = it;
+  st->rel = rel;
+  if (hist && it - 1 < cap) hist[it - 1] = rel;
+  if (rel <= tol) {
+    st->done = 1;
+    return;
+  }
+  st->beta = __ddiv_rn(rzn, st->rz);
+  st->rz = rzn;
+}
+__global__ void dpcg_p_kernel(int64_t n, const rd_pcg_state* st, const double* __restrict__ z,
+                              double* __restrict__ p) {
+  if (st->done || st->status) return;
+  const double beta = st->beta;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+}
+
 int vgrid(Ctx& c, int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * 8, (n + 255) / 256));
 }
@@ -153,6 +218,51 @@ int rd_gpu_pcg_update_p(rd_ctx* ctx, int64_t n, double beta, const double* z, do
     Ctx& c = ctx->c;
     if (n == 0) return;
     dist_p_kernel<<<vgrid(c, n), 256, 0, c.stream>>>(n, beta, z, p);
+    RDG_LAUNCH_CHECK();
+    ++c.launches;
+  });
+}
+
+int rd_gpu_pcg_dist_begin(rd_ctx* ctx, int world, const double* parts, rd_pcg_state* st) {
+  return guard(ctx, [&] {
+    require(world >= 1 && parts && st, "pcg_dist_begin: bad argument");
+    dpcg_begin_kernel<<<1, 1, 0, ctx->c.stream>>>(world, parts, st);
+    RDG_LAUNCH_CHECK();
+    ++ctx->c.launches;
+  });
+}
+int rd_gpu_pcg_dist_alpha(rd_ctx* ctx, int world, const double* parts, rd_pcg_state* st) {
+  return guard(ctx, [&] {
+    require(world >= 1 && parts && st, "pcg_dist_alpha: bad argument");
+    dpcg_alpha_kernel<<<1, 1, 0, ctx->c.stream>>>(world, parts, st);
+    RDG_LAUNCH_CHECK();
+    ++ctx->c.launches;
+  });
+}
+int rd_gpu_pcg_dist_xr(rd_ctx* ctx, int64_t n, const rd_pcg_state* st, const double* p, const double* ap, double* x,
+                       double* r) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    if (n == 0) return;
+    dpcg_xr_kernel<<<vgrid(c, n), 256, 0, c.stream>>>(n, st, p, ap, x, r);
+    RDG_LAUNCH_CHECK();
+    ++c.launches;
+  });
+}
+int rd_gpu_pcg_dist_check(rd_ctx* ctx, int world, const double* parts, rd_pcg_state* st, double tol, double* hist,
+                          int cap) {
+  return guard(ctx, [&] {
+    require(world >= 1 && parts && st, "pcg_dist_check: bad argument");
+    dpcg_check_kernel<<<1, 1, 0, ctx->c.stream>>>(world, parts, st, tol, hist, cap);
+    RDG_LAUNCH_CHECK();
+    ++ctx->c.launches;
+  });
+}
+int rd_gpu_pcg_dist_p(rd_ctx* ctx, int64_t n, const rd_pcg_state* st, const double* z, double* p) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    if (n == 0) return;
+    dpcg_p_kernel<<<vgrid(c, n), 256, 0, c.stream>>>(n, st, z, p);
     RDG_LAUNCH_CHECK();
     ++c.launches;
   });

@@ -124,6 +124,11 @@ class TorchComm:
         self.dist.all_gather_into_tensor(out, t.reshape(1), group=self.group)
         return out.tolist()
 
+    def allgather_into(self, t: torch.Tensor, out: torch.Tensor):
+        """t: 1-element float64 tensor -> out[world] in rank order, on the stream (NCCL for
+        device tensors): the scalar never visits the host."""
+        self.dist.all_gather_into_tensor(out, t.reshape(1), group=self.group)
+
     def link_slabs(self, ops, G):
         """Map the neighbours' slab cell buffers (CUDA IPC over NVLink) for the pipelined hand-off.
 
@@ -222,6 +227,23 @@ class ThreadComm:
 
     def allgather_scalars(self, t: torch.Tensor):
         return self._allgather(float(t.reshape(-1)[0].item()))
+
+    def allgather_into(self, t: torch.Tensor, out: torch.Tensor):
+        """Every rank's scalar into out[world] on this rank's stream (event-ordered copies)."""
+        ev = None
+        if t.is_cuda:
+            # a snapshot: the sender's stream may overwrite t (the next dot) before a
+            # receiver's stream copies it; record_stream keeps the snapshot's block from
+            # being reused until every receiver's copy has run
+            t = t.clone()
+            ev = torch.cuda.Event()
+            ev.record()
+        entries = self._allgather((t, ev))
+        for k, (tk, ek) in enumerate(entries):
+            if ek is not None:
+                torch.cuda.current_stream().wait_event(ek)
+                tk.record_stream(torch.cuda.current_stream())
+            out[k:k + 1].copy_(tk.reshape(1))
 
     def allgather_int(self, v: int):
         return self._allgather(int(v))
@@ -396,6 +418,26 @@ class DeviceOps:
     def coarse(self, level, r, z):
         self.ctx.check(self.rd.lib().rd_gpu_amg_apply_from(self.h.h, int(level), _p(r), _p(z)))
 
+    # -- the PCG scalars on the device (rd_pcg_state, 80 bytes = 10 doubles)
+    def pcg_state(self) -> torch.Tensor:
+        return torch.zeros(10, dtype=torch.float64, device=self.device)
+
+    def pcg_begin(self, parts, st):
+        self.ctx.check(self.rd.lib().rd_gpu_pcg_dist_begin(self.ctx.h, parts.numel(), _p(parts), _p(st)))
+
+    def pcg_alpha(self, parts, st):
+        self.ctx.check(self.rd.lib().rd_gpu_pcg_dist_alpha(self.ctx.h, parts.numel(), _p(parts), _p(st)))
+
+    def pcg_xr(self, st, p, ap, x, r):
+        self.ctx.check(self.rd.lib().rd_gpu_pcg_dist_xr(self.ctx.h, p.numel(), _p(st), _p(p), _p(ap), _p(x), _p(r)))
+
+    def pcg_check(self, parts, st, tol, hist):
+        self.ctx.check(self.rd.lib().rd_gpu_pcg_dist_check(self.ctx.h, parts.numel(), _p(parts), _p(st), float(tol),
+                                                           _p(hist), hist.numel()))
+
+    def pcg_p(self, st, z, p):
+        self.ctx.check(self.rd.lib().rd_gpu_pcg_dist_p(self.ctx.h, p.numel(), _p(st), _p(z), _p(p)))
+
     def set_exact(self, exact: bool):
         self.ctx.check(self.rd.lib().rd_gpu_ctx_set_exact_sweeps(self.ctx.h, 1 if exact else 0))
 
@@ -424,6 +466,15 @@ class _Slab:
         except Exception:
             pass
         self.h = None
+
+
+def _state(st: torch.Tensor) -> dict:
+    """Host copy of an rd_pcg_state (8 doubles, then done / status / iterations as int32)."""
+    a = st.detach().cpu().numpy()
+    iv = a.view(np.int32)
+    return {"rz": float(a[0]), "rz0": float(a[1]), "pap": float(a[2]), "rz_next": float(a[3]),
+            "alpha": float(a[4]), "beta": float(a[5]), "rel": float(a[6]),
+            "done": int(iv[16]), "status": int(iv[17]), "iterations": int(iv[18])}
 
 
 def _p(t):
@@ -519,12 +570,6 @@ class DistSolver:
             if R + 1 < W:
                 ops.append(("recv", R + 1, self.plane(l, v, hi)))
         self.comm.exchange(ops)
-
-    def allsum(self, t):
-        s = 0.0
-        for v in self.comm.allgather_scalars(t):
-            s += v  # rank order: the same bits on every rank
-        return s
 
     # -- smoother
     def sweep(self, l, fwd, f, xin, xout):
@@ -641,47 +686,62 @@ class DistSolver:
         return res
 
     def _pcg(self, tol, max_iter):
-        ops = self.ops
+        """linalg.cpp:64-102 with every scalar on the device: the local dot partials are
+        all-gathered (NCCL) into `parts` and summed in rank order by the state kernels;
+        alpha / beta never leave the device.  The host reads the 80-byte state once per
+        iteration, after the next iteration's halo + A p + x / r update are already queued
+        (no-ops once converged), so the GPU does not idle across the round trip."""
+        ops, comm = self.ops, self.comm
         f = ops.f_local
         x = ops.vec(0)
         r = f.clone()
         z, p, Ap = ops.vec(0), ops.vec(0), ops.vec(0)
         s = ops.scalar()
+        parts = torch.zeros(self.world, dtype=torch.float64, device=s.device)
+        st = ops.pcg_state()
+        hist = torch.zeros(max(max_iter, 1), dtype=torch.float64, device=s.device)
         own = lambda v: self.own(0, v)  # noqa: E731
         out = DistResult(own(x), 0, False, [])
         self.apply(r, z)
         ops.dot(own(r), own(z), s)
-        rz = self.allsum(s)
-        if rz < 0.0:
+        comm.allgather_into(s, parts)
+        ops.pcg_begin(parts, st)
+        hs = _state(st)
+        if hs["status"]:
             raise NotSpdError("pcg: preconditioner not positive definite")
-        rz0 = rz
-        if rz0 == 0.0:
+        if hs["done"]:
             out.converged = True
             return out
         p.copy_(z)
-        for it in range(1, max_iter + 1):
+
+        def ap_xr():
             self.halo(0, p)
             ops.spmv(self.blk("A", 0), p, own(Ap))
             ops.dot(own(p), own(Ap), s)
-            pAp = self.allsum(s)
-            if pAp <= 0.0:
-                raise NotSpdError("pcg: operator not positive definite (p'Ap <= 0)")
-            alpha = rz / pAp
-            ops.xr(alpha, own(p), own(Ap), own(x), own(r))
+            comm.allgather_into(s, parts)
+            ops.pcg_alpha(parts, st)
+            ops.pcg_xr(st, own(p), own(Ap), own(x), own(r))
+
+        if max_iter >= 1:
+            ap_xr()
+        for it in range(1, max_iter + 1):
             self.apply(r, z)
             ops.dot(own(r), own(z), s)
-            rz_next = self.allsum(s)
-            if rz_next < 0.0:
+            comm.allgather_into(s, parts)
+            ops.pcg_check(parts, st, tol, hist)
+            ops.pcg_p(st, own(z), own(p))
+            if it < max_iter:
+                ap_xr()  # the next iteration's first half, queued before the state read
+            hs = _state(st)
+            if hs["status"] == 1:
+                raise NotSpdError("pcg: operator not positive definite (p'Ap <= 0)")
+            if hs["status"]:
                 raise NotSpdError("pcg: preconditioner not positive definite")
-            rel = math.sqrt(rz_next / rz0)
-            out.iterations = it
-            out.residual_history.append(rel)
-            if rel <= tol:
+            out.iterations = hs["iterations"]
+            if hs["done"]:
                 out.converged = True
-                return out
-            beta = rz_next / rz
-            rz = rz_next
-            ops.pupd(beta, own(z), own(p))
+                break
+        out.residual_history = [float(v) for v in hist[: out.iterations].cpu().tolist()]
         return out
 
     def gather_solution(self, x_local: torch.Tensor):

@@ -141,6 +141,11 @@ def lib():
         "rd_gpu_dot_async": (_I, [_P, _I, _P, _P, _P]),
         "rd_gpu_pcg_update_xr": (_I, [_P, C.c_int64, _D, _P, _P, _P, _P]),
         "rd_gpu_pcg_update_p": (_I, [_P, C.c_int64, _D, _P, _P]),
+        "rd_gpu_pcg_dist_begin": (_I, [_P, _I, _P, _P]),
+        "rd_gpu_pcg_dist_alpha": (_I, [_P, _I, _P, _P]),
+        "rd_gpu_pcg_dist_xr": (_I, [_P, C.c_int64, _P, _P, _P, _P, _P]),
+        "rd_gpu_pcg_dist_check": (_I, [_P, _I, _P, _P, _D, _P, _I]),
+        "rd_gpu_pcg_dist_p": (_I, [_P, C.c_int64, _P, _P, _P]),
         "rd_gpu_amg_apply_from": (_I, [_P, _I, _P, _P]),
         "rd_gpu_slab_create": (_I, [_P, _P, _I, _I, C.POINTER(_P)]),
         "rd_gpu_slab_free": (None, [_P]),

@@ -135,6 +135,76 @@ class HostOps:
     def coarse(self, level, r, z):
         z.numpy()[:] = self.h.apply_from(level, r.numpy())
 
+    # -- rd_pcg_state on the host: same layout and arithmetic as dist.cu's dpcg_* kernels
+    def pcg_state(self):
+        return torch.zeros(10, dtype=torch.float64)
+
+    @staticmethod
+    def _st(st):
+        a = st.numpy()
+        return a, a.view(np.int32)
+
+    @staticmethod
+    def _rank_sum(parts):
+        s = 0.0
+        for v in parts.numpy().tolist():
+            s = s + v
+        return s
+
+    def pcg_begin(self, parts, st):
+        a, iv = self._st(st)
+        rz = self._rank_sum(parts)
+        a[0] = a[1] = rz
+        iv[16] = iv[17] = iv[18] = 0
+        if rz < 0.0:
+            iv[17] = 2
+        elif rz == 0.0:
+            iv[16] = 1
+
+    def pcg_alpha(self, parts, st):
+        a, iv = self._st(st)
+        if iv[16] or iv[17]:
+            return
+        pap = self._rank_sum(parts)
+        a[2] = pap
+        if not pap > 0.0:
+            iv[17] = 1
+            return
+        a[4] = a[0] / pap
+
+    def pcg_xr(self, st, p, ap, x, r):
+        a, iv = self._st(st)
+        if iv[16] or iv[17]:
+            return
+        self.xr(float(a[4]), p, ap, x, r)
+
+    def pcg_check(self, parts, st, tol, hist):
+        a, iv = self._st(st)
+        if iv[16] or iv[17]:
+            return
+        rzn = self._rank_sum(parts)
+        a[3] = rzn
+        if rzn < 0.0:
+            iv[17] = 2
+            return
+        rel = float(np.sqrt(np.float64(rzn) / np.float64(a[1])))
+        it = int(iv[18]) + 1
+        iv[18] = it
+        a[6] = rel
+        if it - 1 < hist.numel():
+            hist[it - 1] = rel
+        if rel <= tol:
+            iv[16] = 1
+            return
+        a[5] = rzn / a[0]
+        a[0] = rzn
+
+    def pcg_p(self, st, z, p):
+        a, iv = self._st(st)
+        if iv[16] or iv[17]:
+            return
+        self.pupd(float(a[5]), z, p)
+
     def set_exact(self, exact):
         pass
 
