@@ -160,6 +160,36 @@ typedef struct {
 int rd_gpu_pcg(rd_ctx* ctx, const rd_csr* a, rd_amg* amg, const double* f, double tol, int max_iter,
                double* x, rd_pcg_report* report, double* residual_history);
 
+/* ------------------------------------------------------------ LinOp (linalg.hpp:11) */
+/* rd::LinOp = std::function<Vec(const Vec&)>: a fixed linear map.  Here y = op(x) on DEVICE
+ * vectors of n doubles, enqueued on the context's stream (rd_gpu_ctx_stream); x and y never
+ * alias.  The callback returns RD_OK or an RD_E* code, which the caller propagates.  Built-in
+ * operators are recognised by rd_gpu_pcg_linop and run fused (no callback round trip). */
+typedef int (*rd_linop_fn)(void* user, rd_ctx* ctx, int64_t n, const double* x, double* y);
+typedef struct {
+  rd_linop_fn apply;
+  void* user;
+} rd_linop;
+typedef struct rd_jacobi rd_jacobi;
+/* identity_precond()                                     linalg.hpp:39, linalg.cpp:53-55 */
+int rd_gpu_linop_identity(rd_linop* out);
+/* [&A](x) { return spmv(A, x); }                         linalg.cpp:104-106 (borrows a) */
+int rd_gpu_linop_csr(const rd_csr* a, rd_linop* out);
+/* amg_precond(h)                                         amg.hpp:42, amg.cpp:143-145 (borrows h) */
+int rd_gpu_linop_amg(rd_amg* h, rd_linop* out);
+/* jacobi_precond(A): d = diag(A), RD_ENOTSPD ("non-positive diagonal") when some d_i <= 0,
+ * apply r ./ d                                           linalg.hpp:40, linalg.cpp:57-62 */
+int rd_gpu_jacobi_create(rd_ctx* ctx, const rd_csr* a, rd_jacobi** out);
+void rd_gpu_jacobi_free(rd_jacobi* j);
+int rd_gpu_linop_jacobi(rd_jacobi* j, rd_linop* out);
+/* y = op(x), host or device vectors, synchronous */
+int rd_gpu_linop_apply(rd_ctx* ctx, rd_linop op, int64_t n, const double* x, double* y);
+/* replaces rd::pcg(apply_A, apply_P, f, tol, max_iter)   linalg.hpp:46-47, linalg.cpp:64-102
+ * (and pcg(A, apply_P, ...) with apply_A = rd_gpu_linop_csr(A), linalg.cpp:104-106).
+ * f / x host or device; residual_history host (>= max_iter doubles) or NULL. */
+int rd_gpu_pcg_linop(rd_ctx* ctx, int64_t n, rd_linop apply_a, rd_linop apply_p, const double* f, double tol,
+                     int max_iter, double* x, rd_pcg_report* report, double* residual_history);
+
 /* replaces rd::solve_system(mesh, sys, PrecondKind::amg, p, tol)  bench.hpp:48-57, bench.cpp:185-225:
  * build_amg(A) [setup_seconds], pcg(A, amg, f, tol, 500) [solve_seconds]. */
 typedef struct {

@@ -136,6 +136,80 @@ void require(bool ok, const char* msg) {
 
 }  // namespace
 
+struct rd_jacobi {
+  rd_ctx* ctx = nullptr;
+  DBuf<double> d;
+  int64_t n = 0;
+};
+
+namespace {
+
+// built-in LinOps (linalg.cpp:53-62, 104-106; amg.cpp:143-145): y = op(x) on ctx's stream
+int linop_identity_fn(void*, rd_ctx* ctx, int64_t n, const double* x, double* y) {
+  return guard(ctx, [&] {
+    if (n) RDG_CUDA(cudaMemcpyAsync(y, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->c.stream));
+  });
+}
+int linop_csr_fn(void* u, rd_ctx* ctx, int64_t n, const double* x, double* y) {
+  const rd_csr* a = static_cast<const rd_csr*>(u);
+  return guard(ctx, [&] {
+    require(n == a->a->rows && a->a->rows == a->a->cols, "spmv: dimension mismatch");
+    spmv(ctx->c, *a->a, x, y);
+  });
+}
+int linop_amg_fn(void* u, rd_ctx* ctx, int64_t n, const double* x, double* y) {
+  rd_amg* h = static_cast<rd_amg*>(u);
+  return guard(ctx, [&] {
+    require(!h->h.levels.empty() && n == h->h.levels[0].A.rows, "amg_apply: dimension mismatch");
+    vcycle(ctx->c, h->h, x, y, nullptr);
+  });
+}
+int linop_jacobi_fn(void* u, rd_ctx* ctx, int64_t n, const double* x, double* y) {
+  rd_jacobi* j = static_cast<rd_jacobi*>(u);
+  return guard(ctx, [&] {
+    require(n == j->n, "jacobi_precond: dimension mismatch");
+    jacobi_apply(ctx->c, n, j->d.p, x, y);
+  });
+}
+
+// a LinOp as an operator of the PCG loop (out = op(in), *dot = in . out); built-ins run
+// directly (the AMG V-cycle fuses its dot into the last sweep), callbacks through their ABI
+PcgOp pcg_op(rd_ctx* ctx, const rd_linop& op, int64_t n, const DCsr* level0) {
+  Ctx& c = ctx->c;
+  if (op.apply == linop_csr_fn) {
+    const DCsr* A = static_cast<const rd_csr*>(op.user)->a;
+    require(A->rows == n && A->cols == n, "pcg: operator dimension mismatch");
+    // the hierarchy's level 0 views A's arrays (its stencil facts feed the lattice SpMV)
+    if (level0 && level0->v.p == A->v.p && level0->rp.p == A->rp.p && level0->rows == A->rows) A = level0;
+    return [&c, A](const double* x, double* y, double* d) { spmv_dot(c, *A, x, y, d); };
+  }
+  if (op.apply == linop_amg_fn) {
+    Hierarchy* h = &static_cast<rd_amg*>(op.user)->h;
+    require(!h->levels.empty() && h->levels[0].A.rows == n, "amg_apply: dimension mismatch");
+    return [&c, h](const double* x, double* y, double* d) { vcycle(c, *h, x, y, d); };
+  }
+  if (op.apply == linop_jacobi_fn) {
+    rd_jacobi* j = static_cast<rd_jacobi*>(op.user);
+    require(j->n == n, "jacobi_precond: dimension mismatch");
+    return [&c, j, n](const double* x, double* y, double* d) {
+      jacobi_apply(c, n, j->d.p, x, y);
+      dot(c, n, x, y, d);
+    };
+  }
+  require(op.apply != nullptr, "pcg: null operator");
+  return [ctx, op, n](const double* x, double* y, double* d) {
+    ctx->c.err.clear();
+    const int rc = op.apply(op.user, ctx, n, x, y);
+    if (rc != RD_OK) {
+      const std::string msg = ctx->c.err.empty() ? "operator callback failed" : ctx->c.err;
+      throw Error(rc, msg.c_str());
+    }
+    dot(ctx->c, n, x, y, d);
+  };
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* rd_gpu_version(void) { return "rd_gpu 0.1 (sm_100a)"; }
@@ -516,6 +590,98 @@ int rd_gpu_pcg(rd_ctx* ctx, const rd_csr* a, rd_amg* amg, const double* f, doubl
     PcgResultDev r;
     exact_retry(c, [&] {
       r = pcg_device(c, A, amg ? &amg->h : nullptr, fd, tol, max_iter, xo.dev(), hd.p);
+      xo.finish();
+      if (hist && r.iterations > 0)
+        RDG_CUDA(cudaMemcpyAsync(hist, hd.p, sizeof(double) * r.iterations, cudaMemcpyDefault, c.stream));
+      sync_and_raise(c);
+    });
+    if (rep) {
+      rep->iterations = r.iterations;
+      rep->converged = r.converged ? 1 : 0;
+    }
+  });
+}
+
+// ------------------------------------------------------------ LinOp (linalg.hpp:11)
+int rd_gpu_linop_identity(rd_linop* out) {
+  if (!out) return RD_EINVAL;
+  *out = rd_linop{linop_identity_fn, nullptr};
+  return RD_OK;
+}
+int rd_gpu_linop_csr(const rd_csr* a, rd_linop* out) {
+  if (!a || !out) return RD_EINVAL;
+  *out = rd_linop{linop_csr_fn, const_cast<rd_csr*>(a)};
+  return RD_OK;
+}
+int rd_gpu_linop_amg(rd_amg* h, rd_linop* out) {
+  if (!h || !out) return RD_EINVAL;
+  *out = rd_linop{linop_amg_fn, h};
+  return RD_OK;
+}
+int rd_gpu_jacobi_create(rd_ctx* ctx, const rd_csr* a, rd_jacobi** out) {
+  return guard(ctx, [&] {
+    require(a && out, "jacobi_precond: null argument");
+    Ctx& c = ctx->c;
+    const DCsr& A = *a->a;
+    auto j = std::make_unique<rd_jacobi>();
+    j->ctx = ctx;
+    j->n = A.rows;
+    j->d.alloc(std::max(A.rows, 1), c.stream);
+    DBuf<int> bad(1, c.stream);
+    RDG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
+    csr_diagonal(c, A, j->d.p, bad.p);
+    int hb = 0;
+    RDG_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    if (hb) throw Error(RD_ENOTSPD, "jacobi_precond: non-positive diagonal");
+    *out = j.release();
+  });
+}
+void rd_gpu_jacobi_free(rd_jacobi* j) {
+  if (!j) return;
+  cudaStreamSynchronize(j->ctx->c.stream);
+  PoolScope ps(j->ctx->c.pool);
+  delete j;
+}
+int rd_gpu_linop_jacobi(rd_jacobi* j, rd_linop* out) {
+  if (!j || !out) return RD_EINVAL;
+  *out = rd_linop{linop_jacobi_fn, j};
+  return RD_OK;
+}
+int rd_gpu_linop_apply(rd_ctx* ctx, rd_linop op, int64_t n, const double* x, double* y) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    require(op.apply != nullptr && n >= 0, "linop_apply: bad argument");
+    DBuf<double> tx;
+    const double* xd = in_dev(c, x, n, tx);
+    OutVec<double> yo(c, y, n);
+    exact_retry(c, [&] {
+      if (n) {
+        c.err.clear();
+        const int rc = op.apply(op.user, ctx, n, xd, yo.dev());
+        if (rc != RD_OK) throw Error(rc, c.err.empty() ? "operator callback failed" : c.err.c_str());
+      }
+      yo.finish();
+      sync_and_raise(c);
+    });
+  });
+}
+int rd_gpu_pcg_linop(rd_ctx* ctx, int64_t n, rd_linop apply_a, rd_linop apply_p, const double* f, double tol,
+                     int max_iter, double* x, rd_pcg_report* rep, double* hist) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    require(n >= 0 && n <= INT32_MAX, "pcg: bad dimension");
+    const DCsr* level0 = apply_p.apply == linop_amg_fn && !static_cast<rd_amg*>(apply_p.user)->h.levels.empty()
+                             ? &static_cast<rd_amg*>(apply_p.user)->h.levels[0].A
+                             : nullptr;
+    const PcgOp A = pcg_op(ctx, apply_a, n, level0);
+    const PcgOp P = pcg_op(ctx, apply_p, n, nullptr);
+    DBuf<double> tf, hd(std::max(max_iter, 1), c.stream);
+    const double* fd = in_dev(c, f, n, tf);
+    OutVec<double> xo(c, x, n);
+    PcgResultDev r;
+    exact_retry(c, [&] {
+      r = pcg_ops(c, n, A, P, fd, tol, max_iter, xo.dev(), hd.p);
       xo.finish();
       if (hist && r.iterations > 0)
         RDG_CUDA(cudaMemcpyAsync(hist, hd.p, sizeof(double) * r.iterations, cudaMemcpyDefault, c.stream));

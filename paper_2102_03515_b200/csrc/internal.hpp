@@ -2,6 +2,7 @@
 // host-callable entry points shared between translation units.
 #pragma once
 
+#include <functional>
 #include <memory>
 
 #include "common.cuh"
@@ -62,6 +63,9 @@ void residual(Ctx& c, const DCsr& A, const double* r, const double* z, double* r
 // z += P zc
 void prolong_add(Ctx& c, const DCsr& P, const double* zc, double* z);
 void dot(Ctx& c, int64_t n, const double* a, const double* b, double* out_dev);
+// jacobi_precond (linalg.cpp:57-62): d = diag(A) (0 where absent), *bad_dev = 1 if some d_i <= 0
+void csr_diagonal(Ctx& c, const DCsr& A, double* d, int* bad_dev);
+void jacobi_apply(Ctx& c, int64_t n, const double* d, const double* r, double* z);  // z = r ./ d
 DCsr transpose(Ctx& c, const DCsr& A);
 DCsr spgemm(Ctx& c, const DCsr& A, const DCsr& B);  // Eigen conservative product order
 DCsr prune_zeros(Ctx& c, const DCsr& A);
@@ -159,6 +163,11 @@ struct PcgResultDev {
   int iterations = 0;
   bool converged = false;
 };
+// An operator of the PCG loop: out = op(in) and *dot_out = in . out (device pointers, stream-ordered).
+using PcgOp = std::function<void(const double* in, double* out, double* dot_out)>;
+// linalg.cpp:64-102 over any pair of operators (rd_gpu_pcg_linop)
+PcgResultDev pcg_ops(Ctx& c, int64_t n, const PcgOp& apply_A, const PcgOp& apply_P, const double* f, double tol,
+                     int max_iter, double* x, double* hist_dev);
 // x (device, n) receives the solution; hist_dev (device, >= max_iter) may be null.
 PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, double tol, int max_iter, double* x,
                         double* hist_dev);

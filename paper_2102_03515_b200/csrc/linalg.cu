@@ -445,6 +445,43 @@ void dot(Ctx& c, int64_t n, const double* a, const double* b, double* out_dev) {
   ++c.launches;
 }
 
+// ============================================================== Jacobi (linalg.cpp:57-62)
+namespace {
+// d_i = A(i,i) (0 when the row stores no diagonal, like Eigen's diagonal()); bad = 1 if some d_i <= 0
+__global__ void csr_diag_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                const double* __restrict__ v, double* __restrict__ d, int* bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double di = 0.0;
+  for (int k = rp[i]; k < rp[i + 1]; ++k)
+    if (ci[k] == i) {
+      di = v[k];
+      break;
+    }
+  d[i] = di;
+  if (di <= 0.0) *bad = 1;
+}
+__global__ void jacobi_kernel(int64_t n, const double* __restrict__ d, const double* __restrict__ r,
+                              double* __restrict__ z) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = __ddiv_rn(r[i], d[i]);
+}
+}  // namespace
+
+void csr_diagonal(Ctx& c, const DCsr& A, double* d, int* bad_dev) {
+  if (A.rows == 0) return;
+  csr_diag_kernel<<<div_up(A.rows, 256), 256, 0, c.stream>>>(A.rows, A.rp.p, A.ci.p, A.v.p, d, bad_dev);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+}
+void jacobi_apply(Ctx& c, int64_t n, const double* d, const double* r, double* z) {
+  if (n == 0) return;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * 8, (n + 255) / 256));
+  jacobi_kernel<<<g, 256, 0, c.stream>>>(n, d, r, z);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+}
+
 // ============================================================== structure ops
 namespace {
 __global__ void count_cols_kernel(int64_t nnz, const int* __restrict__ ci, int* cnt) {

@@ -85,9 +85,8 @@ int vec_grid(Ctx& c, int64_t n) {
 
 }  // namespace
 
-PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, double tol, int max_iter, double* x,
-                        double* hist_dev) {
-  const int64_t n = A.rows;
+PcgResultDev pcg_ops(Ctx& c, int64_t n, const PcgOp& apply_A, const PcgOp& apply_P, const double* f, double tol,
+                     int max_iter, double* x, double* hist_dev) {
   PcgResultDev out;
   if (n == 0) {
     out.converged = true;
@@ -98,14 +97,7 @@ PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, do
   RDG_CUDA(cudaMemsetAsync(st.p, 0, sizeof(PcgState), c.stream));
   RDG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c.stream));
   RDG_CUDA(cudaMemcpyAsync(r.p, f, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
-  auto precond = [&](double* dot_out) {
-    if (h) {
-      vcycle(c, *h, r.p, z.p, dot_out);
-    } else {
-      RDG_CUDA(cudaMemcpyAsync(z.p, r.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
-      dot(c, n, r.p, z.p, dot_out);
-    }
-  };
+  auto precond = [&](double* dot_out) { apply_P(r.p, z.p, dot_out); };
   precond(&st.p->rz);
   pcg_init_kernel<<<1, 1, 0, c.stream>>>(st.p);
   RDG_LAUNCH_CHECK();
@@ -120,16 +112,11 @@ PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, do
   }
   RDG_CUDA(cudaMemcpyAsync(p.p, z.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
   const int g = vec_grid(c, n);
-  // the hierarchy's level 0 views A's arrays (its stencil facts feed the lattice SpMV)
-  const DCsr& As = (h && !h->levels.empty() && h->levels[0].A.v.p == A.v.p && h->levels[0].A.rp.p == A.rp.p &&
-                    h->levels[0].A.rows == A.rows)
-                       ? h->levels[0].A
-                       : A;
   // A p and the x / r update of iteration it are enqueued before the host waits on the
   // convergence check of iteration it - 1, so the GPU never idles across that round trip;
   // once converged they are no-ops (pcg_xr_kernel reads st->done; Ap and pAp are scratch)
   auto enqueue_ap_xr = [&]() {
-    spmv_dot(c, As, p.p, Ap.p, &st.p->pAp);
+    apply_A(p.p, Ap.p, &st.p->pAp);
     pcg_xr_kernel<<<g, 256, 0, c.stream>>>(n, st.p, p.p, Ap.p, x, r.p);
     RDG_LAUNCH_CHECK();
     ++c.launches;
@@ -162,6 +149,26 @@ PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, do
     }
   }
   return out;
+}
+
+PcgResultDev pcg_device(Ctx& c, const DCsr& A, Hierarchy* h, const double* f, double tol, int max_iter, double* x,
+                        double* hist_dev) {
+  // the hierarchy's level 0 views A's arrays (its stencil facts feed the lattice SpMV)
+  const DCsr& As = (h && !h->levels.empty() && h->levels[0].A.v.p == A.v.p && h->levels[0].A.rp.p == A.rp.p &&
+                    h->levels[0].A.rows == A.rows)
+                       ? h->levels[0].A
+                       : A;
+  const int64_t n = A.rows;
+  const PcgOp apply_A = [&](const double* p, double* Ap, double* pAp) { spmv_dot(c, As, p, Ap, pAp); };
+  const PcgOp apply_P = [&](const double* r, double* z, double* rz) {
+    if (h) {
+      vcycle(c, *h, r, z, rz);
+    } else {
+      RDG_CUDA(cudaMemcpyAsync(z, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+      dot(c, n, r, z, rz);
+    }
+  };
+  return pcg_ops(c, n, apply_A, apply_P, f, tol, max_iter, x, hist_dev);
 }
 
 }  // namespace rdg

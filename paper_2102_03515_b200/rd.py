@@ -141,6 +141,14 @@ def lib():
         "rd_gpu_dot_async": (_I, [_P, _I, _P, _P, _P]),
         "rd_gpu_pcg_update_xr": (_I, [_P, C.c_int64, _D, _P, _P, _P, _P]),
         "rd_gpu_pcg_update_p": (_I, [_P, C.c_int64, _D, _P, _P]),
+        "rd_gpu_linop_identity": (_I, [_P]),
+        "rd_gpu_linop_csr": (_I, [_P, _P]),
+        "rd_gpu_linop_amg": (_I, [_P, _P]),
+        "rd_gpu_jacobi_create": (_I, [_P, _P, _P]),
+        "rd_gpu_jacobi_free": (None, [_P]),
+        "rd_gpu_linop_jacobi": (_I, [_P, _P]),
+        "rd_gpu_linop_apply": (_I, [_P, _LinOp, C.c_int64, _P, _P]),
+        "rd_gpu_pcg_linop": (_I, [_P, C.c_int64, _LinOp, _LinOp, _P, _D, _I, _P, _P, _P]),
         "rd_gpu_pcg_dist_begin": (_I, [_P, _I, _P, _P]),
         "rd_gpu_pcg_dist_alpha": (_I, [_P, _I, _P, _P]),
         "rd_gpu_pcg_dist_xr": (_I, [_P, C.c_int64, _P, _P, _P, _P, _P]),
@@ -167,6 +175,14 @@ def lib():
 
 class _PcgReport(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int)]
+
+
+# rd_linop (include/rd_gpu.h): y = op(x) on device vectors, on the context's stream
+_LINOP_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
+class _LinOp(C.Structure):
+    _fields_ = [("apply", _LINOP_FN), ("user", C.c_void_p)]
 
 
 class _SolveOutcome(C.Structure):
@@ -595,8 +611,12 @@ class PcgResult:
 
 def pcg(A: Csr, precond="amg", f=None, tol: float = 1e-8, max_iter: int = 500,
         hierarchy: AmgHierarchy | None = None) -> PcgResult:
-    """linalg.hpp:46-49 with amg_precond(h) (or the identity)."""
+    """linalg.hpp:46-49 with amg_precond(h), the identity, Jacobi, or any LinOp."""
     f = np.ascontiguousarray(f, np.float64)
+    if isinstance(precond, LinOp):
+        return pcg_linop(A, precond, f, tol, max_iter)
+    if precond == "jacobi":
+        return pcg_linop(A, jacobi_precond(A), f, tol, max_iter)
     if precond == "amg" and hierarchy is None:
         hierarchy = build_amg(A)
     if precond not in ("amg", "identity"):
@@ -607,6 +627,131 @@ def pcg(A: Csr, precond="amg", f=None, tol: float = 1e-8, max_iter: int = 500,
     A.ctx.check(lib().rd_gpu_pcg(A.ctx.h, A.h, hierarchy.h if precond == "amg" else None, _ptr(f), float(tol),
                                  int(max_iter), _ptr(x), C.byref(rep), _ptr(hist)))
     return PcgResult(x[: A.rows], rep.iterations, bool(rep.converged), hist[: rep.iterations].copy())
+
+
+# ------------------------------------------------------------------ LinOp (linalg.hpp:11)
+class LinOp:
+    """rd::LinOp: a fixed linear map y = op(x), applied on the device (rd_linop).  Built-ins come
+    from identity_precond / spmv_op / amg_precond / jacobi_precond; `LinOp.from_device_fn(fn, n)`
+    wraps a Python callable fn(x, y) on device tensors (torch, on the current stream)."""
+
+    def __init__(self, st: _LinOp, keep=()):
+        self._st = st
+        self._keep = keep  # objects the operator borrows (matrix, hierarchy, callback)
+
+    def __call__(self, x, ctx: "Context | None" = None):
+        """y = op(x): host array in -> host array out (device tensors are used in place)."""
+        ctx = ctx or self._ctx()
+        if isinstance(x, np.ndarray) or not hasattr(x, "data_ptr"):
+            x = np.ascontiguousarray(x, np.float64)
+            y = np.zeros(max(x.size, 1))
+            ctx.check(lib().rd_gpu_linop_apply(ctx.h, self._st, x.size, _ptr(x), _ptr(y)))
+            return y[: x.size]
+        y = x.new_empty(x.shape)
+        ctx.check(lib().rd_gpu_linop_apply(ctx.h, self._st, x.numel(), _ptr(x), _ptr(y)))
+        return y
+
+    def _ctx(self):
+        for k in self._keep:
+            if hasattr(k, "ctx"):
+                return k.ctx
+        return default_context()
+
+    @staticmethod
+    def from_device_fn(fn, ctx: "Context | None" = None) -> "LinOp":
+        """fn(x, y): torch float64 device tensors of n entries; write y = op(x) on the current
+        stream (the context's stream is made current around the call)."""
+        import torch
+
+        ctx = ctx or default_context()
+
+        def tramp(user, hctx, n, x, y):
+            try:
+                s = torch.cuda.ExternalStream(lib().rd_gpu_ctx_stream(ctx.h) or 0)
+                with torch.cuda.stream(s):
+                    xt = _device_view(x, n)
+                    yt = _device_view(y, n)
+                    fn(xt, yt)
+                return RD_OK
+            except Exception:  # noqa: BLE001 - an exception cannot cross the C frame
+                return RD_ERUNTIME
+
+        cb = _LINOP_FN(tramp)
+        op = LinOp(_LinOp(cb, None), keep=(cb, ctx))
+        return op
+
+
+def _device_view(ptr, n):
+    """A float64 torch tensor over n doubles of device memory at ptr (no copy)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr or 0), False),
+                                    "version": 2}
+
+    return torch.as_tensor(_Arr(), device="cuda")
+
+
+def identity_precond() -> LinOp:
+    """linalg.hpp:39 identity_precond()."""
+    st = _LinOp()
+    lib().rd_gpu_linop_identity(C.byref(st))
+    return LinOp(st)
+
+
+def spmv_op(A: Csr) -> LinOp:
+    """[&A](x) { return spmv(A, x); } (linalg.cpp:104-106)."""
+    st = _LinOp()
+    A.ctx.check(lib().rd_gpu_linop_csr(A.h, C.byref(st)))
+    return LinOp(st, keep=(A,))
+
+
+def amg_precond(h: "AmgHierarchy") -> LinOp:
+    """amg.hpp:42 amg_precond(h): one V-cycle per application."""
+    st = _LinOp()
+    h.ctx.check(lib().rd_gpu_linop_amg(h.h, C.byref(st)))
+    return LinOp(st, keep=(h,))
+
+
+class _Jacobi:
+    def __init__(self, A: Csr):
+        self.ctx = A.ctx
+        h = _P()
+        self.ctx.check(lib().rd_gpu_jacobi_create(self.ctx.h, A.h, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and not _closing:
+                lib().rd_gpu_jacobi_free(self.h)
+        except Exception:
+            pass
+        self.h = None
+
+
+def jacobi_precond(A: Csr) -> LinOp:
+    """linalg.hpp:40 jacobi_precond(A): r ./ diag(A); RdNotSpdError on a non-positive diagonal."""
+    j = _Jacobi(A)
+    st = _LinOp()
+    A.ctx.check(lib().rd_gpu_linop_jacobi(j.h, C.byref(st)))
+    return LinOp(st, keep=(j, A))
+
+
+def pcg_linop(apply_A, apply_P: LinOp, f, tol: float = 1e-8, max_iter: int = 500,
+              ctx: "Context | None" = None) -> PcgResult:
+    """linalg.hpp:46-49 pcg(apply_A, apply_P, f, tol, max_iter); apply_A may be a Csr (the SpMat
+    overload).  f: host array (x returned on the host)."""
+    if isinstance(apply_A, Csr):
+        apply_A = spmv_op(apply_A)
+    ctx = ctx or apply_A._ctx()
+    f = np.ascontiguousarray(f, np.float64)
+    n = f.size
+    x = np.zeros(max(n, 1))
+    hist = np.zeros(max(max_iter, 1))
+    rep = _PcgReport()
+    ctx.check(lib().rd_gpu_pcg_linop(ctx.h, n, apply_A._st, apply_P._st, _ptr(f), float(tol), int(max_iter), _ptr(x),
+                                     C.byref(rep), _ptr(hist)))
+    return PcgResult(x[:n], rep.iterations, bool(rep.converged), hist[: rep.iterations].copy())
 
 
 @dataclass
