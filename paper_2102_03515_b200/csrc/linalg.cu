@@ -234,114 +234,162 @@ __global__ void __launch_bounds__(kSpmvNT) spmv_staged_kernel(int rows, const in
 }
 
 // SpMV on a lattice level whose rows are known on chip (smoother_lattice.cu's checks):
-// uniform (tab = the 15-slot row) or class-uniform (tab = 64 class rows).  One block
-// per x-line, threads along x (coalesced neighbour reads); the row sum from +0 in slot
-// = ascending column order, absent slots adding +0 * x_i (exact: a running sum that
-// starts at +0 is never -0).  Reads x and writes y only: the CSR stays untouched.
-template <int MODE, bool CLS>
-__global__ void __launch_bounds__(128) stencil_spmv_kernel(int L, const double* __restrict__ tab,
-                                                           const double* __restrict__ x, double* __restrict__ y,
-                                                           const double* __restrict__ r) {
-  __shared__ __align__(16) double st[CLS ? 64 * 16 : 16];
-  for (int k = threadIdx.x; k < (CLS ? 64 * 16 : 16); k += blockDim.x) st[k] = __ldg(tab + k);
-  __syncthreads();
-  const int line = blockIdx.x;
-  const int yy = line % L, zz = line / L;
-  const long long P = (long long)L * L;
-  const bool ym = yy > 0, yp = yy < L - 1, zm = zz > 0, zp = zz < L - 1;
-  const int cyz = pos_class(yy, L) * 4 + pos_class(zz, L);
-  const long long off[15] = {-1 - L - P, -L - P, -1 - P, -P, -1 - L, -L, -1, 0, 1, L, 1 + L, P, 1 + P, L + P, 1 + L + P};
-  for (int a = threadIdx.x; a < L; a += blockDim.x) {
-    const long long i = (long long)line * L + a;
-    const bool am = a > 0, ap = a < L - 1;
-    const bool pr[15] = {am && ym && zm, ym && zm, am && zm, zm, am && ym, ym, am, true,
-                         ap, yp, ap && yp, zp, ap && zp, yp && zp, ap && yp && zp};
-    const double* v = CLS ? st + (pos_class(a, L) * 16 + cyz) * 16 : st;
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < 15; ++k) {
-      const double vk = pr[k] ? v[k] : 0.0;
-      acc = __dadd_rn(acc, __dmul_rn(vk, x[pr[k] ? i + off[k] : i]));
-    }
-    y[i] = MODE == kResidual ? __dsub_rn(r[i], acc) : acc;
-  }
+// uniform (tab = the 15-slot row) or class-uniform (tab = 64 class rows).  2.5-D blocked: a
+// block owns a 32 (x) x 16 (y) column of rows, two rows per thread, and marches up 4-16 planes
+// in z.  The x values of each plane (with a one-line halo in x and y, zero outside the box)
+// arrive by cp.async in a kStNR-plane shared-memory ring, kStD planes ahead of the plane being
+// summed (the residual's r rides in the same copy groups), so several planes per block are in
+// flight.  A row reads 7 of its 15 neighbours from shared memory per plane: the plane-(z+1)
+// values it read as "above" are its "centre" values at z+1, and its centre-plane values are
+// its "below" values at z+1, carried in registers.  Each x value is read from L2 / HBM about
+// 1.3 times.  A row sums its 15 slots from +0 in ascending column order; absent slots read
+// x = +0 (finite coefficient * +0 = +-0, and a running sum from +0 never becomes -0), so the
+// result is the CSR row sum bit for bit.  kDot adds p . (A p) with a fixed-order block
+// reduction (deterministic, independent of block completion order).
+constexpr int kStTX = 32, kStTY = 16, kStNR = 8, kStD = 5;
+constexpr int kStNT = 256, kStRows = kStTX * kStTY / kStNT;  // 2 rows per thread (y and y + 8)
+constexpr int kStPX = kStTX + 2, kStPY = kStTY + 2, kStPlane = kStPX * kStPY;
+constexpr int kStE = (kStPlane + kStNT - 1) / kStNT;  // staging elements per thread
+static_assert(kStNR >= kStD + 3, "a ring slot is refilled only after every thread left the planes it held");
+static_assert(kStRows == 2, "two rows per thread");
+static_assert((kStNR & (kStNR - 1)) == 0, "ring index by mask");
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
 }
 
-// The same product, 2.5-D blocked: a block owns a 32 (x) x 8 (y) column of rows and marches
-// up ZC planes in z, the x values of planes z-1 .. z+2 (with a one-line halo in x and y,
-// zero outside the box) staged in a 4-plane shared-memory ring, so each x value is read
-// from L2 / HBM about once instead of nine times (one line per block above).  A row sums
-// its 15 slots from +0 in ascending column order; absent slots read x = +0 (finite coefficient
-// * +0 = +-0, and a running sum from +0 never becomes -0), so the result is the CSR row sum.
-constexpr int kStTX = 32, kStTY = 8, kStZC = 8;
-constexpr int kStPX = kStTX + 2, kStPY = kStTY + 2, kStPlane = kStPX * kStPY;
 template <int MODE, bool CLS>
-__global__ void __launch_bounds__(kStTX* kStTY) stencil_spmv_tiled_kernel(int L, const double* __restrict__ tab,
-                                                                         const double* __restrict__ x,
-                                                                         double* __restrict__ y,
-                                                                         const double* __restrict__ r) {
+__global__ void __launch_bounds__(kStNT) stencil_spmv_tiled_kernel(int L, int gx, int gy, int zc, const double* __restrict__ tab,
+                                                                  const double* __restrict__ x,
+                                                                  double* __restrict__ y,
+                                                                  const double* __restrict__ r, double* partials,
+                                                                  unsigned* counter, double* dot_out) {
   __shared__ __align__(16) double st[CLS ? 64 * 16 : 16];
-  __shared__ double pl[4][kStPlane];
+  // dynamic: the x ring [kStNR][kStPlane], then (residual) the r ring [kStNR][kStRows * kStNT]
+  extern __shared__ __align__(16) double st_dyn[];
+  double(*pl)[kStPlane] = reinterpret_cast<double(*)[kStPlane]>(st_dyn);
+  double(*rr)[kStRows * kStNT] = reinterpret_cast<double(*)[kStRows * kStNT]>(st_dyn + kStNR * kStPlane);
+  __shared__ double red[kStNT / 32];
   const int tid = threadIdx.x, tx = tid % kStTX, ty = tid / kStTX;
-  for (int k = tid; k < (CLS ? 64 * 16 : 16); k += kStTX * kStTY) st[k] = __ldg(tab + k);
-  const int a0 = blockIdx.x * kStTX, y0 = blockIdx.y * kStTY, z0 = blockIdx.z * kStZC;
-  const int z1 = min(z0 + kStZC, L);
+  for (int k = tid; k < (CLS ? 64 * 16 : 16); k += kStNT) st[k] = __ldg(tab + k);
+  const int b = blockIdx.x;
+  const int a0 = (b % gx) * kStTX, y0 = ((b / gx) % gy) * kStTY, z0 = (b / (gx * gy)) * zc;
+  const int z1 = min(z0 + zc, L);
   const long long P = (long long)L * L;
-  // this thread's staging elements of a plane (kStPlane = 340 <= 2 * 256)
-  auto stage = [&](int z, double (&v)[2]) {
+  const int a = a0 + tx;
+  int yy[kStRows];
+  bool valid[kStRows];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int e = tid + q * kStTX * kStTY;
-      v[q] = 0.0;
-      if (e < kStPlane) {
-        const int aa = a0 - 1 + e % kStPX, yy = y0 - 1 + e / kStPX;
-        if (z >= 0 && z < L && aa >= 0 && aa < L && yy >= 0 && yy < L) v[q] = __ldg(x + (z * P + (long long)yy * L + aa));
+  for (int j = 0; j < kStRows; ++j) {
+    yy[j] = y0 + ty + 8 * j;
+    valid[j] = a < L && yy[j] < L;
+  }
+  // this thread's staging elements of a plane: in-plane offset, inside the box or not.  Outside
+  // elements are zero in every ring slot (written once here, never copied); planes outside the
+  // box are zeroed by stores instead of copied.
+  int off[kStE];
+  bool inb[kStE];
+#pragma unroll
+  for (int k = 0; k < kStE; ++k) {
+    const int e = tid + k * kStNT;
+    const int aa = a0 - 1 + e % kStPX, ye = y0 - 1 + e / kStPX;
+    inb[k] = e < kStPlane && aa >= 0 && aa < L && ye >= 0 && ye < L;
+    off[k] = inb[k] ? ye * L + aa : 0;
+    if (e < kStPlane && !inb[k])
+      for (int q = 0; q < kStNR; ++q) pl[q][e] = 0.0;
+  }
+  const int roff[kStRows] = {valid[0] ? yy[0] * L + a : 0, valid[1] ? yy[1] * L + a : 0};
+  // copy group of plane q (planes past z1 commit an empty group: the wait count stays uniform)
+  auto issue = [&](int q) {
+    if (q <= z1) {
+      double* dst = pl[(q + kStNR) & (kStNR - 1)];
+      if (q >= 0 && q < L) {
+        const double* base = x + (long long)q * P;
+#pragma unroll
+        for (int k = 0; k < kStE; ++k)
+          if (inb[k]) cp_async8(dst + tid + k * kStNT, base + off[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < kStE; ++k)
+          if (inb[k]) dst[tid + k * kStNT] = 0.0;
+      }
+      if (MODE == kResidual && q >= z0 && q < z1) {
+        const double* rb = r + (long long)q * P;
+#pragma unroll
+        for (int j = 0; j < kStRows; ++j)
+          if (valid[j]) cp_async8(&rr[q & (kStNR - 1)][tid + j * kStNT], rb + roff[j]);
       }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  auto put = [&](int z, const double (&v)[2]) {
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int e = tid + q * kStTX * kStTY;
-      if (e < kStPlane) pl[(z + 4) & 3][e] = v[q];
-    }
-  };
-  double v0[2], v1[2], v2[2];
-  stage(z0 - 1, v0);
-  stage(z0, v1);
-  stage(z0 + 1, v2);
-  put(z0 - 1, v0);
-  put(z0, v1);
-  put(z0 + 1, v2);
-  __syncthreads();
-  const int a = a0 + tx, yy = y0 + ty;
-  const bool valid = a < L && yy < L;
-  const int cay = CLS ? (pos_class(a < L ? a : 0, L) * 16 + pos_class(yy < L ? yy : 0, L) * 4) : 0;
-  double U[15];
+  for (int q = 0; q < kStD; ++q) issue(z0 - 1 + q);
+  int cay[kStRows];
+#pragma unroll
+  for (int j = 0; j < kStRows; ++j)
+    cay[j] = CLS ? (pos_class(a < L ? a : 0, L) * 16 + pos_class(yy[j] < L ? yy[j] : 0, L) * 4) : 0;
+  double U[CLS ? 1 : 15];
+  __syncthreads();  // st
   if (!CLS) {
 #pragma unroll
     for (int k = 0; k < 15; ++k) U[k] = st[k];
   }
-  const int c0 = (ty + 1) * kStPX + tx + 1;  // this row's cell in a staged plane
+  double cm[kStRows][4], cp[kStRows][4];  // carried: below (-1-1, 0-1, -10, 00), centre (00, 10, 01, 11)
+  double contrib = 0.0;
+#pragma unroll 2
   for (int z = z0; z < z1; ++z) {
-    double nv[2];
-    stage(z + 2, nv);  // in flight while this plane's rows are summed
-    const double* pm = pl[(z - 1 + 4) & 3];
-    const double* p0 = pl[z & 3];
-    const double* pp = pl[(z + 1) & 3];
-    const double* v = CLS ? st + (cay + pos_class(z, L)) * 16 : U;
-    const double xs[15] = {pm[c0 - kStPX - 1], pm[c0 - kStPX], pm[c0 - 1], pm[c0],
-                           p0[c0 - kStPX - 1], p0[c0 - kStPX], p0[c0 - 1], p0[c0], p0[c0 + 1], p0[c0 + kStPX],
-                           p0[c0 + kStPX + 1], pp[c0], pp[c0 + 1], pp[c0 + kStPX], pp[c0 + kStPX + 1]};
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < 15; ++k) acc = __dadd_rn(acc, __dmul_rn(v[k], xs[k]));
-    if (valid) {
-      const long long i = z * P + (long long)yy * L + a;
-      y[i] = MODE == kResidual ? __dsub_rn(r[i], acc) : acc;
-    }
-    put(z + 2, nv);
+    issue(z + kStD - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kStD - 2) : "memory");  // planes <= z + 1 landed
     __syncthreads();
+    const double* p0 = pl[z & (kStNR - 1)];
+    const double* pp = pl[(z + 1) & (kStNR - 1)];
+    if (z == z0) {  // prime the carried values from planes z0 - 1 and z0
+      const double* pm = pl[(z - 1 + kStNR) & (kStNR - 1)];
+#pragma unroll
+      for (int j = 0; j < kStRows; ++j) {
+        const int c = (ty + 8 * j + 1) * kStPX + tx + 1;
+        cm[j][0] = pm[c - kStPX - 1];
+        cm[j][1] = pm[c - kStPX];
+        cm[j][2] = pm[c - 1];
+        cm[j][3] = pm[c];
+        cp[j][0] = p0[c];
+        cp[j][1] = p0[c + 1];
+        cp[j][2] = p0[c + kStPX];
+        cp[j][3] = p0[c + kStPX + 1];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kStRows; ++j) {
+      const int c = (ty + 8 * j + 1) * kStPX + tx + 1;
+      const double* v = CLS ? st + (cay[j] + pos_class(z, L)) * 16 : U;
+      const double xs[15] = {cm[j][0], cm[j][1], cm[j][2], cm[j][3],
+                             p0[c - kStPX - 1], p0[c - kStPX], p0[c - 1], cp[j][0], cp[j][1], cp[j][2], cp[j][3],
+                             pp[c], pp[c + 1], pp[c + kStPX], pp[c + kStPX + 1]};
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < 15; ++k) acc = __dadd_rn(acc, __dmul_rn(v[k], xs[k]));
+      if (valid[j]) {
+        const long long i = z * P + (long long)yy[j] * L + a;
+        if (MODE == kResidual) {
+          y[i] = __dsub_rn(rr[z & (kStNR - 1)][tid + j * kStNT], acc);
+        } else {
+          y[i] = acc;
+          if (MODE == kDot) contrib = __dadd_rn(contrib, __dmul_rn(xs[7], acc));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        cm[j][k] = xs[4 + (k < 3 ? k : 3)];
+        cp[j][k] = xs[11 + k];
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (MODE == kDot) {
+    const double bs = block_sum_fixed<kStNT>(contrib, red);
+    if (tid == 0) partials[b] = bs;
+    finish_reduction<kStNT>(partials, counter, red, [&](double t) { *dot_out = t; });
   }
 }
 
@@ -356,13 +404,30 @@ void launch_spmv(Ctx& c, const DCsr& A, const double* x, double* y, const double
       A.lat.lx == A.lat.lz && (int64_t)A.lat.lx * A.lat.lx * A.lat.lx == A.rows && A.cols == A.rows) {
     const int L = A.lat.lx;
     const bool cls = A.lat_uni_state == 2;
-    constexpr int M = MODE == kResidual ? kResidual : kPlain;
-    auto* k = cls ? stencil_spmv_tiled_kernel<M, true> : stencil_spmv_tiled_kernel<M, false>;
-    const dim3 grid(div_up(L, kStTX), div_up(L, kStTY), div_up(L, kStZC));
-    k<<<grid, kStTX * kStTY, 0, c.stream>>>(L, cls ? A.lat_cls.p : A.lat_uni.p, x, y, r);
+    const int gx = div_up(L, kStTX), gy = div_up(L, kStTY);
+    // planes per block: each block's planes are a dependent chain (one ring step each), so the
+    // shortest chain that still fits the grid in the resident slots (2 blocks per SM) wins
+    int zc = 4;
+    while (zc < 16 && (int64_t)gx * gy * div_up(L, zc) > 2 * (int64_t)c.num_sms) zc *= 2;
+    const int64_t nb = (int64_t)gx * gy * div_up(L, zc);
+    // the fused dot needs one partial per block
+    const bool fused = MODE != kDot || nb <= Ctx::kMaxPartials;
+    constexpr int M2 = MODE == kDot ? kPlain : MODE;
+    auto* k = fused ? (cls ? stencil_spmv_tiled_kernel<MODE, true> : stencil_spmv_tiled_kernel<MODE, false>)
+                    : (cls ? stencil_spmv_tiled_kernel<M2, true> : stencil_spmv_tiled_kernel<M2, false>);
+    const size_t smem = sizeof(double) * kStNR * (kStPlane + (MODE == kResidual ? kStRows * kStNT : 0));
+    static bool attr = false;  // per MODE instantiation
+    if (!attr) {
+      for (auto* kk : {stencil_spmv_tiled_kernel<MODE, true>, stencil_spmv_tiled_kernel<MODE, false>,
+                       stencil_spmv_tiled_kernel<M2, true>, stencil_spmv_tiled_kernel<M2, false>})
+        RDG_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    k<<<(unsigned)nb, kStNT, smem, c.stream>>>(L, gx, gy, zc, cls ? A.lat_cls.p : A.lat_uni.p, x, y, r, c.d_partials,
+                                            c.d_counter, dot_out);
     RDG_LAUNCH_CHECK();
     ++c.launches;
-    if (MODE == kDot) dot(c, A.rows, x, y, dot_out);
+    if (!fused) dot(c, A.rows, x, y, dot_out);
     return;
   }
   const int nb = div_up(A.rows, kSpmvNT);
