@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -247,6 +248,121 @@ inline PcgResult pcg(const DeviceMatrix& A, const AmgHierarchy* h, const std::ve
   out.report.converged = rep.converged != 0;
   out.report.residual_history.assign(hist.begin(), hist.begin() + rep.iterations);
   return out;
+}
+
+// linalg.hpp:11 rd::LinOp -- a fixed linear map, here y = op(x) on DEVICE vectors enqueued on the
+// context's stream (rd_linop).  Built-ins (identity_precond, spmv_op, amg_precond, jacobi_precond)
+// run fused inside pcg; LinOp::device wraps a callable on device pointers, LinOp::host the
+// reference's own host-vector LinOp (a copy out and back around each application).
+class LinOp {
+ public:
+  using DeviceFn = std::function<void(const double* x_dev, double* y_dev, int64_t n)>;
+  using HostFn = std::function<std::vector<double>(const std::vector<double>&)>;
+  LinOp() = default;
+  LinOp(rd_linop op, Context* ctx, std::shared_ptr<void> keep) : op_(op), ctx_(ctx), keep_(std::move(keep)) {}
+
+  static LinOp device(Context& ctx, DeviceFn fn) {
+    auto f = std::make_shared<DeviceFn>(std::move(fn));
+    return LinOp(rd_linop{&device_tramp, f.get()}, &ctx, f);
+  }
+  static LinOp host(Context& ctx, HostFn fn) {
+    auto f = std::make_shared<HostFn>(std::move(fn));
+    return LinOp(rd_linop{&host_tramp, f.get()}, &ctx, f);
+  }
+  // y = op(x) on host vectors (rd_gpu_linop_apply)
+  std::vector<double> operator()(const std::vector<double>& x) const {
+    Context& c = ctx_ ? *ctx_ : default_context();
+    std::vector<double> y(x.size());
+    if (!x.empty()) check(rd_gpu_linop_apply(c.get(), op_, (int64_t)x.size(), x.data(), y.data()), c.get());
+    return y;
+  }
+  const rd_linop& c_op() const { return op_; }
+  Context* context() const { return ctx_; }
+
+ private:
+  static int device_tramp(void* user, rd_ctx*, int64_t n, const double* x, double* y) {
+    try {
+      (*static_cast<DeviceFn*>(user))(x, y, n);
+      return RD_OK;
+    } catch (const Error& e) {
+      return e.code;
+    } catch (const std::invalid_argument&) {
+      return RD_EINVAL;
+    } catch (...) {
+      return RD_ERUNTIME;
+    }
+  }
+  static int host_tramp(void* user, rd_ctx* ctx, int64_t n, const double* x, double* y) {
+    try {
+      std::vector<double> hx((size_t)n);
+      check(rd_gpu_copy(ctx, hx.data(), x, sizeof(double) * (size_t)n), ctx);
+      const std::vector<double> hy = (*static_cast<HostFn*>(user))(hx);
+      if ((int64_t)hy.size() != n) return RD_EINVAL;
+      check(rd_gpu_copy(ctx, y, hy.data(), sizeof(double) * (size_t)n), ctx);
+      return RD_OK;
+    } catch (const Error& e) {
+      return e.code;
+    } catch (const std::invalid_argument&) {
+      return RD_EINVAL;
+    } catch (...) {
+      return RD_ERUNTIME;
+    }
+  }
+  rd_linop op_{nullptr, nullptr};
+  Context* ctx_ = nullptr;
+  std::shared_ptr<void> keep_;
+};
+
+// linalg.hpp:39 identity_precond()
+inline LinOp identity_precond() {
+  rd_linop op{};
+  check(rd_gpu_linop_identity(&op), nullptr);
+  return LinOp(op, nullptr, nullptr);
+}
+// linalg.cpp:104-106: the SpMat overload's operator [&A](x) { return spmv(A, x); }
+inline LinOp spmv_op(const DeviceMatrix& A) {
+  rd_linop op{};
+  check(rd_gpu_linop_csr(A.get(), &op), A.context().get());
+  return LinOp(op, &A.context(), std::make_shared<DeviceMatrix>(A));
+}
+// amg.hpp:42 amg_precond(h)
+inline LinOp amg_precond(const AmgHierarchy& h) {
+  rd_linop op{};
+  check(rd_gpu_linop_amg(h.get(), &op), h.context().get());
+  return LinOp(op, &h.context(), std::make_shared<AmgHierarchy>(h));
+}
+// linalg.hpp:40 jacobi_precond(A): throws std::runtime_error on a non-positive diagonal
+inline LinOp jacobi_precond(const DeviceMatrix& A) {
+  rd_jacobi* j = nullptr;
+  check(rd_gpu_jacobi_create(A.context().get(), A.get(), &j), A.context().get());
+  std::shared_ptr<rd_jacobi> keep(j, rd_gpu_jacobi_free);
+  rd_linop op{};
+  check(rd_gpu_linop_jacobi(j, &op), A.context().get());
+  return LinOp(op, &A.context(), keep);
+}
+
+// linalg.hpp:46-47 pcg(apply_A, apply_P, f, tol, max_iter)
+inline PcgResult pcg(const LinOp& apply_A, const LinOp& apply_P, const std::vector<double>& f, double tol = 1e-8,
+                     int max_iter = 500) {
+  Context& c = apply_A.context() ? *apply_A.context()
+               : apply_P.context() ? *apply_P.context()
+                                   : default_context();
+  PcgResult out;
+  out.x.resize(f.size());
+  std::vector<double> hist(max_iter > 0 ? max_iter : 1);
+  rd_pcg_report rep{};
+  check(rd_gpu_pcg_linop(c.get(), (int64_t)f.size(), apply_A.c_op(), apply_P.c_op(), f.empty() ? nullptr : f.data(),
+                         tol, max_iter, out.x.empty() ? nullptr : out.x.data(), &rep, hist.data()),
+        c.get());
+  out.report.iterations = rep.iterations;
+  out.report.converged = rep.converged != 0;
+  out.report.residual_history.assign(hist.begin(), hist.begin() + rep.iterations);
+  return out;
+}
+// linalg.hpp:48-49 pcg(A, apply_P, f, tol, max_iter)
+inline PcgResult pcg(const DeviceMatrix& A, const LinOp& apply_P, const std::vector<double>& f, double tol = 1e-8,
+                     int max_iter = 500) {
+  return pcg(spmv_op(A), apply_P, f, tol, max_iter);
 }
 
 // bench.hpp:48-57 SolveOutcome / solve_system(..., PrecondKind::amg, ...)

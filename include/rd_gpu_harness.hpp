@@ -8,9 +8,10 @@
 //   * run_precond_bench -- the bench-precond rows                       (bench.cpp:392-423)
 //   * MatrixMarket coordinate / array I/O, %.17g round trip            (io.cpp:14-97)
 //
-// Only what the device path serves is routed: bench-precond with the AMG preconditioner.
-// BDDC, Jacobi and the unpreconditioned solver are not part of the north-star path and
-// throw std::invalid_argument (the reference's exception type for a rejected config).
+// Only what the device path serves is routed: bench-precond with the AMG preconditioner, and
+// solve_system with AMG or Jacobi.  BDDC and the unpreconditioned (dense Cholesky) solver are
+// not part of the north-star path and throw std::invalid_argument (the reference's exception
+// type for a rejected config).
 #pragma once
 
 #include <algorithm>
@@ -353,14 +354,33 @@ inline int failed_rows(const EocTable& t) {
 }
 
 // ------------------------------------------------------------------ solve_system / bench
-// bench.cpp:185-241 for PrecondKind::amg (the device path): timing excludes build_system,
-// setup_seconds = build_amg, solve_seconds = pcg, empty systems converge immediately
+// bench.cpp:185-241 for PrecondKind::amg and ::jacobi (the device path): timing excludes
+// build_system, setup_seconds = build_amg / jacobi_precond, solve_seconds = pcg, empty systems
+// converge immediately.  none (dense Cholesky) and bddc are not served by the device path.
 inline SolveOutcome solve_system(const TetMesh& /*mesh*/, const FemSystem& sys, PrecondKind kind, int /*p*/,
                                  double tol) {
-  if (kind != PrecondKind::amg)
-    throw std::invalid_argument("solve_system: only the AMG preconditioner is served by the device path (" +
-                                precond_name(kind) + " requested)");
-  return solve_system_amg(sys, tol);
+  if (kind == PrecondKind::amg) return solve_system_amg(sys, tol);
+  if (kind != PrecondKind::jacobi)
+    throw std::invalid_argument("solve_system: the " + precond_name(kind) +
+                                " preconditioner is not served by the device path");
+  SolveOutcome out;
+  if (sys.n_dofs() == 0) {  // bench.cpp:188-192
+    out.converged = true;
+    return out;
+  }
+  using clk = std::chrono::steady_clock;
+  const std::vector<double> f = sys.f();
+  const auto t0 = clk::now();
+  const LinOp P = jacobi_precond(sys.A);  // bench.cpp:205-207
+  const auto t1 = clk::now();
+  PcgResult res = pcg(sys.A, P, f, tol, 500);
+  const auto t2 = clk::now();
+  out.u = std::move(res.x);
+  out.iterations = res.report.iterations;
+  out.converged = res.report.converged;
+  out.setup_seconds = std::chrono::duration<double>(t1 - t0).count();
+  out.solve_seconds = std::chrono::duration<double>(t2 - t1).count();
+  return out;
 }
 
 // bench.cpp:392-423: one row per (rho, n), rho outer; columns rho,n,dofs,iterations,converged,

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "rd_gpu.hpp"
+#include "rd_gpu_harness.hpp"
 
 static int g_fail = 0, g_pass = 0;
 #define CHECK(cond)                                                      \
@@ -143,6 +144,62 @@ int main() {
       threw = true;
     }
     CHECK(threw);
+  }
+  {  // linalg.hpp:11, 39-49 / amg.hpp:42: the LinOp overloads, as bench.cpp:205-218 calls them
+    auto mesh = build_structured_cube(16, ctx);
+    auto sys = build_system(mesh, 1.0 / 256.0, Target::ball);
+    AmgHierarchy h(sys.A);
+    const std::vector<double> f = sys.f();
+    auto ref = pcg(sys.A, &h, f, 1e-8, 500);
+    auto r = pcg(sys.A, amg_precond(h), f, 1e-8, 500);  // bench.cpp:218
+    CHECK(r.report.converged && r.report.iterations == ref.report.iterations && r.x == ref.x);
+    auto rj = pcg(sys.A, jacobi_precond(sys.A), f, 1e-8, 500);  // bench.cpp:205-207
+    CHECK(rj.report.converged && rj.report.iterations > r.report.iterations);
+    double dmax = 0.0, xmax = 0.0;
+    for (size_t i = 0; i < f.size(); ++i) {
+      dmax = std::fmax(dmax, std::fabs(rj.x[i] - ref.x[i]));
+      xmax = std::fmax(xmax, std::fabs(ref.x[i]));
+    }
+    CHECK(dmax <= 1e-6 * xmax);
+    // bench.cpp:204-213 solve_system(..., PrecondKind::jacobi, ...) through the harness layer
+    const SolveOutcome so = solve_system(mesh, sys, PrecondKind::jacobi, 0, 1e-8);
+    CHECK(so.converged && so.iterations == rj.report.iterations && so.u == rj.x && so.solve_seconds > 0.0);
+    // the reference's host-vector LinOp (bench.cpp:59-61 style: a nested solve as an operator)
+    int calls = 0;
+    LinOp host_amg = LinOp::host(ctx, [&](const std::vector<double>& b) {
+      ++calls;
+      return amg_apply(h, b);
+    });
+    auto rh = pcg(sys.A, host_amg, f, 1e-8, 500);
+    CHECK(rh.report.iterations == ref.report.iterations && calls == rh.report.iterations + 1);
+    dmax = 0.0;
+    for (size_t i = 0; i < f.size(); ++i) dmax = std::fmax(dmax, std::fabs(rh.x[i] - ref.x[i]));
+    CHECK(dmax <= 1e-10 * xmax);
+    // an operator applied on its own equals the library call it wraps
+    CHECK(spmv_op(sys.A)(f) == spmv(sys.A, f));
+    CHECK(amg_precond(h)(f) == amg_apply(h, f));
+    // a throwing operator surfaces as the call's exception
+    LinOp bad = LinOp::host(ctx, [](const std::vector<double>&) -> std::vector<double> {
+      throw std::runtime_error("operator failed");
+    });
+    bool threw = false;
+    try {
+      pcg(sys.A, bad, f, 1e-8, 10);
+    } catch (const std::runtime_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+    // linalg.cpp:57-61: a non-positive diagonal
+    threw = false;
+    try {
+      jacobi_precond(from_dense(ctx, 2, {1.0, 0.0, 0.0, -1.0}));
+    } catch (const std::runtime_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+    // test_linalg.cpp:96-103 through the identity LinOp
+    auto r1 = pcg(from_dense(ctx, 1, {2.0}), identity_precond(), std::vector<double>{4.0}, 1e-12, 10);
+    CHECK(r1.report.converged && r1.report.iterations == 1 && std::fabs(r1.x[0] - 2.0) < 1e-14);
   }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail;
