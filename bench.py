@@ -53,8 +53,9 @@ def parse():
                         "boundary cells into the next GPU's memory (NVLink, CUDA IPC); exact = planes handed on "
                         "over NCCL between sweeps (both the single-GPU sweep bit for bit); block = concurrent "
                         "processor-block SGS (a different preconditioner)")
-    p.add_argument("--gather-rows", dest="gather_rows", type=int, default=262144,
-                   help="N > 1: levels with at most this many rows run whole on rank 0")
+    p.add_argument("--gather-rows", dest="gather_rows", type=int, default=None,
+                   help="N > 1: levels with at most this many rows run whole on rank 0 (default: by "
+                        "cost, a level is cut while every rank gets >= 65536 of its rows)")
     p.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of slabs")
     p.add_argument("--dist", action="store_true", help="run the slab-distributed path even at N = 1")
     return p.parse_args()

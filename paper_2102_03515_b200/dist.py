@@ -17,7 +17,7 @@ ranks, one GPU per rank, the way §8(e) lays out:
   CPU): one plane per face before every SpMV / residual / restriction /
   prolongation / smoother pass that reads a neighbour's rows; the inner products
   all-gathered (16 bytes per iteration) and summed in rank order, so every rank
-  holds the same scalars; levels at or below ``gather_rows`` gathered onto rank 0
+  holds the same scalars; levels too small to pay for their exchanges gathered onto rank 0
   (``rd_gpu_amg_apply_from``) and the correction scattered back.
 * **Smoother.**  ``mode="exact"`` hands the Gauss-Seidel wavefront from rank to
   rank (the upstream ghost plane is the neighbour's *fresh* values): the
@@ -81,12 +81,18 @@ class SlabPlan:
         return max(lo - 1, 0), min(hi + 1, self.sides[l])
 
 
-def choose_dist_levels(sides, rows, structured, world: int, gather_rows: int) -> int:
-    """Distribute the leading lattice levels with more than `gather_rows` rows (at least level 0),
-    as many as the 2^G-aligned cuts allow."""
+MIN_ROWS_PER_RANK = 65536  # below this a level's slab work no longer pays for its exchanges
+
+
+def choose_dist_levels(sides, rows, structured, world: int, gather_rows: int | None = None) -> int:
+    """Distribute the leading lattice levels (at least level 0), as many as the 2^G-aligned cuts
+    allow.  gather_rows=None: by cost -- a level is cut while every rank's share has at least
+    MIN_ROWS_PER_RANK rows (its per-sweep plane exchanges and hand-off waits are then small
+    against the slab's own sweep); otherwise levels with more than `gather_rows` rows are cut."""
     nl = len(rows)
     G = 1
-    while G < nl - 1 and rows[G] > gather_rows and structured[G]:
+    keep = (lambda r: r // world >= MIN_ROWS_PER_RANK) if gather_rows is None else (lambda r: r > gather_rows)
+    while G < nl - 1 and keep(rows[G]) and structured[G]:
         G += 1
     while G >= 1:
         try:
@@ -506,7 +512,8 @@ class DistResult:
 class DistSolver:
     """Slab-distributed AMG-PCG (linalg.cpp:64-102 with amg_precond, amg.cpp:119-145)."""
 
-    def __init__(self, comm, ops, gather_rows: int = 262144, mode: str = "exact", dist_levels: int | None = None):
+    def __init__(self, comm, ops, gather_rows: int | None = None, mode: str = "exact",
+                 dist_levels: int | None = None):
         if mode not in ("exact", "block", "pipelined"):
             raise ValueError("mode must be 'exact', 'block' or 'pipelined'")
         self.comm, self.ops, self.mode = comm, ops, mode

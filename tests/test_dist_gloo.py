@@ -133,8 +133,17 @@ def test_slab_plan_alignment():
         owned = [p.owned(l, r) for r in range(8)]
         assert owned[0][0] == 0 and owned[-1][1] == p.sides[l]
         assert all(owned[r][1] == owned[r + 1][0] for r in range(7))
-    # C2 with the default gather threshold: only level 0 is cut
+    # C2 with a 262,144-row gather threshold: only level 0 is cut
+    sides = [127, 64, 32, 16, 8, 4]
     rows = [127 ** 3, 64 ** 3, 32 ** 3, 16 ** 3, 8 ** 3, 4 ** 3]
-    assert choose_dist_levels([127, 64, 32, 16, 8, 4], rows, [True] * 6, 8, 262144) == 1
+    assert choose_dist_levels(sides, rows, [True] * 6, 8, 262144) == 1
+    # by cost (>= 65,536 rows per rank): 2 and 4 ranks cut levels 0-1, 8 ranks level 0 only
+    assert choose_dist_levels(sides, rows, [True] * 6, 2) == 2
+    assert choose_dist_levels(sides, rows, [True] * 6, 4) == 2
+    assert choose_dist_levels(sides, rows, [True] * 6, 8) == 1
+    # C4 (n = 256) on 8 ranks: levels 0 and 1 (level 1: 2,097,152 / 8 = 262,144 rows per rank)
+    s4 = [255, 128, 64, 32, 16, 8, 4]
+    r4 = [s ** 3 for s in s4]
+    assert choose_dist_levels(s4, r4, [True] * 7, 8) == 2
     with pytest.raises(ValueError):
         SlabPlan([7, 4, 2], 8, 1)
