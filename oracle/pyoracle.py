@@ -100,6 +100,12 @@ def lib():
         "or_h1_semi_error_manufactured": (_I, [_P, _P, _pd, _D, C.POINTER(_D)]),
         "or_error_norms_target": (_I, [_P, _P, _pd, _I, _I, C.c_uint64, C.POINTER(_D), C.POINTER(_D)]),
         "or_target_grad": (_I, [_I, _I, C.c_uint64, _I, _pd, _pd]),
+        "or_estimate": (_I, [_P, _P, _pd, _I, C.c_uint64, _pd, C.POINTER(_D)]),
+        "or_mark_dorfler": (_I, [_I, _pd, _D, _pi, C.POINTER(_I)]),
+        "or_bisect_marked": (_I, [_P, _I, _pi, C.POINTER(_P)]),
+        "or_uniform_refine": (_I, [_P, C.POINTER(_P)]),
+        "or_adaptive_solve": (_I, [_P, _I, C.c_uint64, _D, _I, _D, _D, _I, C.POINTER(_I), _pi, _pd, C.POINTER(_P),
+                                   _pd, _I]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -200,6 +206,19 @@ def build_structured_cube(n: int) -> Mesh:
     """mesh.cpp:29-65."""
     h = _P()
     _check(lib().or_build_structured_cube(int(n), C.byref(h)))
+    hh = _Handle(h, lib().or_mesh_free)
+    nv, nt = _I(), _I()
+    lib().or_mesh_info(h, C.byref(nv), C.byref(nt))
+    xyz = np.zeros((max(nv.value, 1), 3))
+    tets = np.zeros((max(nt.value, 1), 4), np.int32)
+    b = np.zeros(max(nv.value, 1), np.uint8)
+    re = np.zeros(max(nt.value, 1), np.uint8)
+    gen = np.zeros(max(nt.value, 1), np.int32)
+    lib().or_mesh_get(h, xyz, tets, b, re, gen)
+    return Mesh(n, xyz[: nv.value], tets[: nt.value], b[: nv.value], re[: nt.value], gen[: nt.value], hh)
+
+
+def _mesh_from_handle(h, n: int = -1) -> Mesh:
     hh = _Handle(h, lib().or_mesh_free)
     nv, nt = _I(), _I()
     lib().or_mesh_info(h, C.byref(nv), C.byref(nt))
@@ -499,3 +518,53 @@ def target_dual_norm(sys: FemSystem, coeffs) -> float:
     out = _D()
     _check(lib().or_target_dual_norm(sys._h.h, np.ascontiguousarray(coeffs, np.float64), C.byref(out)))
     return out.value
+
+
+# ---------------------------------------------------------------- adaptivity (§8(f)3)
+def estimate(mesh: Mesh, sys: FemSystem, coeffs, target: str, seed: int = 0):
+    """adapt.cpp:35-124 -> (per_tet, global)."""
+    per = np.zeros(max(mesh.tets.shape[0], 1))
+    g = _D()
+    _check(lib().or_estimate(mesh._h.h, sys._h.h, np.ascontiguousarray(coeffs, np.float64), TARGETS[target],
+                             int(seed), per, C.byref(g)))
+    return per[: mesh.tets.shape[0]], g.value
+
+
+def mark_dorfler(eta, theta: float) -> np.ndarray:
+    """adapt.cpp:126-150 -> marked tet ids in marking order."""
+    eta = np.ascontiguousarray(eta, np.float64)
+    out = np.zeros(max(eta.size, 1), np.int32)
+    k = _I()
+    _check(lib().or_mark_dorfler(eta.size, eta if eta.size else np.zeros(1), float(theta), out, C.byref(k)))
+    return out[: k.value]
+
+
+def bisect_marked(mesh: Mesh, marked) -> Mesh:
+    """mesh.cpp:67-145."""
+    mk = np.ascontiguousarray(marked, np.int32).reshape(-1)
+    h = _P()
+    _check(lib().or_bisect_marked(mesh._h.h, mk.size, mk if mk.size else np.zeros(1, np.int32), C.byref(h)))
+    return _mesh_from_handle(h)
+
+
+def uniform_refine(mesh: Mesh) -> Mesh:
+    """mesh.cpp:147-156."""
+    h = _P()
+    _check(lib().or_uniform_refine(mesh._h.h, C.byref(h)))
+    return _mesh_from_handle(h)
+
+
+def adaptive_solve(mesh: Mesh, target: str, rho: float, dof_budget: int, tol: float = 1e-8, theta: float = 0.5,
+                   seed: int = 0, cap: int = 256, coeffs_cap: int = 1 << 22):
+    """adapt.cpp:152-205 with the AMG solver -> (history rows, final mesh, final coefficients)."""
+    k = _I()
+    hi = np.zeros(3 * cap, np.int32)
+    hd = np.zeros(3 * cap)
+    fm = _P()
+    co = np.zeros(coeffs_cap)
+    _check(lib().or_adaptive_solve(mesh._h.h, TARGETS[target], int(seed), float(rho), int(dof_budget), float(tol),
+                                   float(theta), cap, C.byref(k), hi, hd, C.byref(fm), co, coeffs_cap))
+    rows = [dict(level=int(hi[3 * i]), dofs=int(hi[3 * i + 1]), iterations=int(hi[3 * i + 2]), eta=float(hd[3 * i]),
+                 err_l2_sq=float(hd[3 * i + 1]), err_hm1_sq=float(hd[3 * i + 2])) for i in range(min(k.value, cap))]
+    final = _mesh_from_handle(fm)
+    return rows, final, co[: rows[-1]["dofs"]].copy()

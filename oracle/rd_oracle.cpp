@@ -28,6 +28,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 namespace {
@@ -1223,6 +1224,317 @@ double target_dual_norm(const System& s, const double* coeffs) {
   return std::sqrt(rw);
 }
 
+// ---------------------------------------------------------------------------
+// adapt.cpp / mesh.cpp:67-156 (§8(f)3: the adaptive loop)
+
+// Eigen VectorXd::sum with SSE2: the same Redux.h LinearVectorizedTraversal as eigen_dot
+double eigen_sum(const double* a, int64_t n) {
+  if (n <= 0) return 0.0;
+  const int64_t aligned2 = (n / 4) * 4, aligned = (n / 2) * 2;
+  double res;
+  if (aligned) {
+    double p0a = a[0], p0b = a[1];
+    if (aligned > 2) {
+      double p1a = a[2], p1b = a[3];
+      for (int64_t i = 4; i < aligned2; i += 4) {
+        p0a = p0a + a[i];
+        p0b = p0b + a[i + 1];
+        p1a = p1a + a[i + 2];
+        p1b = p1b + a[i + 3];
+      }
+      p0a = p0a + p1a;
+      p0b = p0b + p1b;
+      if (aligned > aligned2) {
+        p0a = p0a + a[aligned2];
+        p0b = p0b + a[aligned2 + 1];
+      }
+    }
+    res = p0a + p0b;
+    for (int64_t i = aligned; i < n; ++i) res = res + a[i];
+  } else {
+    res = a[0];
+  }
+  return res;
+}
+
+double norm3(const double* d) { return std::sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]); }
+double dist3(const V3& a, const V3& b) {
+  const double d[3] = {a.c[0] - b.c[0], a.c[1] - b.c[1], a.c[2] - b.c[2]};
+  return norm3(d);
+}
+
+struct Estimate {
+  Vec per_tet;
+  double global = 0.0;
+};
+
+// adapt.cpp:35-124: eta_tau^2 = a_tau^2 vol ||target - u_h||^2_tau (the estimator's own rule:
+// subdivision64 for discontinuous targets, degree 5 otherwise) + for every interior face, in
+// ascending (sorted vertex key, tet) order, 1/2 rho^-1/2 a_F area [rho grad u_h . n]^2 on both sides
+Estimate estimate(const Mesh& m, const DofMap& dm, const double* coeffs, double rho, const Target& tg) {
+  const double inv_sqrt_rho = 1.0 / std::sqrt(rho);
+  const auto nodal = nodal_field(m, dm, coeffs);
+  const int nt = m.nt();
+  const Rule& rule = tg.tag == discontinuous ? rule_by_id(3) : rule_by_id(2);
+  Vec eta_sq(static_cast<size_t>(nt));
+  std::vector<std::array<double, 3>> grad(static_cast<size_t>(nt));
+  parallel_for(nt, [&](int64_t b, int64_t e) {
+    for (int64_t t = b; t < e; ++t) {
+      const auto verts = tet_vertices(m, static_cast<int>(t));
+      const auto& tet = m.tets[static_cast<size_t>(t)];
+      const LocalGeom lg = local_geom(verts);  // |J.determinant()| / 6 and J.inverse() rows
+      double g[3] = {0.0, 0.0, 0.0}, g0[3] = {0.0, 0.0, 0.0};
+      for (int i = 0; i < 3; ++i) {
+        const double s = nodal[static_cast<size_t>(tet[static_cast<size_t>(i + 1)])];
+        for (int c = 0; c < 3; ++c) {
+          g[c] = g[c] + s * lg.grad[i + 1][c];
+          g0[c] = g0[c] - lg.grad[i + 1][c];
+        }
+      }
+      const double s0 = nodal[static_cast<size_t>(tet[0])];
+      for (int c = 0; c < 3; ++c) g[c] = g[c] + s0 * g0[c];
+      grad[static_cast<size_t>(t)] = {g[0], g[1], g[2]};
+      double acc = 0.0;
+      for (int q = 0; q < rule.size(); ++q) {
+        const auto& lam = rule.pts[static_cast<size_t>(q)];
+        const V3 x = physical_point(lam, verts);
+        double uh = 0.0;
+        for (int i = 0; i < 4; ++i) uh += lam[static_cast<size_t>(i)] * nodal[static_cast<size_t>(tet[static_cast<size_t>(i)])];
+        const double d = tg(x) - uh;
+        acc += rule.w[static_cast<size_t>(q)] * d * d;
+      }
+      double h = 0.0;
+      for (int a = 0; a < 4; ++a)
+        for (int c = a + 1; c < 4; ++c) h = std::max(h, dist3(verts[static_cast<size_t>(a)], verts[static_cast<size_t>(c)]));
+      const double a_tau = std::min(h * inv_sqrt_rho, 1.0);
+      eta_sq[static_cast<size_t>(t)] = a_tau * a_tau * lg.volume * acc;
+    }
+  });
+  struct FaceRef {
+    std::array<int, 3> key;
+    int tet;
+  };
+  constexpr int kOpp[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
+  std::vector<FaceRef> faces;
+  faces.reserve(static_cast<size_t>(nt) * 4);
+  for (int t = 0; t < nt; ++t) {
+    const auto& tet = m.tets[static_cast<size_t>(t)];
+    for (int l = 0; l < 4; ++l) {
+      std::array<int, 3> key = {tet[static_cast<size_t>(kOpp[l][0])], tet[static_cast<size_t>(kOpp[l][1])],
+                                tet[static_cast<size_t>(kOpp[l][2])]};
+      std::sort(key.begin(), key.end());
+      faces.push_back({key, t});
+    }
+  }
+  std::sort(faces.begin(), faces.end(), [](const FaceRef& a, const FaceRef& b) {
+    if (a.key != b.key) return a.key < b.key;
+    return a.tet < b.tet;
+  });
+  for (size_t i = 0; i + 1 < faces.size(); ++i) {
+    if (faces[i].key != faces[i + 1].key) continue;
+    const FaceRef& fa = faces[i];
+    const FaceRef& fb = faces[i + 1];
+    const V3& v0 = m.vertices[static_cast<size_t>(fa.key[0])];
+    const V3& v1 = m.vertices[static_cast<size_t>(fa.key[1])];
+    const V3& v2 = m.vertices[static_cast<size_t>(fa.key[2])];
+    double a[3], b[3];
+    for (int c = 0; c < 3; ++c) {
+      a[c] = v1.c[c] - v0.c[c];
+      b[c] = v2.c[c] - v0.c[c];
+    }
+    const double cr[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+    const double cn = norm3(cr);
+    const double area = 0.5 * cn;
+    const double sq = (cr[0] * cr[0] + cr[1] * cr[1]) + cr[2] * cr[2];  // normalized(): v / sqrt(|v|^2)
+    const double nr = std::sqrt(sq);
+    const double nn[3] = {sq > 0.0 ? cr[0] / nr : cr[0], sq > 0.0 ? cr[1] / nr : cr[1], sq > 0.0 ? cr[2] / nr : cr[2]};
+    const auto& ga = grad[static_cast<size_t>(fa.tet)];
+    const auto& gb = grad[static_cast<size_t>(fb.tet)];
+    const double dg[3] = {ga[0] - gb[0], ga[1] - gb[1], ga[2] - gb[2]};
+    const double jump = rho * ((dg[0] * nn[0] + dg[1] * nn[1]) + dg[2] * nn[2]);
+    const double h_f = std::max({dist3(v0, v1), dist3(v1, v2), dist3(v0, v2)});
+    const double a_f = std::min(h_f * inv_sqrt_rho, 1.0);
+    const double term = 0.5 * inv_sqrt_rho * a_f * area * jump * jump;
+    eta_sq[static_cast<size_t>(fa.tet)] += term;
+    eta_sq[static_cast<size_t>(fb.tet)] += term;
+    ++i;
+  }
+  Estimate est;
+  est.per_tet.resize(static_cast<size_t>(nt));
+  for (int t = 0; t < nt; ++t) est.per_tet[static_cast<size_t>(t)] = std::sqrt(eta_sq[static_cast<size_t>(t)]);
+  est.global = std::sqrt(eigen_sum(eta_sq.data(), nt));
+  return est;
+}
+
+// adapt.cpp:126-150
+std::vector<int> mark_dorfler(const Vec& eta, double theta) {
+  if (!(theta > 0.0 && theta <= 1.0)) throw std::invalid_argument("mark_dorfler: theta must be in (0, 1]");
+  const int nt = static_cast<int>(eta.size());
+  std::vector<int> order(static_cast<size_t>(nt));
+  for (int t = 0; t < nt; ++t) order[static_cast<size_t>(t)] = t;
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    const double ea = eta[static_cast<size_t>(a)], eb = eta[static_cast<size_t>(b)];
+    if (ea != eb) return ea > eb;
+    return a < b;
+  });
+  double total = 0.0;
+  for (int t : order) total += eta[static_cast<size_t>(t)] * eta[static_cast<size_t>(t)];
+  const double goal = theta * theta * total;
+  std::vector<int> marked;
+  double acc = 0.0;
+  for (int t : order) {
+    const double e = eta[static_cast<size_t>(t)];
+    if (acc >= goal || e == 0.0) break;
+    marked.push_back(t);
+    acc += e * e;
+  }
+  return marked;
+}
+
+int64_t edge_key(int a, int b) {  // mesh.cpp:20-23
+  if (a > b) std::swap(a, b);
+  return (static_cast<int64_t>(a) << 32) | static_cast<uint32_t>(b);
+}
+
+// mesh.cpp:67-145: bisect the marked tets at edge (0, d), then every tet still carrying a split
+// edge, round by round; midpoints numbered in order of first split (tets ascending)
+Mesh bisect_marked(const Mesh& mesh, const std::vector<int>& marked) {
+  Mesh m = mesh;
+  std::vector<uint8_t> flag(m.tets.size(), 0);
+  for (int t : marked) {
+    if (t < 0 || t >= m.nt()) throw std::out_of_range("bisect_marked: tet index out of range");
+    flag[static_cast<size_t>(t)] = 1;
+  }
+  std::unordered_map<int64_t, int> midpoint;
+  auto mid_vertex = [&](int a, int b) {
+    const int64_t key = edge_key(a, b);
+    const auto it = midpoint.find(key);
+    if (it != midpoint.end()) return it->second;
+    const int z = m.nv();
+    const V3& va = m.vertices[static_cast<size_t>(a)];
+    const V3& vb = m.vertices[static_cast<size_t>(b)];
+    const V3 x{{0.5 * (va.c[0] + vb.c[0]), 0.5 * (va.c[1] + vb.c[1]), 0.5 * (va.c[2] + vb.c[2])}};
+    m.vertices.push_back(x);
+    m.boundary.push_back(on_unit_boundary(x) ? 1 : 0);
+    midpoint.emplace(key, z);
+    return z;
+  };
+  constexpr int kLocalEdges[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+  int round = 0;
+  while (std::find(flag.begin(), flag.end(), uint8_t{1}) != flag.end()) {
+    if (++round > 1000) throw std::logic_error("bisect_marked: conforming closure did not terminate");
+    std::vector<std::array<int, 4>> tets;
+    std::vector<uint8_t> tags;
+    std::vector<int> gens;
+    tets.reserve(m.tets.size() * 2);
+    for (size_t t = 0; t < m.tets.size(); ++t) {
+      if (!flag[t]) {
+        tets.push_back(m.tets[t]);
+        tags.push_back(m.refinement_edge[t]);
+        gens.push_back(m.generation[t]);
+        continue;
+      }
+      const auto p = m.tets[t];
+      const int d = m.refinement_edge[t];
+      const int z = mid_vertex(p[0], p[static_cast<size_t>(d)]);
+      std::array<int, 4> c1 = p;
+      c1[static_cast<size_t>(d)] = z;
+      std::array<int, 4> c2;
+      for (int q = 0; q < d; ++q) c2[static_cast<size_t>(q)] = p[static_cast<size_t>(q + 1)];
+      c2[static_cast<size_t>(d)] = z;
+      for (int q = d + 1; q < 4; ++q) c2[static_cast<size_t>(q)] = p[static_cast<size_t>(q)];
+      const uint8_t nd = static_cast<uint8_t>(d == 1 ? 3 : d - 1);
+      const int g = m.generation[t] + 1;
+      tets.push_back(c1);
+      tags.push_back(nd);
+      gens.push_back(g);
+      tets.push_back(c2);
+      tags.push_back(nd);
+      gens.push_back(g);
+    }
+    m.tets = std::move(tets);
+    m.refinement_edge = std::move(tags);
+    m.generation = std::move(gens);
+    flag.assign(m.tets.size(), 0);
+    for (size_t t = 0; t < m.tets.size(); ++t) {
+      const auto& v = m.tets[t];
+      for (const auto& e : kLocalEdges)
+        if (midpoint.count(edge_key(v[static_cast<size_t>(e[0])], v[static_cast<size_t>(e[1])]))) {
+          flag[t] = 1;
+          break;
+        }
+    }
+  }
+  return m;
+}
+
+Mesh uniform_refine(const Mesh& mesh) {  // mesh.cpp:147-156: three full sweeps
+  Mesh m = mesh;
+  for (int sweep = 0; sweep < 3; ++sweep) {
+    std::vector<int> all(m.tets.size());
+    for (size_t t = 0; t < all.size(); ++t) all[t] = static_cast<int>(t);
+    m = bisect_marked(m, all);
+  }
+  return m;
+}
+
+int n_interior(const Mesh& m) {  // mesh_stats(...).n_interior_dofs
+  int k = 0;
+  for (uint8_t b : m.boundary) k += b ? 0 : 1;
+  return k;
+}
+
+struct AdaptLevel {
+  int level = 0, dofs = 0;
+  double eta = 0.0, err_l2_sq = 0.0, err_hm1_sq = 0.0;
+  int iterations = 0;
+  double seconds = 0.0;
+};
+
+// adapt.cpp:152-205 with the AMG solver of bench.cpp:65-74 / test_adapt.cpp:36-41:
+// build_amg(A) then pcg(A, amg_precond, f, tol, 500)
+std::vector<AdaptLevel> adaptive_solve(const Mesh& initial, const Target& tg, double rho, int dof_budget,
+                                       double tol, double theta, Mesh* final_mesh, Vec* final_coeffs) {
+  std::vector<AdaptLevel> hist;
+  Mesh mesh = initial;
+  int level = 0;
+  for (;;) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const System sys = build_system(mesh, rho, tg);
+    PcgOut res;
+    if (!sys.f.empty()) {
+      const Amg h = build_amg(sys.A, 64, 1);
+      const Csr& A = sys.A;
+      res = pcg([&A](const Vec& v) { return spmv(A, v); }, [&h](const Vec& r) { return amg_apply(h, r); }, sys.f,
+                tol, 500);
+    }
+    const Estimate est = estimate(mesh, sys.dm, res.x.data(), rho, tg);
+    const double l2_sq = l2_error_target_squared(mesh, sys.dm, res.x.data(), tg);
+    const double hm1 = target_dual_norm(sys, res.x.data());
+    AdaptLevel row;
+    row.level = level;
+    row.dofs = sys.dm.n_dofs();
+    row.eta = est.global;
+    row.err_l2_sq = l2_sq;
+    row.err_hm1_sq = hm1 * hm1;
+    row.iterations = res.iterations;
+    row.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    hist.push_back(row);
+    if (row.dofs >= dof_budget) {
+      if (final_mesh) *final_mesh = std::move(mesh);
+      if (final_coeffs) *final_coeffs = std::move(res.x);
+      return hist;
+    }
+    if (++level > 200) throw std::runtime_error("adaptive_solve: level cap reached before the dof budget");
+    const std::vector<int> marked = mark_dorfler(est.per_tet, theta);
+    Mesh refined = bisect_marked(mesh, marked);
+    if (n_interior(refined) == row.dofs)
+      throw std::runtime_error("adaptive_solve: refinement stagnated at level " + std::to_string(level - 1) +
+                               " (" + std::to_string(row.dofs) + " dofs)");
+    mesh = std::move(refined);
+  }
+}
+
 template <class F>
 int guard(F&& fn) {
   try {
@@ -1569,6 +1881,52 @@ int or_error_norms_target(const or_mesh* m, const or_system* s, const double* co
     if (h1) *h1 = h1_semi_error(m->m, s->s.dm, coeffs, ex);
   });
 }
+// §8(f)3 -- adaptivity (adapt.hpp, mesh.hpp:40-44)
+int or_estimate(const or_mesh* m, const or_system* s, const double* coeffs, int kind, uint64_t seed,
+                double* per_tet, double* global) {
+  return guard([&] {
+    if (kind == OR_TARGET_SINE_RANDOM) throw std::invalid_argument("estimate: the sine+random target needs a lattice");
+    const Estimate e = estimate(m->m, s->s.dm, coeffs, s->s.rho, make_target(kind, 0, seed));
+    std::memcpy(per_tet, e.per_tet.data(), e.per_tet.size() * sizeof(double));
+    *global = e.global;
+  });
+}
+int or_mark_dorfler(int n, const double* eta, double theta, int* marked, int* n_marked) {
+  return guard([&] {
+    const std::vector<int> mk = mark_dorfler(Vec(eta, eta + n), theta);
+    std::memcpy(marked, mk.data(), mk.size() * sizeof(int));
+    *n_marked = static_cast<int>(mk.size());
+  });
+}
+int or_bisect_marked(const or_mesh* m, int n_marked, const int* marked, or_mesh** out) {
+  return guard([&] { *out = new or_mesh{bisect_marked(m->m, std::vector<int>(marked, marked + n_marked))}; });
+}
+int or_uniform_refine(const or_mesh* m, or_mesh** out) {
+  return guard([&] { *out = new or_mesh{uniform_refine(m->m)}; });
+}
+/* history rows: level, dofs, iterations (int[3]) and eta, err_l2_sq, err_hm1_sq (double[3]) */
+int or_adaptive_solve(const or_mesh* initial, int kind, uint64_t seed, double rho, int dof_budget, double tol,
+                      double theta, int cap, int* n_levels, int* hist_i, double* hist_d, or_mesh** final_mesh,
+                      double* coeffs, int coeffs_cap) {
+  return guard([&] {
+    if (kind == OR_TARGET_SINE_RANDOM) throw std::invalid_argument("adaptive_solve: the sine+random target needs a lattice");
+    Mesh fm;
+    Vec fc;
+    const auto h = adaptive_solve(initial->m, make_target(kind, 0, seed), rho, dof_budget, tol, theta, &fm, &fc);
+    *n_levels = static_cast<int>(h.size());
+    for (int k = 0; k < static_cast<int>(h.size()) && k < cap; ++k) {
+      hist_i[3 * k] = h[static_cast<size_t>(k)].level;
+      hist_i[3 * k + 1] = h[static_cast<size_t>(k)].dofs;
+      hist_i[3 * k + 2] = h[static_cast<size_t>(k)].iterations;
+      hist_d[3 * k] = h[static_cast<size_t>(k)].eta;
+      hist_d[3 * k + 1] = h[static_cast<size_t>(k)].err_l2_sq;
+      hist_d[3 * k + 2] = h[static_cast<size_t>(k)].err_hm1_sq;
+    }
+    if (coeffs && static_cast<int>(fc.size()) <= coeffs_cap) std::memcpy(coeffs, fc.data(), fc.size() * sizeof(double));
+    if (final_mesh) *final_mesh = new or_mesh{std::move(fm)};
+  });
+}
+
 int or_target_grad(int kind, int n, uint64_t seed, int npts, const double* xyz, double* g) {
   return guard([&] {
     const Target t = make_target(kind, n, seed);

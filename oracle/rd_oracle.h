@@ -122,6 +122,17 @@ int or_error_norms_target(const or_mesh* m, const or_system* s, const double* co
 /* the target's exact gradient at npts points (xyz [npts][3] -> g [npts][3]) */
 int or_target_grad(int kind, int n, uint64_t seed, int npts, const double* xyz, double* g);
 
+/* §8(f)3 adaptivity: estimate (adapt.cpp:35-124), mark_dorfler (:126-150), bisect_marked
+ * (mesh.cpp:67-145), uniform_refine (:147-156), adaptive_solve (adapt.cpp:152-205, AMG solver) */
+int or_estimate(const or_mesh* m, const or_system* s, const double* coeffs, int kind, uint64_t seed,
+                double* per_tet, double* global);
+int or_mark_dorfler(int n, const double* eta, double theta, int* marked, int* n_marked);
+int or_bisect_marked(const or_mesh* m, int n_marked, const int* marked, or_mesh** out);
+int or_uniform_refine(const or_mesh* m, or_mesh** out);
+int or_adaptive_solve(const or_mesh* initial, int kind, uint64_t seed, double rho, int dof_budget, double tol,
+                      double theta, int cap, int* n_levels, int* hist_i, double* hist_d, or_mesh** final_mesh,
+                      double* coeffs, int coeffs_cap);
+
 #ifdef __cplusplus
 }
 #endif
