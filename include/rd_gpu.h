@@ -160,6 +160,39 @@ typedef struct {
 int rd_gpu_pcg(rd_ctx* ctx, const rd_csr* a, rd_amg* amg, const double* f, double tol, int max_iter,
                double* x, rd_pcg_report* report, double* residual_history);
 
+/* ------------------------------------------------------------ adaptivity */
+/* bisection state of a mesh (mesh.hpp:17-20): refinement edge (0, d), d in {1,2,3}, and
+ * generation per tet; build_structured_cube / rd_gpu_mesh_create meshes carry d = 3, gen 0.
+ * Host or device arrays; either may be NULL. */
+int rd_gpu_mesh_tags(const rd_mesh* mesh, uint8_t* refinement_edge, int32_t* generation);
+int rd_gpu_mesh_set_tags(rd_mesh* mesh, const uint8_t* refinement_edge, const int32_t* generation);
+/* replaces rd::bisect_marked(mesh, marked)             mesh.hpp:44, mesh.cpp:67-145: newest-vertex
+ * bisection of the marked tets with conforming closure; a new mesh (vertex, tet, tag and
+ * generation arrays identical to the reference's).  RD_EINVAL for an id outside [0, n_tets)
+ * (the reference throws std::out_of_range). */
+int rd_gpu_bisect_marked(rd_ctx* ctx, const rd_mesh* mesh, int n_marked, const int32_t* marked, rd_mesh** out);
+/* replaces rd::uniform_refine(mesh)                     mesh.hpp:40, mesh.cpp:147-156 */
+int rd_gpu_uniform_refine(rd_ctx* ctx, const rd_mesh* mesh, rd_mesh** out);
+/* replaces rd::estimate(sol, target)                    adapt.hpp:21, adapt.cpp:35-124: eta per tet
+ * (n_tets doubles, host or device) and the global sqrt(sum eta^2).  The system carries rho. */
+int rd_gpu_estimate(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs,
+                    const rd_target* target, double* per_tet, double* global);
+/* replaces rd::mark_dorfler(est, theta)                 adapt.hpp:24, adapt.cpp:126-150: the marked
+ * tets in marking order (>= n ints, host or device) and their count; RD_EINVAL unless 0 < theta <= 1 */
+int rd_gpu_mark_dorfler(rd_ctx* ctx, int n, const double* per_tet, double theta, int32_t* marked, int* n_marked);
+/* replaces rd::adaptive_solve(initial, target, rho, dof_budget, solver, theta)  adapt.hpp:44-47,
+ * adapt.cpp:152-205, with the AMG solver of bench.cpp:65-74 (build_amg + pcg(tol, 500)).
+ * history: >= cap rows (the level count is returned in *n_levels even when it exceeds cap);
+ * final_mesh (may be NULL) receives the last mesh; coeffs (host or device, may be NULL) the last
+ * solution when it fits coeffs_cap. */
+typedef struct {
+  int level, dofs, iterations;
+  double eta, err_l2_sq, err_hm1_sq, seconds;
+} rd_adapt_level;
+int rd_gpu_adaptive_solve(rd_ctx* ctx, const rd_mesh* initial, const rd_target* target, double rho, int dof_budget,
+                          double tol, double theta, rd_adapt_level* history, int cap, int* n_levels,
+                          rd_mesh** final_mesh, double* coeffs, int coeffs_cap);
+
 /* ------------------------------------------------------------ LinOp (linalg.hpp:11) */
 /* rd::LinOp = std::function<Vec(const Vec&)>: a fixed linear map.  Here y = op(x) on DEVICE
  * vectors of n doubles, enqueued on the context's stream (rd_gpu_ctx_stream); x and y never

@@ -1526,4 +1526,269 @@ void error_norms_target(Ctx& c, const DMesh& m, const DSystem& s, const double* 
   error_norms_field(c, m, s, coeffs, ex, l2, h1);
 }
 
+// ---------------------------------------------------------------- adapt.cpp:35-124: the estimator
+namespace {
+__device__ __forceinline__ double norm3d(const double* d) {
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2])));
+}
+__device__ __forceinline__ double dist3d(const double* a, const double* b) {
+  const double d[3] = {__dsub_rn(a[0], b[0]), __dsub_rn(a[1], b[1]), __dsub_rn(a[2], b[2])};
+  return norm3d(d);
+}
+
+// per tet: grad u_h (J.inverse() rows, adapt.cpp:55-65) and the element term
+// a_tau^2 vol sum_q w_q (target - u_h)^2 (the estimator's own rule, adapt.cpp:67-76)
+template <int NQ>
+__global__ void est_tet_kernel(int nt, const int* __restrict__ tets, const double* __restrict__ xyz,
+                               const int* __restrict__ v2d, const double* __restrict__ coeffs, int kind,
+                               double isr, double* __restrict__ grad, double* __restrict__ eta_sq) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const int4 t4 = reinterpret_cast<const int4*>(tets)[t];
+  const int tv[4] = {t4.x, t4.y, t4.z, t4.w};
+  double V[4][3], nod[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) V[k][c] = xyz[3 * (int64_t)tv[k] + c];
+    const int d = v2d[tv[k]];
+    nod[k] = d >= 0 ? coeffs[d] : 0.0;
+  }
+  Geom G;
+  const bool ok = local_geom(V[0], V[1], V[2], V[3], G);
+  double g[3] = {0.0, 0.0, 0.0}, g0[3] = {0.0, 0.0, 0.0};
+  if (ok) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        g[c] = __dadd_rn(g[c], __dmul_rn(nod[i + 1], G.g[i + 1][c]));
+        g0[c] = __dsub_rn(g0[c], G.g[i + 1][c]);
+      }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) g[c] = __dadd_rn(g[c], __dmul_rn(nod[0], g0[c]));
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) grad[3 * (int64_t)t + c] = g[c];
+  double acc = 0.0;
+  for (int q = 0; q < NQ; ++q) {
+    const double* lam = NQ == 14 ? c_rules.p14[q] : c_rules.p64[q];
+    const double w = NQ == 14 ? c_rules.w14[q] : c_rules.w64[q];
+    double X[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s = __dadd_rn(s, __dmul_rn(lam[k], V[k][c]));
+      X[c] = s;
+    }
+    double u = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u = __dadd_rn(u, __dmul_rn(lam[k], nod[k]));
+    const double d = __dsub_rn(target_eval(kind, X[0], X[1], X[2], nullptr, 0), u);
+    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(w, d), d));
+  }
+  double h = 0.0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = a + 1; b < 4; ++b) h = fmax(h, dist3d(V[a], V[b]));
+  const double a_tau = fmin(__dmul_rn(h, isr), 1.0);
+  eta_sq[t] = __dmul_rn(__dmul_rn(__dmul_rn(a_tau, a_tau), ok ? G.vol : 0.0), acc);
+}
+
+// the 4 faces of tet t as sorted vertex triples (face l opposite local vertex l, adapt.cpp:86-97)
+__global__ void face_key_kernel(int nt, const int* __restrict__ tets, int* __restrict__ fk) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= 4 * (int64_t)nt) return;
+  const int t = (int)(f >> 2), l = (int)(f & 3);
+  int k[3], j = 0;
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+    if (v != l) k[j++] = tets[4 * (int64_t)t + v];
+  int a = min(k[0], min(k[1], k[2])), c = max(k[0], max(k[1], k[2]));
+  int b = max(min(k[0], k[1]), min(max(k[0], k[1]), k[2]));  // the median
+  fk[3 * f] = a;
+  fk[3 * f + 1] = b;
+  fk[3 * f + 2] = c;
+}
+
+__device__ __forceinline__ uint64_t face_hash(int a, int b, int c) {
+  uint64_t z = ((uint64_t)(uint32_t)a * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)(uint32_t)b * 0xC2B2AE3D27D4EB4Full) ^
+               ((uint64_t)(uint32_t)c * 0x165667B19E3779F9ull);
+  z = (z ^ (z >> 29)) * 0xBF58476D1CE4E5B9ull;
+  return z ^ (z >> 32);
+}
+
+// pairs the two faces of every interior face (a conforming mesh has at most two per key)
+__global__ void face_match_kernel(int64_t nf, const int* __restrict__ fk, int* slot, uint64_t mask, int* partner) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const int a = fk[3 * f], b = fk[3 * f + 1], c = fk[3 * f + 2];
+  uint64_t h = face_hash(a, b, c) & mask;
+  for (;;) {
+    const int prev = atomicCAS(slot + h, -1, (int)f);
+    if (prev == -1) return;
+    if (fk[3 * (int64_t)prev] == a && fk[3 * (int64_t)prev + 1] == b && fk[3 * (int64_t)prev + 2] == c) {
+      partner[f] = prev;
+      partner[prev] = (int)f;
+      return;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+// adapt.cpp:106-119: the face term, the same value for both sides (fa = the lower tet)
+__global__ void face_term_kernel(int64_t nf, const int* __restrict__ fk, const int* __restrict__ partner,
+                                 const double* __restrict__ xyz, const double* __restrict__ grad, double rho,
+                                 double isr, double* __restrict__ fterm) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const int p = partner[f];
+  if (p < 0 || p < f) return;
+  const int ta = (int)(f >> 2), tb = p >> 2;
+  double v[3][3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[k][c] = xyz[3 * (int64_t)fk[3 * f + k] + c];
+  double a[3], b[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    a[c] = __dsub_rn(v[1][c], v[0][c]);
+    b[c] = __dsub_rn(v[2][c], v[0][c]);
+  }
+  const double cr[3] = {__dsub_rn(__dmul_rn(a[1], b[2]), __dmul_rn(a[2], b[1])),
+                        __dsub_rn(__dmul_rn(a[2], b[0]), __dmul_rn(a[0], b[2])),
+                        __dsub_rn(__dmul_rn(a[0], b[1]), __dmul_rn(a[1], b[0]))};
+  const double cn = norm3d(cr);
+  const double area = __dmul_rn(0.5, cn);
+  const double sq = __dadd_rn(__dadd_rn(__dmul_rn(cr[0], cr[0]), __dmul_rn(cr[1], cr[1])), __dmul_rn(cr[2], cr[2]));
+  const double nr = __dsqrt_rn(sq);
+  double nn[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) nn[c] = sq > 0.0 ? __ddiv_rn(cr[c], nr) : cr[c];
+  double dg[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) dg[c] = __dsub_rn(grad[3 * (int64_t)ta + c], grad[3 * (int64_t)tb + c]);
+  const double jump = __dmul_rn(rho, dot3(dg, nn));
+  const double h_f = fmax(fmax(dist3d(v[0], v[1]), dist3d(v[1], v[2])), dist3d(v[0], v[2]));
+  const double a_f = fmin(__dmul_rn(h_f, isr), 1.0);
+  const double term =
+      __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(0.5, isr), a_f), area), jump), jump);
+  fterm[f] = term;
+  fterm[p] = term;
+}
+
+__device__ __forceinline__ bool key_less(const int* x, const int* y) {
+  return x[0] != y[0] ? x[0] < y[0] : x[1] != y[1] ? x[1] < y[1] : x[2] < y[2];
+}
+
+// eta_tau^2 += a tet's interior-face terms in ascending face-key order (the sorted face list of
+// adapt.cpp:98-121 visits a tet's faces in that order); per_tet = sqrt
+__global__ void est_finish_kernel(int nt, const int* __restrict__ fk, const int* __restrict__ partner,
+                                  const double* __restrict__ fterm, double* __restrict__ eta_sq,
+                                  double* __restrict__ per_tet) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  int ord[4] = {0, 1, 2, 3};
+  const int* k = fk + 12 * (int64_t)t;
+#pragma unroll
+  for (int i = 1; i < 4; ++i)
+    for (int j = i; j > 0 && key_less(k + 3 * ord[j], k + 3 * ord[j - 1]); --j) {
+      const int x = ord[j];
+      ord[j] = ord[j - 1];
+      ord[j - 1] = x;
+    }
+  double e = eta_sq[t];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t f = 4 * (int64_t)t + ord[i];
+    if (partner[f] >= 0) e = __dadd_rn(e, fterm[f]);
+  }
+  eta_sq[t] = e;
+  per_tet[t] = __dsqrt_rn(e);
+}
+
+// Eigen VectorXd::sum with SSE2 (Redux.h: two 2-lane packet accumulators), the oracle's eigen_sum:
+// lanes 0-3 run the four interleaved sequential sums, lane 0 combines them
+__global__ void eigen_sum_kernel(int64_t n, const double* __restrict__ a, double* out) {
+  __shared__ double acc[4];
+  const int l = threadIdx.x;
+  const int64_t aligned2 = (n / 4) * 4, aligned = (n / 2) * 2;
+  if (l < 4 && aligned > 2) {
+    double s = a[l];
+    for (int64_t i = 4 + l; i < aligned2; i += 4) s = __dadd_rn(s, a[i]);
+    acc[l] = s;
+  }
+  __syncthreads();
+  if (l != 0) return;
+  double res;
+  if (n <= 0) {
+    res = 0.0;
+  } else if (aligned) {
+    double p0a = a[0], p0b = a[1];
+    if (aligned > 2) {
+      p0a = __dadd_rn(acc[0], acc[2]);
+      p0b = __dadd_rn(acc[1], acc[3]);
+      if (aligned > aligned2) {
+        p0a = __dadd_rn(p0a, a[aligned2]);
+        p0b = __dadd_rn(p0b, a[aligned2 + 1]);
+      }
+    }
+    res = __dadd_rn(p0a, p0b);
+    for (int64_t i = aligned; i < n; ++i) res = __dadd_rn(res, a[i]);
+  } else {
+    res = a[0];
+  }
+  *out = res;
+}
+}  // namespace
+
+void estimate(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, int kind, double* per_tet,
+              double* eta_sq_out, double* global) {
+  if (kind < 0 || kind > RD_TARGET_QUADRATIC) throw Error(RD_EINVAL, "estimate: unknown target kind");
+  if (kind == RD_TARGET_SINE_RANDOM)
+    throw Error(RD_EINVAL, "estimate: the sine+random target is defined on a lattice, not on adapted meshes");
+  if (!(s.rho > 0.0)) throw Error(RD_EINVAL, "estimate: rho must be positive");
+  upload_rules(c);
+  const int nt = m.nt;
+  const int64_t nf = 4 * (int64_t)nt;
+  const double rho = s.rho, isr = 1.0 / std::sqrt(rho);
+  DBuf<double> grad(std::max<int64_t>(3 * (int64_t)nt, 1), c.stream), eta(std::max(nt, 1), c.stream),
+      fterm(std::max<int64_t>(nf, 1), c.stream), sum(1, c.stream);
+  DBuf<int> fk(std::max<int64_t>(3 * nf, 1), c.stream), partner(std::max<int64_t>(nf, 1), c.stream);
+  uint64_t H = 1024;
+  while (H < 2 * (uint64_t)nf) H <<= 1;
+  DBuf<int> slot(H, c.stream);
+  if (nt > 0) {
+    const bool disc = kind == RD_TARGET_BOX || kind == RD_TARGET_BALL;  // Smoothness::discontinuous
+    if (disc)
+      est_tet_kernel<64><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, s.v2d.p, coeffs, kind, isr,
+                                                                grad.p, eta.p);
+    else
+      est_tet_kernel<14><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, m.tets.p, m.xyz.p, s.v2d.p, coeffs, kind, isr,
+                                                                grad.p, eta.p);
+    RDG_LAUNCH_CHECK();
+    RDG_CUDA(cudaMemsetAsync(slot.p, 0xff, sizeof(int) * H, c.stream));
+    RDG_CUDA(cudaMemsetAsync(partner.p, 0xff, sizeof(int) * nf, c.stream));
+    face_key_kernel<<<div_up(nf, 256), 256, 0, c.stream>>>(nt, m.tets.p, fk.p);
+    face_match_kernel<<<div_up(nf, 256), 256, 0, c.stream>>>(nf, fk.p, slot.p, H - 1, partner.p);
+    face_term_kernel<<<div_up(nf, 256), 256, 0, c.stream>>>(nf, fk.p, partner.p, m.xyz.p, grad.p, rho, isr,
+                                                            fterm.p);
+    est_finish_kernel<<<div_up(nt, 256), 256, 0, c.stream>>>(nt, fk.p, partner.p, fterm.p, eta.p, per_tet);
+    RDG_LAUNCH_CHECK();
+    c.launches += 5;
+  }
+  eigen_sum_kernel<<<1, 32, 0, c.stream>>>(nt, eta.p, sum.p);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+  if (eta_sq_out && nt > 0)
+    RDG_CUDA(cudaMemcpyAsync(eta_sq_out, eta.p, sizeof(double) * nt, cudaMemcpyDeviceToDevice, c.stream));
+  double h = 0.0;
+  RDG_CUDA(cudaMemcpyAsync(&h, sum.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  RDG_CUDA(cudaStreamSynchronize(c.stream));
+  *global = std::sqrt(h);
+}
+
 }  // namespace rdg

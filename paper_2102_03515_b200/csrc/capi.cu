@@ -134,6 +134,72 @@ void require(bool ok, const char* msg) {
   if (!ok) throw Error(RD_EINVAL, msg);
 }
 
+// bench.cpp:55-63 target_dual_norm: r = f - M u (assembly.cpp:354-356), w = K^-1 r (dense LLT
+// for n <= 2000, assembly.cpp:342-347; else AMG(K)-PCG to 1e-11, bench.cpp:58-61), sqrt(r . w)
+double target_dual_norm_dev(Ctx& c, const DSystem& S, const double* u) {
+  const int n = S.n_dofs;
+  if (n == 0) return 0.0;
+  DBuf<double> r(n, c.stream), w(n, c.stream), rw(1, c.stream);
+  residual(c, S.M, S.f.p, u, r.p);
+  exact_retry(c, [&] {
+    if (n <= 2000) {
+      DBuf<double> Lk;
+      dense_llt(c, S.K, Lk);
+      dense_llt_solve(c, n, Lk.p, r.p, w.p);
+    } else {
+      Hierarchy hk;
+      build_hierarchy(c, S.K, 64, 1, hk);
+      pcg_device(c, S.K, &hk, r.p, 1e-11, 500, w.p, nullptr);
+    }
+    sync_and_raise(c);
+  });
+  dot(c, n, r.p, w.p, rw.p);
+  double h = 0.0;
+  RDG_CUDA(cudaMemcpyAsync(&h, rw.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  RDG_CUDA(cudaStreamSynchronize(c.stream));
+  if (h < 0.0) throw Error(RD_ERUNTIME, "hminus1_norm: negative dual pairing");
+  return std::sqrt(h);
+}
+
+void mesh_copy(Ctx& c, const DMesh& in, DMesh& out) {
+  out.nv = in.nv;
+  out.nt = in.nt;
+  out.lattice_n = in.lattice_n;
+  out.xyz.alloc(std::max<int64_t>(3 * (int64_t)in.nv, 1), c.stream);
+  out.boundary.alloc(std::max(in.nv, 1), c.stream);
+  out.tets.alloc(std::max<int64_t>(4 * (int64_t)in.nt, 4), c.stream);
+  if (in.nv) {
+    RDG_CUDA(cudaMemcpyAsync(out.xyz.p, in.xyz.p, sizeof(double) * 3 * (size_t)in.nv, cudaMemcpyDeviceToDevice,
+                             c.stream));
+    RDG_CUDA(cudaMemcpyAsync(out.boundary.p, in.boundary.p, (size_t)in.nv, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  if (in.nt)
+    RDG_CUDA(cudaMemcpyAsync(out.tets.p, in.tets.p, sizeof(int) * 4 * (size_t)in.nt, cudaMemcpyDeviceToDevice,
+                             c.stream));
+  if (in.tag.p && in.nt) {
+    out.tag.alloc(in.nt, c.stream);
+    out.gen.alloc(in.nt, c.stream);
+    RDG_CUDA(cudaMemcpyAsync(out.tag.p, in.tag.p, (size_t)in.nt, cudaMemcpyDeviceToDevice, c.stream));
+    RDG_CUDA(cudaMemcpyAsync(out.gen.p, in.gen.p, sizeof(int) * (size_t)in.nt, cudaMemcpyDeviceToDevice, c.stream));
+  }
+}
+
+int count_interior(Ctx& c, const DMesh& m) {  // mesh_stats(...).n_interior_dofs
+  std::vector<uint8_t> b((size_t)m.nv);
+  if (m.nv) RDG_CUDA(cudaMemcpyAsync(b.data(), m.boundary.p, (size_t)m.nv, cudaMemcpyDeviceToHost, c.stream));
+  RDG_CUDA(cudaStreamSynchronize(c.stream));
+  int k = 0;
+  for (uint8_t v : b) k += v ? 0 : 1;
+  return k;
+}
+
+rd_mesh* wrap_mesh(rd_ctx* ctx, DMesh&& m) {
+  auto h = std::make_unique<rd_mesh>();
+  h->ctx = ctx;
+  h->m = std::move(m);
+  return h.release();
+}
+
 }  // namespace
 
 struct rd_jacobi {
@@ -602,6 +668,164 @@ int rd_gpu_pcg(rd_ctx* ctx, const rd_csr* a, rd_amg* amg, const double* f, doubl
   });
 }
 
+// ------------------------------------------------------------ adaptivity (§8(f)3)
+int rd_gpu_mesh_tags(const rd_mesh* mesh, uint8_t* re, int32_t* gen) {
+  return guard(mesh ? mesh->ctx : nullptr, [&] {
+    require(mesh != nullptr, "mesh_tags: null mesh");
+    Ctx& c = mesh->ctx->c;
+    const DMesh& m = mesh->m;
+    if (!m.nt) return;
+    if (m.tag.p) {
+      if (re) RDG_CUDA(cudaMemcpyAsync(re, m.tag.p, (size_t)m.nt, cudaMemcpyDefault, c.stream));
+      if (gen) RDG_CUDA(cudaMemcpyAsync(gen, m.gen.p, sizeof(int) * (size_t)m.nt, cudaMemcpyDefault, c.stream));
+    } else {  // tag 3, generation 0 (mesh.cpp:60-61)
+      const std::vector<uint8_t> t3((size_t)m.nt, 3);
+      const std::vector<int32_t> g0((size_t)m.nt, 0);
+      if (re) RDG_CUDA(cudaMemcpyAsync(re, t3.data(), (size_t)m.nt, cudaMemcpyDefault, c.stream));
+      if (gen) RDG_CUDA(cudaMemcpyAsync(gen, g0.data(), sizeof(int) * (size_t)m.nt, cudaMemcpyDefault, c.stream));
+      RDG_CUDA(cudaStreamSynchronize(c.stream));
+      return;
+    }
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int rd_gpu_mesh_set_tags(rd_mesh* mesh, const uint8_t* re, const int32_t* gen) {
+  return guard(mesh ? mesh->ctx : nullptr, [&] {
+    require(mesh && re && gen, "mesh_set_tags: null argument");
+    Ctx& c = mesh->ctx->c;
+    DMesh& m = mesh->m;
+    if (!m.nt) return;
+    std::vector<uint8_t> hre((size_t)m.nt);
+    RDG_CUDA(cudaMemcpyAsync(hre.data(), re, (size_t)m.nt, cudaMemcpyDefault, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    for (uint8_t d : hre) require(d >= 1 && d <= 3, "mesh_set_tags: refinement edge tags must be 1, 2 or 3");
+    m.tag.alloc(m.nt, c.stream);
+    m.gen.alloc(m.nt, c.stream);
+    RDG_CUDA(cudaMemcpyAsync(m.tag.p, hre.data(), (size_t)m.nt, cudaMemcpyHostToDevice, c.stream));
+    RDG_CUDA(cudaMemcpyAsync(m.gen.p, gen, sizeof(int) * (size_t)m.nt, cudaMemcpyDefault, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int rd_gpu_bisect_marked(rd_ctx* ctx, const rd_mesh* mesh, int n_marked, const int32_t* marked, rd_mesh** out) {
+  return guard(ctx, [&] {
+    require(mesh && out && n_marked >= 0 && (marked || n_marked == 0), "bisect_marked: bad argument");
+    Ctx& c = ctx->c;
+    DBuf<int> tm;
+    const int* md = in_dev(c, marked, (size_t)n_marked, tm);
+    DMesh m;
+    bisect_marked(c, mesh->m, md, n_marked, m);
+    *out = wrap_mesh(ctx, std::move(m));
+  });
+}
+int rd_gpu_uniform_refine(rd_ctx* ctx, const rd_mesh* mesh, rd_mesh** out) {
+  return guard(ctx, [&] {
+    require(mesh && out, "uniform_refine: null argument");
+    Ctx& c = ctx->c;
+    DMesh cur;
+    mesh_copy(c, mesh->m, cur);
+    for (int sweep = 0; sweep < 3; ++sweep) {  // mesh.cpp:147-156: three full sweeps
+      DBuf<int> all(std::max(cur.nt, 1), c.stream);
+      std::vector<int> h((size_t)cur.nt);
+      for (int t = 0; t < cur.nt; ++t) h[(size_t)t] = t;
+      if (cur.nt) RDG_CUDA(cudaMemcpyAsync(all.p, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, c.stream));
+      DMesh next;
+      bisect_marked(c, cur, all.p, cur.nt, next);
+      cur = std::move(next);
+    }
+    *out = wrap_mesh(ctx, std::move(cur));
+  });
+}
+int rd_gpu_estimate(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, const double* coeffs,
+                    const rd_target* target, double* per_tet, double* global) {
+  return guard(ctx, [&] {
+    require(mesh && sys && target && per_tet && global && (coeffs || sys->s.n_dofs == 0), "estimate: null argument");
+    require(sys->s.nv == mesh->m.nv, "estimate: system does not belong to the mesh");
+    Ctx& c = ctx->c;
+    DBuf<double> tc;
+    const double* cd = in_dev(c, coeffs, sys->s.n_dofs, tc);
+    OutVec<double> po(c, per_tet, (size_t)mesh->m.nt);
+    estimate(c, mesh->m, sys->s, cd, target->kind, po.dev(), nullptr, global);
+    po.finish();
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int rd_gpu_mark_dorfler(rd_ctx* ctx, int n, const double* per_tet, double theta, int32_t* marked, int* n_marked) {
+  return guard(ctx, [&] {
+    require(n >= 0 && n_marked && (n == 0 || (per_tet && marked)), "mark_dorfler: bad argument");
+    Ctx& c = ctx->c;
+    DBuf<double> te;
+    const double* ed = in_dev(c, per_tet, (size_t)n, te);
+    OutVec<int> mo(c, marked, (size_t)n);
+    int k = 0;
+    mark_dorfler(c, n, ed, theta, mo.dev(), &k);
+    if (k) RDG_CUDA(cudaMemcpyAsync(marked, mo.dev(), sizeof(int) * (size_t)k, cudaMemcpyDefault, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    *n_marked = k;
+  });
+}
+int rd_gpu_adaptive_solve(rd_ctx* ctx, const rd_mesh* initial, const rd_target* target, double rho, int dof_budget,
+                          double tol, double theta, rd_adapt_level* history, int cap, int* n_levels,
+                          rd_mesh** final_mesh, double* coeffs, int coeffs_cap) {
+  return guard(ctx, [&] {
+    using clk = std::chrono::steady_clock;
+    require(initial && target && n_levels && (history || cap <= 0), "adaptive_solve: null argument");
+    require(rho > 0.0, "adaptive_solve: rho must be positive");
+    require(target->kind != RD_TARGET_SINE_RANDOM,
+            "adaptive_solve: the sine+random target is defined on a lattice, not on adapted meshes");
+    require(theta > 0.0 && theta <= 1.0, "mark_dorfler: theta must be in (0, 1]");
+    Ctx& c = ctx->c;
+    DMesh mesh;
+    mesh_copy(c, initial->m, mesh);
+    int level = 0, rows = 0;
+    for (;;) {
+      const auto t0 = clk::now();
+      DSystem sys;
+      build_system(c, mesh, rho, target->kind, target->seed, sys);
+      const int n = sys.n_dofs;
+      DBuf<double> x(std::max(n, 1), c.stream);
+      PcgResultDev res;
+      res.converged = true;
+      if (n > 0) {  // the solver: build_amg(A) then pcg(A, amg_precond, f, tol, 500)
+        exact_retry(c, [&] {
+          Hierarchy h;
+          build_hierarchy(c, sys.A, 64, 1, h, /*borrow=*/true);
+          res = pcg_device(c, sys.A, &h, sys.f.p, tol, 500, x.p, nullptr);
+          RDG_CUDA(cudaStreamSynchronize(c.stream));
+          sync_and_raise(c);
+        });
+      }
+      DBuf<double> per(std::max(mesh.nt, 1), c.stream);
+      double eta = 0.0;
+      estimate(c, mesh, sys, x.p, target->kind, per.p, nullptr, &eta);
+      const double l2_sq = l2_error_target_squared(c, mesh, sys, x.p, target->kind, target->seed);
+      const double hm1 = target_dual_norm_dev(c, sys, x.p);
+      rd_adapt_level row{level, n, res.iterations, eta, l2_sq, hm1 * hm1,
+                         std::chrono::duration<double>(clk::now() - t0).count()};
+      if (rows < cap) history[rows] = row;
+      ++rows;
+      *n_levels = rows;
+      if (n >= dof_budget) {
+        if (coeffs && n <= coeffs_cap && n > 0) {
+          RDG_CUDA(cudaMemcpyAsync(coeffs, x.p, sizeof(double) * (size_t)n, cudaMemcpyDefault, c.stream));
+          RDG_CUDA(cudaStreamSynchronize(c.stream));
+        }
+        if (final_mesh) *final_mesh = wrap_mesh(ctx, std::move(mesh));
+        return;
+      }
+      if (++level > 200) throw Error(RD_ERUNTIME, "adaptive_solve: level cap reached before the dof budget");
+      DBuf<int> marked(std::max(mesh.nt, 1), c.stream);
+      int k = 0;
+      mark_dorfler(c, mesh.nt, per.p, theta, marked.p, &k);
+      DMesh refined;
+      bisect_marked(c, mesh, marked.p, k, refined);
+      if (count_interior(c, refined) == n)
+        throw Error(RD_ERUNTIME, "adaptive_solve: refinement stagnated at level " + std::to_string(level - 1) + " (" +
+                                     std::to_string(n) + " dofs)");
+      mesh = std::move(refined);
+    }
+  });
+}
+
 // ------------------------------------------------------------ LinOp (linalg.hpp:11)
 int rd_gpu_linop_identity(rd_linop* out) {
   if (!out) return RD_EINVAL;
@@ -871,33 +1095,9 @@ int rd_gpu_target_dual_norm(rd_ctx* ctx, const rd_system* sys, const double* coe
   return guard(ctx, [&] {
     require(sys && coeffs && out, "target_dual_norm: null argument");
     Ctx& c = ctx->c;
-    const DSystem& S = sys->s;
-    const int n = S.n_dofs;
-    if (n == 0) {
-      *out = 0.0;
-      return;
-    }
-    DBuf<double> tc, r(n, c.stream), w(n, c.stream), rw(1, c.stream);
-    const double* u = in_dev(c, coeffs, n, tc);
-    residual(c, S.M, S.f.p, u, r.p);  // target_residual: f - M u (assembly.cpp:354-356)
-    exact_retry(c, [&] {
-      if (n <= 2000) {  // hminus1_norm's dense branch (assembly.cpp:342-347)
-        DBuf<double> Lk;
-        dense_llt(c, S.K, Lk);
-        dense_llt_solve(c, n, Lk.p, r.p, w.p);
-      } else {  // bench.cpp:58-61: AMG on K, PCG to 1e-11 from zero
-        Hierarchy hk;
-        build_hierarchy(c, S.K, 64, 1, hk);
-        pcg_device(c, S.K, &hk, r.p, 1e-11, 500, w.p, nullptr);
-      }
-      sync_and_raise(c);
-    });
-    dot(c, n, r.p, w.p, rw.p);
-    double h = 0.0;
-    RDG_CUDA(cudaMemcpyAsync(&h, rw.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-    RDG_CUDA(cudaStreamSynchronize(c.stream));
-    if (h < 0.0) throw Error(RD_ERUNTIME, "hminus1_norm: negative dual pairing");
-    *out = std::sqrt(h);
+    DBuf<double> tc;
+    const double* u = in_dev(c, coeffs, sys->s.n_dofs, tc);
+    *out = target_dual_norm_dev(c, sys->s, u);
   });
 }
 

@@ -181,6 +181,10 @@ struct DMesh {
   DBuf<double> xyz;
   DBuf<int> tets;
   DBuf<uint8_t> boundary;
+  // bisection state (mesh.hpp:17-20): refinement edge (0, tag) and generation per tet; empty
+  // for build_structured_cube / uploaded meshes, which carry tag 3 and generation 0
+  DBuf<uint8_t> tag;
+  DBuf<int> gen;
 };
 
 struct DSystem {
@@ -208,6 +212,13 @@ void error_norms_target(Ctx& c, const DMesh& m, const DSystem& s, const double* 
 // assembly.cpp:312-331: squared L2 distance of the P1 field to the target (the target's rule)
 double l2_error_target_squared(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, int kind,
                                uint64_t seed);
+// adapt.cu -- adapt.cpp:126-150 (marked: device, >= n ints; *count on the host) and
+// mesh.cpp:67-145 (out: a new mesh; marked: device ids)
+void mark_dorfler(Ctx& c, int n, const double* eta, double theta, int* marked, int* count);
+void bisect_marked(Ctx& c, const DMesh& in, const int* marked, int n_marked, DMesh& out);
+// adapt.cpp:35-124: per_tet (device, n_tets) = eta_tau, optional eta_tau^2 copy, global = sqrt(sum eta^2)
+void estimate(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, int kind, double* per_tet,
+              double* eta_sq_out, double* global);
 
 }  // namespace rdg
 

@@ -141,6 +141,13 @@ def lib():
         "rd_gpu_dot_async": (_I, [_P, _I, _P, _P, _P]),
         "rd_gpu_pcg_update_xr": (_I, [_P, C.c_int64, _D, _P, _P, _P, _P]),
         "rd_gpu_pcg_update_p": (_I, [_P, C.c_int64, _D, _P, _P]),
+        "rd_gpu_mesh_tags": (_I, [_P, _P, _P]),
+        "rd_gpu_mesh_set_tags": (_I, [_P, _P, _P]),
+        "rd_gpu_bisect_marked": (_I, [_P, _P, _I, _P, _P]),
+        "rd_gpu_uniform_refine": (_I, [_P, _P, _P]),
+        "rd_gpu_estimate": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+        "rd_gpu_mark_dorfler": (_I, [_P, _I, _P, _D, _P, _P]),
+        "rd_gpu_adaptive_solve": (_I, [_P, _P, _P, _D, _I, _D, _D, _P, _I, _P, _P, _P, _I]),
         "rd_gpu_linop_identity": (_I, [_P]),
         "rd_gpu_linop_csr": (_I, [_P, _P]),
         "rd_gpu_linop_amg": (_I, [_P, _P]),
@@ -192,6 +199,11 @@ class _SolveOutcome(C.Structure):
 
 class _Target(C.Structure):
     _fields_ = [("kind", C.c_int), ("seed", C.c_uint64)]
+
+
+class _AdaptLevel(C.Structure):
+    _fields_ = [("level", C.c_int), ("dofs", C.c_int), ("iterations", C.c_int), ("eta", C.c_double),
+                ("err_l2_sq", C.c_double), ("err_hm1_sq", C.c_double), ("seconds", C.c_double)]
 
 
 def _ptr(x):
@@ -344,6 +356,18 @@ class TetMesh:
         b = np.zeros(max(self.n_vertices, 1), np.uint8)
         self.ctx.check(lib().rd_gpu_mesh_download(self.h, _ptr(xyz), _ptr(tets), _ptr(b)))
         return xyz[: self.n_vertices], tets[: self.n_tets], b[: self.n_vertices]
+
+    def tags(self):
+        """mesh.hpp:17-20: (refinement_edge u8[n_tets], generation i32[n_tets])."""
+        re = np.zeros(max(self.n_tets, 1), np.uint8)
+        gen = np.zeros(max(self.n_tets, 1), np.int32)
+        self.ctx.check(lib().rd_gpu_mesh_tags(self.h, _ptr(re), _ptr(gen)))
+        return re[: self.n_tets], gen[: self.n_tets]
+
+    def set_tags(self, refinement_edge, generation):
+        re = np.ascontiguousarray(refinement_edge, np.uint8)
+        gen = np.ascontiguousarray(generation, np.int32)
+        self.ctx.check(lib().rd_gpu_mesh_set_tags(self.h, _ptr(re), _ptr(gen)))
 
     def __del__(self):
         try:
@@ -795,3 +819,67 @@ def solve_system_amg(A: Csr, f, tol: float = 1e-8, u=None) -> SolveOutcome:
     A.ctx.check(lib().rd_gpu_solve_system_amg(A.ctx.h, A.h, _ptr(f), float(tol), _ptr(u), C.byref(out)))
     return SolveOutcome(u[: A.rows] if host else u, out.iterations, bool(out.converged), out.setup_seconds,
                         out.solve_seconds)
+
+
+# ------------------------------------------------------------------ adaptivity
+def bisect_marked(mesh: TetMesh, marked) -> TetMesh:
+    """mesh.hpp:44 / mesh.cpp:67-145 on the device."""
+    mk = np.ascontiguousarray(marked, np.int32).reshape(-1)
+    h = _P()
+    mesh.ctx.check(lib().rd_gpu_bisect_marked(mesh.ctx.h, mesh.h, mk.size, _ptr(mk) if mk.size else None,
+                                              C.byref(h)))
+    return TetMesh(h, mesh.ctx)
+
+
+def uniform_refine(mesh: TetMesh) -> TetMesh:
+    """mesh.hpp:40 / mesh.cpp:147-156 on the device."""
+    h = _P()
+    mesh.ctx.check(lib().rd_gpu_uniform_refine(mesh.ctx.h, mesh.h, C.byref(h)))
+    return TetMesh(h, mesh.ctx)
+
+
+def estimate(sys: FemSystem, coeffs, target: str, seed: int = 0):
+    """adapt.hpp:21 / adapt.cpp:35-124 on the device -> (per_tet, global)."""
+    coeffs = np.ascontiguousarray(coeffs, np.float64)
+    if coeffs.size != sys.n_dofs:
+        raise RdInvalidArgument("estimate: coefficient vector size mismatch")
+    per = np.zeros(max(sys.mesh.n_tets, 1))
+    g = C.c_double()
+    t = _Target(TARGETS[target], int(seed))
+    sys.ctx.check(lib().rd_gpu_estimate(sys.ctx.h, sys.mesh.h, sys.h, _ptr(coeffs) if coeffs.size else None,
+                                        C.byref(t), _ptr(per), C.byref(g)))
+    return per[: sys.mesh.n_tets], g.value
+
+
+def mark_dorfler(eta, theta: float, ctx: Context | None = None) -> np.ndarray:
+    """adapt.hpp:24 / adapt.cpp:126-150 on the device -> marked tets in marking order."""
+    ctx = ctx or default_context()
+    eta = np.ascontiguousarray(eta, np.float64)
+    out = np.zeros(max(eta.size, 1), np.int32)
+    k = C.c_int()
+    ctx.check(lib().rd_gpu_mark_dorfler(ctx.h, eta.size, _ptr(eta) if eta.size else None, float(theta), _ptr(out),
+                                        C.byref(k)))
+    return out[: k.value]
+
+
+@dataclass
+class AdaptResult:
+    history: list
+    mesh: TetMesh
+    coefficients: np.ndarray
+
+
+def adaptive_solve(initial: TetMesh, target: str, rho: float, dof_budget: int, tol: float = 1e-8,
+                   theta: float = 0.5, seed: int = 0, cap: int = 256, coeffs_cap: int = 1 << 24) -> AdaptResult:
+    """adapt.hpp:44-47 / adapt.cpp:152-205 on the device, with the AMG solver (build_amg + pcg(tol, 500))."""
+    ctx = initial.ctx
+    hist = (_AdaptLevel * cap)()
+    k = C.c_int()
+    fm = _P()
+    co = np.zeros(coeffs_cap)
+    t = _Target(TARGETS[target], int(seed))
+    ctx.check(lib().rd_gpu_adaptive_solve(ctx.h, initial.h, C.byref(t), float(rho), int(dof_budget), float(tol),
+                                          float(theta), hist, cap, C.byref(k), C.byref(fm), _ptr(co), coeffs_cap))
+    rows = [dict(level=r.level, dofs=r.dofs, iterations=r.iterations, eta=r.eta, err_l2_sq=r.err_l2_sq,
+                 err_hm1_sq=r.err_hm1_sq, seconds=r.seconds) for r in hist[: min(k.value, cap)]]
+    return AdaptResult(rows, TetMesh(fm, ctx), co[: rows[-1]["dofs"]].copy())
