@@ -7,6 +7,7 @@
 // std::runtime_error (subclass rd_gpu::Error keeps the code).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <functional>
 #include <memory>
@@ -106,6 +107,32 @@ class TetMesh {
   int n_vertices() const { int v; rd_gpu_mesh_info(get(), &v, nullptr, nullptr); return v; }
   int n_tets() const { int t; rd_gpu_mesh_info(get(), nullptr, &t, nullptr); return t; }
   Context& context() const { return *ctx_; }
+  // mesh.hpp:13-24 arrays on the host
+  std::vector<double> vertices() const {
+    std::vector<double> x(3 * (size_t)n_vertices());
+    check(rd_gpu_mesh_download(get(), x.data(), nullptr, nullptr), ctx_->get());
+    return x;
+  }
+  std::vector<int32_t> tets() const {
+    std::vector<int32_t> t(4 * (size_t)n_tets());
+    check(rd_gpu_mesh_download(get(), nullptr, t.data(), nullptr), ctx_->get());
+    return t;
+  }
+  std::vector<uint8_t> boundary_vertex() const {
+    std::vector<uint8_t> b((size_t)n_vertices());
+    check(rd_gpu_mesh_download(get(), nullptr, nullptr, b.data()), ctx_->get());
+    return b;
+  }
+  std::vector<uint8_t> refinement_edge() const {
+    std::vector<uint8_t> r((size_t)n_tets());
+    check(rd_gpu_mesh_tags(get(), r.data(), nullptr), ctx_->get());
+    return r;
+  }
+  std::vector<int32_t> generation() const {
+    std::vector<int32_t> g((size_t)n_tets());
+    check(rd_gpu_mesh_tags(get(), nullptr, g.data()), ctx_->get());
+    return g;
+  }
 
  private:
   Context* ctx_;
@@ -363,6 +390,82 @@ inline PcgResult pcg(const LinOp& apply_A, const LinOp& apply_P, const std::vect
 inline PcgResult pcg(const DeviceMatrix& A, const LinOp& apply_P, const std::vector<double>& f, double tol = 1e-8,
                      int max_iter = 500) {
   return pcg(spmv_op(A), apply_P, f, tol, max_iter);
+}
+
+// ------------------------------------------------------------------ adaptivity (adapt.hpp, mesh.hpp:40-44)
+// mesh.hpp:44 bisect_marked: throws std::invalid_argument for an id outside [0, n_tets)
+inline TetMesh bisect_marked(const TetMesh& mesh, const std::vector<int>& marked) {
+  rd_mesh* h = nullptr;
+  check(rd_gpu_bisect_marked(mesh.context().get(), mesh.get(), (int)marked.size(),
+                             marked.empty() ? nullptr : marked.data(), &h),
+        mesh.context().get());
+  return TetMesh(mesh.context(), h);
+}
+// mesh.hpp:40 uniform_refine
+inline TetMesh uniform_refine(const TetMesh& mesh) {
+  rd_mesh* h = nullptr;
+  check(rd_gpu_uniform_refine(mesh.context().get(), mesh.get(), &h), mesh.context().get());
+  return TetMesh(mesh.context(), h);
+}
+// adapt.hpp:13-21
+struct Estimate {
+  std::vector<double> per_tet;
+  double global = 0.0;
+};
+inline Estimate estimate(const TetMesh& mesh, const FemSystem& sys, const std::vector<double>& coeffs, Target target,
+                         uint64_t seed = 0) {
+  if ((int)coeffs.size() != sys.n_dofs()) throw std::invalid_argument("estimate: coefficient size mismatch");
+  Estimate e;
+  e.per_tet.resize((size_t)mesh.n_tets());
+  const rd_target t{static_cast<int>(target), seed};
+  check(rd_gpu_estimate(mesh.context().get(), mesh.get(), sys.get(), coeffs.empty() ? nullptr : coeffs.data(), &t,
+                        e.per_tet.empty() ? nullptr : e.per_tet.data(), &e.global),
+        mesh.context().get());
+  return e;
+}
+// adapt.hpp:24
+inline std::vector<int> mark_dorfler(const Estimate& est, double theta, Context& ctx = default_context()) {
+  std::vector<int> m(est.per_tet.size());
+  int k = 0;
+  check(rd_gpu_mark_dorfler(ctx.get(), (int)est.per_tet.size(), est.per_tet.empty() ? nullptr : est.per_tet.data(),
+                            theta, m.empty() ? nullptr : m.data(), &k),
+        ctx.get());
+  m.resize((size_t)k);
+  return m;
+}
+// adapt.hpp:26-42
+struct AdaptLevel {
+  int level = 0, dofs = 0;
+  double eta = 0.0, err_l2_sq = 0.0, err_hm1_sq = 0.0;
+  int iterations = 0;
+  double seconds = 0.0;
+};
+struct AdaptResult {
+  TetMesh mesh;
+  std::vector<double> coefficients;
+  std::vector<AdaptLevel> history;
+};
+// adapt.hpp:44-47 with the AMG SystemSolver of bench.cpp:65-74 (solve_system, PrecondKind::amg, tol)
+inline AdaptResult adaptive_solve(const TetMesh& initial, Target target, double rho, int dof_budget, double tol,
+                                  double theta = 0.5, uint64_t seed = 0) {
+  Context& ctx = initial.context();
+  std::vector<rd_adapt_level> rows(256);
+  int nl = 0;
+  rd_mesh* fm = nullptr;
+  std::vector<double> co(std::max(dof_budget, 1) * (size_t)16 + 4096);
+  const rd_target t{static_cast<int>(target), seed};
+  int rc = rd_gpu_adaptive_solve(ctx.get(), initial.get(), &t, rho, dof_budget, tol, theta, rows.data(),
+                                 (int)rows.size(), &nl, &fm, co.data(), (int)co.size());
+  check(rc, ctx.get());
+  AdaptResult out{TetMesh(ctx, fm), {}, {}};
+  for (int k = 0; k < nl && k < (int)rows.size(); ++k) {
+    const rd_adapt_level& r = rows[(size_t)k];
+    out.history.push_back(AdaptLevel{r.level, r.dofs, r.eta, r.err_l2_sq, r.err_hm1_sq, r.iterations, r.seconds});
+  }
+  const int nd = out.history.empty() ? 0 : out.history.back().dofs;
+  if (nd > (int)co.size()) throw std::runtime_error("adaptive_solve: final solution larger than the staging buffer");
+  out.coefficients.assign(co.begin(), co.begin() + nd);
+  return out;
 }
 
 // bench.hpp:48-57 SolveOutcome / solve_system(..., PrecondKind::amg, ...)

@@ -408,6 +408,63 @@ inline EocTable run_precond_bench(const ExperimentConfig& cfg, Context* ctx_opt 
   return t;
 }
 
+// ------------------------------------------------------------------ adaptive experiment (bench.cpp:425-474)
+inline double eoc_generic(double e_prev, double e_cur, double x_prev, double x_cur) {  // bench.cpp:243-249
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  if (!(e_prev > 0.0) || !(e_cur > 0.0) || !(x_prev > 0.0) || !(x_cur > 0.0)) return nan;
+  const double d = std::log(x_prev / x_cur);
+  if (d == 0.0) return nan;
+  return std::log(e_prev / e_cur) / d;
+}
+
+// bench.cpp:425-449: per rho, adaptive_solve from build_structured_cube(8) with the configured
+// solver (the device path serves AMG), one row per level
+inline EocTable run_adaptive_experiment(const ExperimentConfig& cfg, Context* ctx_opt = nullptr) {
+  validate(cfg);
+  if (cfg.example == ExampleKind::smooth)
+    throw std::invalid_argument("adaptive experiment needs the box or nonzero_bc example");
+  if (cfg.dof_budget < 1) throw std::invalid_argument("adaptive experiment needs a dof budget");
+  if (cfg.precond != PrecondKind::amg)
+    throw std::invalid_argument("adaptive experiment: the device path serves the amg solver (" +
+                                precond_name(cfg.precond) + " requested)");
+  const Target target = make_target(cfg.example);
+  Context& ctx = ctx_opt ? *ctx_opt : default_context();
+  const TetMesh initial = build_structured_cube(8, ctx);
+  EocTable t;
+  t.columns = {"rho", "level", "dofs", "eta", "l2_sq", "hm1_sq", "iterations", "seconds"};
+  for (double rho : cfg.rho_list) {
+    const AdaptResult res = adaptive_solve(initial, target, rho, cfg.dof_budget, cfg.tol, cfg.theta);
+    for (const AdaptLevel& lv : res.history)
+      t.rows.push_back({rho, double(lv.level), double(lv.dofs), lv.eta, lv.err_l2_sq, lv.err_hm1_sq,
+                        double(lv.iterations), lv.seconds});
+  }
+  return t;
+}
+
+// bench.cpp:451-474: the last level of every rho group, with eoc columns over rho
+inline EocTable adaptive_rho_summary(const EocTable& levels) {
+  const int rc = column_index(levels, "rho"), dc = column_index(levels, "dofs");
+  const int lc = column_index(levels, "l2_sq"), hc = column_index(levels, "hm1_sq");
+  EocTable t;
+  t.columns = {"rho", "dofs", "l2_sq", "l2_eoc", "hm1_sq", "hm1_eoc"};
+  std::vector<std::vector<double>> finals;
+  for (size_t i = 0; i < levels.rows.size(); ++i) {
+    const bool last = i + 1 == levels.rows.size() || levels.rows[i + 1][(size_t)rc] != levels.rows[i][(size_t)rc];
+    if (last) finals.push_back(levels.rows[i]);
+  }
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  double prev_rho = nan, prev_l2 = nan, prev_hm1 = nan;
+  for (const auto& row : finals) {
+    const double rho = row[(size_t)rc], l2 = row[(size_t)lc], hm1 = row[(size_t)hc];
+    t.rows.push_back({rho, row[(size_t)dc], l2, eoc_generic(prev_l2, l2, prev_rho, rho), hm1,
+                      eoc_generic(prev_hm1, hm1, prev_rho, rho)});
+    prev_rho = rho;
+    prev_l2 = l2;
+    prev_hm1 = hm1;
+  }
+  return t;
+}
+
 // ------------------------------------------------------------------ MatrixMarket (io.cpp)
 namespace detail {
 inline std::string fmt17(double v) {  // io.cpp:14-18

@@ -1,15 +1,16 @@
-// rdbench -- the reference CLI's bench-precond subcommand (tools/rdbench.cpp:76-113, exit
-// codes :121-125, :186-190) on the device path, through include/rd_gpu_harness.hpp.
+// rdbench -- the reference CLI's bench-precond and adapt subcommands (tools/rdbench.cpp:76-151,
+// exit codes :121-125, :186-190) on the device path, through include/rd_gpu_harness.hpp.
 //
-//   rdbench bench-precond [--rho R...] [--n N...] [--precond amg] [--tol T] [--threads K]
+//   rdbench bench-precond|adapt [--rho R...] [--n N...] [--precond amg] [--tol T] [--threads K]
 //                         [--seed S] [--out PATH] [--example smooth|box|nonzero_bc] [--p P]
 //                         [--budget B] [--theta X] [--gnuplot] [--config FILE.json]
 //
-// Defaults are the reference's (rho 1..1e-12, n 8 16 32, amg, tol 1e-8).  Output: the CSV
-// of run_precond_bench (or --gnuplot blocks) to stdout or --out.  Exit codes as the
-// reference: 0 all rows converged, 1 some row did not (the run still completes), 2 an
-// exception (bad config, device error).  Other subcommands (table-h, table-rho, adapt,
-// export-vtk) drive BDDC / adaptivity / VTK, which are not part of the device path: exit 2.
+// Defaults are the reference's (bench-precond: rho 1..1e-12, n 8 16 32, amg, tol 1e-8; adapt: rho
+// 1e-2 1e-3 1e-4, budget 200000, box).  Output: the CSV of run_precond_bench, or the adaptive
+// level history plus its eoc summary (or --gnuplot blocks), to stdout or --out.  Exit codes as
+// the reference: 0 all rows converged, 1 some bench-precond row did not (the run still
+// completes), 2 an exception (bad config, device error).  table-h, table-rho and export-vtk
+// (convergence tables, VTK) are not part of the device path: exit 2.
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -61,7 +62,7 @@ long long to_i(const std::string& s) {
 }
 
 void usage() {
-  std::cerr << "usage: rdbench bench-precond [--rho R...] [--n N...] [--precond amg] [--tol T]\n"
+  std::cerr << "usage: rdbench bench-precond|adapt [--rho R...] [--n N...] [--precond amg] [--tol T]\n"
                "                             [--threads K] [--seed S] [--out PATH] [--example NAME]\n"
                "                             [--p P] [--budget B] [--theta X] [--gnuplot] [--config FILE]\n";
 }
@@ -76,13 +77,20 @@ int main(int argc, char** argv) {
   }
   try {
     const std::string cmd = args[0];
-    if (cmd == "table-h" || cmd == "table-rho" || cmd == "adapt" || cmd == "export-vtk")
-      throw std::invalid_argument(cmd + " is not part of the device path (BDDC / adaptivity / VTK)");
-    if (cmd != "bench-precond") throw std::invalid_argument("unknown subcommand " + cmd);
-    rd_gpu::ExperimentConfig cfg;  // rdbench.cpp:94-97 defaults
-    cfg.rho_list = {1.0, 1e-2, 1e-4, 1e-6, 1e-8, 1e-10, 1e-12};
-    cfg.n_list = {8, 16, 32};
+    if (cmd == "table-h" || cmd == "table-rho" || cmd == "export-vtk")
+      throw std::invalid_argument(cmd + " is not part of the device path (convergence tables / VTK)");
+    if (cmd != "bench-precond" && cmd != "adapt") throw std::invalid_argument("unknown subcommand " + cmd);
+    const bool adapt = cmd == "adapt";
+    rd_gpu::ExperimentConfig cfg;
     std::string precond = "amg", example = "smooth";
+    if (adapt) {  // rdbench.cpp:99-104 defaults
+      cfg.rho_list = {1e-2, 1e-3, 1e-4};
+      cfg.dof_budget = 200000;
+      example = "box";
+    } else {  // rdbench.cpp:94-97 defaults
+      cfg.rho_list = {1.0, 1e-2, 1e-4, 1e-6, 1e-8, 1e-10, 1e-12};
+      cfg.n_list = {8, 16, 32};
+    }
     for (size_t k = 1; k < args.size(); ++k) {
       const std::string& a = args[k];
       if (a == "--rho") {
@@ -126,6 +134,17 @@ int main(int argc, char** argv) {
     cfg.precond = rd_gpu::precond_from_name(precond);  // rdbench.cpp:55-59 finish()
     cfg.example = rd_gpu::example_from_name(example);
     rd_gpu::validate(cfg);
+    if (adapt) {  // rdbench.cpp:140-151: the level history, then the eoc summary
+      const rd_gpu::EocTable t = rd_gpu::run_adaptive_experiment(cfg);
+      std::string text;
+      if (cfg.gnuplot) {
+        text = rd_gpu::gnuplot_blocks(t, "rho");
+      } else {
+        text = rd_gpu::to_csv(t) + "\n" + rd_gpu::to_csv(rd_gpu::adaptive_rho_summary(t));
+      }
+      emit(text, cfg.output);
+      return 0;
+    }
     const rd_gpu::EocTable t = rd_gpu::run_precond_bench(cfg);
     emit(cfg.gnuplot ? rd_gpu::gnuplot_blocks(t, "rho") : rd_gpu::to_csv(t), cfg.output);
     const int bad = rd_gpu::failed_rows(t);

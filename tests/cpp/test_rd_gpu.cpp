@@ -201,6 +201,53 @@ int main() {
     auto r1 = pcg(from_dense(ctx, 1, {2.0}), identity_precond(), std::vector<double>{4.0}, 1e-12, 10);
     CHECK(r1.report.converged && r1.report.iterations == 1 && std::fabs(r1.x[0] - 2.0) < 1e-14);
   }
+  {  // mesh.hpp:40-44, adapt.hpp (test_mesh.cpp:92-150, test_adapt.cpp:105-161 through the C++ layer)
+    auto mesh = build_structured_cube(2, ctx);
+    auto out = bisect_marked(mesh, {5});
+    CHECK(out.n_tets() > mesh.n_tets() && out.n_vertices() > mesh.n_vertices());
+    auto all = bisect_marked(mesh, [&] {
+      std::vector<int> a(mesh.n_tets());
+      for (int t = 0; t < mesh.n_tets(); ++t) a[t] = t;
+      return a;
+    }());
+    CHECK(all.n_tets() == 2 * mesh.n_tets());
+    bool gen1 = true;
+    for (int g : all.generation()) gen1 = gen1 && g == 1;
+    CHECK(gen1);
+    bool threw = false;
+    try {
+      bisect_marked(build_structured_cube(1, ctx), {6});
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    auto fine = uniform_refine(build_structured_cube(1, ctx));
+    CHECK(fine.n_tets() == 48 && fine.n_vertices() == 27);
+    Estimate hand;
+    hand.per_tet = {3.0, 2.0, 2.0, 1.0};
+    CHECK(mark_dorfler(hand, 0.6).size() == 1);
+    hand.per_tet = {1.0, 0.0, 2.0, 0.0, 0.5};
+    CHECK(mark_dorfler(hand, 1.0) == std::vector<int>({2, 0, 4}));
+    auto sys = build_system(build_structured_cube(4, ctx), 1e-2, Target::box);
+    auto m4 = build_structured_cube(4, ctx);
+    auto s4 = build_system(m4, 1e-2, Target::box);
+    auto u = pcg(s4.A, amg_precond(AmgHierarchy(s4.A)), s4.f(), 1e-10, 500).x;
+    Estimate e = estimate(m4, s4, u, Target::box);
+    double sq = 0.0;
+    bool nonneg = true;
+    for (double v : e.per_tet) {
+      nonneg = nonneg && v >= 0.0;
+      sq += v * v;
+    }
+    CHECK(nonneg && e.global > 0.0 && std::fabs(e.global - std::sqrt(sq)) <= 1e-13 * e.global);
+    AdaptResult res = adaptive_solve(build_structured_cube(4, ctx), Target::box, 1e-2, 800, 1e-10);
+    CHECK(res.history.size() >= 2 && res.history.back().dofs >= 800);
+    CHECK((int)res.coefficients.size() == res.history.back().dofs);
+    CHECK(res.history.back().eta < res.history.front().eta);
+    std::printf("adaptive: %zu levels, %d dofs, eta %.6g -> %.6g\n", res.history.size(), res.history.back().dofs,
+                res.history.front().eta, res.history.back().eta);
+    (void)sys;
+  }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail;
 }

@@ -30,7 +30,8 @@ def test_harness_host_checks(tmp_path):
 @pytest.mark.parametrize("args", [["bench-precond", "--rho", "-1"], ["bench-precond", "--n", "0"],
                                   ["bench-precond", "--tol", "0"], ["bench-precond", "--precond", "jacobi"],
                                   ["bench-precond", "--precond", "ilu"], ["bench-precond", "--example", "ball"],
-                                  ["bench-precond", "--bogus"], ["table-h"], ["adapt"], ["nope"], []])
+                                  ["bench-precond", "--bogus"], ["table-h"], ["adapt", "--example", "smooth"],
+                                  ["adapt", "--budget", "0"], ["adapt", "--precond", "jacobi"], ["nope"], []])
 def test_rdbench_rejects_with_exit_2(args):
     """Rejected configs raise std::invalid_argument before any device work: exit code 2 and an
     'error:' line (rdbench.cpp:186-190); the other subcommands are outside the device path."""
@@ -76,3 +77,28 @@ def test_rdbench_unattainable_tolerance(tmp_path, n):
     else:
         rows = [l.split() for l in out.stdout.splitlines() if l and not l.startswith("#")]
         assert len(rows) == 1 and rows[0][4] == "1", out.stdout
+
+
+@pytest.mark.gpu
+def test_rdbench_adapt(O, tmp_path):
+    """rdbench adapt (rdbench.cpp:99-104, 140-151; bench.cpp:425-474): the level history per rho,
+    a blank line, then the eoc summary; the history matches the oracle's adaptive_solve from
+    build_structured_cube(8) level for level (dofs and iterations equal; the columns agree to the
+    CSV's %.6e, i.e. within 1e-6 relative)."""
+    path = tmp_path / "adapt.csv"
+    out = subprocess.run([_built(RDBENCH), "adapt", "--rho", "1e-2", "--budget", "3000", "--tol", "1e-10",
+                          "--out", str(path)], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    hist_text, summ_text = path.read_text().split("\n\n")
+    rows = list(csv.DictReader(io.StringIO(hist_text)))
+    summ = list(csv.DictReader(io.StringIO(summ_text)))
+    assert list(rows[0].keys()) == ["rho", "level", "dofs", "eta", "l2_sq", "hm1_sq", "iterations", "seconds"]
+    assert list(summ[0].keys()) == ["rho", "dofs", "l2_sq", "l2_eoc", "hm1_sq", "hm1_eoc"]
+    orows, _, _ = O.adaptive_solve(O.build_structured_cube(8), "box", 1e-2, 3000, tol=1e-10)
+    assert len(rows) == len(orows) >= 2
+    for r, o in zip(rows, orows):
+        assert int(r["level"]) == o["level"] and int(r["dofs"]) == o["dofs"]
+        assert int(r["iterations"]) == o["iterations"]
+        for k, ok in (("eta", "eta"), ("l2_sq", "err_l2_sq"), ("hm1_sq", "err_hm1_sq")):
+            assert float(r[k]) == pytest.approx(o[ok], rel=1e-6), k
+    assert int(summ[0]["dofs"]) == orows[-1]["dofs"]
