@@ -627,7 +627,37 @@ def generic_legs(ctx, stream, n=N_DEFAULT):
             del s, h, mesh, u
         except Exception as ex:  # reported, never fatal for the headline line
             out.append({"config": name, "error": str(ex)[:200]})
+    out.append(adaptive_leg(ctx, stream))
     return out
+
+
+def adaptive_leg(ctx, stream, budget=200000, rho=1e-2):
+    """rdbench adapt's loop (rdbench.cpp:99-104: box target, budget 200,000 dofs)
+    from build_structured_cube(8) on the device -- per level build_system (generic assembly on the
+    bisected mesh), AMG setup + PCG, estimator, error norms, H^-1 dual norm, Dorfler marking and
+    newest-vertex bisection.  One warm-up run, then one timed run (CUDA events)."""
+    import torch
+
+    from paper_2102_03515_b200 import rd
+
+    try:
+        init = rd.build_structured_cube(8, ctx)
+        rd.adaptive_solve(init, "box", rho, budget, tol=TOL)
+        ctx.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        res = rd.adaptive_solve(init, "box", rho, budget, tol=TOL)
+        e.record(stream)
+        torch.cuda.synchronize()
+        h = res.history
+        return {"config": "adaptive_box", "what": "adaptive_solve(cube(8), box, rho=1e-2, budget 200000, AMG tol "
+                "1e-8, theta 0.5): every level on the generic path", "levels": len(h), "final_dofs": h[-1]["dofs"],
+                "ms_total": a.elapsed_time(e), "iterations": [r["iterations"] for r in h],
+                "dofs": [r["dofs"] for r in h], "seconds_per_level": [round(r["seconds"], 5) for r in h],
+                "eta": [h[0]["eta"], h[-1]["eta"]]}
+    except Exception as ex:  # reported, never fatal for the headline line
+        return {"config": "adaptive_box", "error": str(ex)[:200]}
 
 
 def host_info():

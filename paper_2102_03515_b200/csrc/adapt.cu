@@ -187,23 +187,52 @@ __global__ void fill_u8_kernel(int64_t n, uint8_t v, uint8_t* a) {
   if (i < n) a[i] = v;
 }
 
-// adapt.cpp:139-149 in sorted order: total, goal = theta^2 total, then the prefix that reaches it
-__global__ void dorfler_cut_kernel(int n, const unsigned long long* __restrict__ sorted_bits, double theta,
-                                   int* count) {
+// adapt.cpp:139-149 in sorted order: total, goal = theta^2 total, then the prefix that reaches it.
+// The sums are sequential (the cut must see the reference's rounding), so one thread runs them;
+// the block stages each chunk's squares in shared memory first, so that thread only chains adds.
+constexpr int kCutNT = 256, kCutChunk = 4096;
+__global__ void __launch_bounds__(kCutNT) dorfler_cut_kernel(int n, const unsigned long long* __restrict__ sorted_bits,
+                                                             double theta, int* count) {
+  __shared__ double sq[kCutChunk];
+  __shared__ int stop;
   double total = 0.0;
-  for (int i = 0; i < n; ++i) {
-    const double e = __longlong_as_double((long long)sorted_bits[i]);
-    total = __dadd_rn(total, __dmul_rn(e, e));
+  for (int c0 = 0; c0 < n; c0 += kCutChunk) {
+    const int m = min(kCutChunk, n - c0);
+    for (int k = threadIdx.x; k < m; k += kCutNT) {
+      const double e = __longlong_as_double((long long)sorted_bits[c0 + k]);
+      sq[k] = __dmul_rn(e, e);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < m; ++k) total = __dadd_rn(total, sq[k]);
+    __syncthreads();
   }
-  const double goal = __dmul_rn(__dmul_rn(theta, theta), total);
+  const double goal = __dmul_rn(__dmul_rn(theta, theta), total);  // thread 0's value is the one used
   double acc = 0.0;
-  int k = 0;
-  for (; k < n; ++k) {
-    const double e = __longlong_as_double((long long)sorted_bits[k]);
-    if (acc >= goal || e == 0.0) break;
-    acc = __dadd_rn(acc, __dmul_rn(e, e));
+  int kk = 0;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < n && !stop; c0 += kCutChunk) {
+    const int m = min(kCutChunk, n - c0);
+    for (int k = threadIdx.x; k < m; k += kCutNT) {
+      const double e = __longlong_as_double((long long)sorted_bits[c0 + k]);
+      sq[k] = e == 0.0 ? -1.0 : __dmul_rn(e, e);  // -1: a zero indicator ends the marking
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int k = 0;
+      for (; k < m; ++k) {
+        if (acc >= goal || sq[k] < 0.0) {
+          stop = 1;
+          break;
+        }
+        acc = __dadd_rn(acc, sq[k]);
+      }
+      kk = c0 + k;
+    }
+    __syncthreads();
   }
-  *count = k;
+  if (threadIdx.x == 0) *count = kk;
 }
 
 __global__ void iota_kernel(int n, int* a) {
@@ -256,7 +285,7 @@ void mark_dorfler(Ctx& c, int n, const double* eta, double theta, int* marked, i
   DBuf<char> tmp(std::max<size_t>(tmp_bytes, 1), c.stream);
   RDG_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tmp_bytes, kin, kout.p, idx.p, marked, n, 0, 64,
                                                      c.stream));
-  dorfler_cut_kernel<<<1, 1, 0, c.stream>>>(n, kout.p, theta, cnt.p);
+  dorfler_cut_kernel<<<1, kCutNT, 0, c.stream>>>(n, kout.p, theta, cnt.p);
   RDG_LAUNCH_CHECK();
   c.launches += 2;
   RDG_CUDA(cudaMemcpyAsync(count, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));

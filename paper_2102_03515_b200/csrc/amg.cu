@@ -17,7 +17,11 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "internal.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace rdg {
 
@@ -187,6 +191,36 @@ __global__ void __launch_bounds__(kCoarseNT) llt_solve_kernel(int n, const doubl
     __syncthreads();
   }
   for (int i = threadIdx.x; i < n; i += kCoarseNT) x[i] = sh[i];
+}
+
+// The same factorization for matrices past shared memory (the H^-1 dual norm's dense branch,
+// n <= 2000), on the whole GPU, right-looking: after column j is divided by its pivot, every
+// trailing lower-triangle entry subtracts L(i,j) L(m,j).  Each entry thus sees its products in
+// k order, exactly llt_kernel's (and the oracle's) left-looking sequence -- the factor is
+// bit-identical -- while the work per column is a wide parallel update instead of one sequential
+// dot product per element.  Cooperative grid: two grid barriers per column; warp per row.
+__global__ void __launch_bounds__(256) llt_right_kernel(int n, double* L, int* err) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+  for (int j = 0; j < n; ++j) {
+    const double s = L[(size_t)j * n + j];  // every k < j already subtracted
+    if (!(s > 0.0)) {
+      if (gt == 0) *err = 1;
+      return;  // every block sees the same pivot
+    }
+    const double piv = __dsqrt_rn(s);
+    for (int64_t i = j + 1 + gt; i < n; i += gs) L[(size_t)i * n + j] = __ddiv_rn(L[(size_t)i * n + j], piv);
+    grid.sync();
+    if (gt == 0) L[(size_t)j * n + j] = piv;
+    for (int64_t i = j + 1 + gw; i < n; i += nw) {
+      const double lij = L[(size_t)i * n + j];
+      double* row = L + (size_t)i * n;
+      for (int64_t m = j + 1 + lane; m <= i; m += 32) row[m] = __dsub_rn(row[m], __dmul_rn(lij, L[(size_t)m * n + j]));
+    }
+    grid.sync();
+  }
 }
 
 // ---------------------------------------------------------------- lattice levels
@@ -668,8 +702,16 @@ void dense_llt(Ctx& c, const DCsr& A, DBuf<double>& L, int* err_dev) {
       attr = true;
     }
     llt_kernel<true><<<1, 256, llt_smem(n), c.stream>>>(n, L.p, err_dev ? err_dev : err.p);
-  } else {
-    llt_kernel<false><<<1, 256, 0, c.stream>>>(n, L.p, err_dev ? err_dev : err.p);
+  } else {  // the whole GPU (cooperative launch: every block resident)
+    int per_sm = 0;
+    RDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, llt_right_kernel, 256, 0));
+    const int blocks = std::max(1, per_sm * c.num_sms);
+    int* ep = err_dev ? err_dev : err.p;
+    int nn = n;
+    double* lp = L.p;
+    void* args[] = {&nn, &lp, &ep};
+    RDG_CUDA(cudaLaunchCooperativeKernel((const void*)llt_right_kernel, dim3(blocks), dim3(256), args, 0, c.stream));
+    ++c.launches;
   }
   RDG_LAUNCH_CHECK();
   c.launches += 2;

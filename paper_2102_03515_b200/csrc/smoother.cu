@@ -18,6 +18,8 @@
 //    the small threshold.
 //  * the structured lattice kernel (smoother_lattice.cu) handles matrices whose
 //    pattern was verified to be the 15-point Kuhn stencil on a box.
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace rdg {
@@ -114,6 +116,137 @@ __global__ void __launch_bounds__(kGsCtaNT, 1) gs_syncfree_cta_kernel(int n, con
   }
 }
 
+// s -= p_q for q = 0 .. m-1 in order (d takes the diagonal's entry), the p_q held by lane q.
+// (Measured: issuing the shuffles eight at a time ahead of the subtractions was slower.)
+__device__ __forceinline__ void row_accumulate(double p, unsigned dmask, int m, double& s, double& d) {
+  for (int q = 0; q < m; ++q) {
+    const double pq = __shfl_sync(0xffffffffu, p, q);
+    if ((dmask >> q) & 1u)
+      d = pq;
+    else
+      s = __dsub_rn(s, pq);
+  }
+}
+
+// Warp per row (generic CSR, any size): the row's entries are handled 32 at a time, so the
+// waits on its already-visited neighbours overlap (lane k polls entry k's flag) instead of one
+// L2 round trip per neighbour in sequence, and the new values load in parallel after one
+// acquire fence.  The sum then runs sequentially over the entries in column order on every
+// lane (products shuffled in): the reference's arithmetic, bit for bit.  Warps take rows in
+// ticket order, so every wait is on a row some earlier warp owns: no deadlock.
+constexpr int kGswNT = 256;
+__global__ void __launch_bounds__(kGswNT) gs_syncfree_warp_kernel(int n, const int* __restrict__ rp,
+                                                                  const int* __restrict__ ci,
+                                                                  const double* __restrict__ val,
+                                                                  const double* __restrict__ f,
+                                                                  const double* __restrict__ xin, double* xout,
+                                                                  unsigned* flags, unsigned epoch, int* ticket,
+                                                                  int* err, int fwd) {
+  __shared__ int blk;
+  if (threadIdx.x == 0) blk = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int t = blk * (kGswNT / 32) + (threadIdx.x >> 5);
+  if (t >= n) return;
+  const int i = fwd ? t : n - 1 - t;
+  const int b = rp[i], e = rp[i + 1];
+  // wait for every visited neighbour (relaxed polls), then one acquire fence
+  for (int k0 = b; k0 < e; k0 += 32) {
+    const int k = k0 + lane;
+    if (k < e) {
+      const int j = ci[k];
+      if (fwd ? (j < i) : (j > i)) {
+        unsigned v;
+        do {
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + j) : "memory");
+        } while (v != epoch);
+      }
+    }
+  }
+  __syncwarp();
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  double s = f[i], d = 0.0;
+  for (int k0 = b; k0 < e; k0 += 32) {
+    const int k = k0 + lane;
+    double p = 0.0;
+    bool diag = false;
+    if (k < e) {
+      const int j = ci[k];
+      const double a = val[k];
+      diag = j == i;
+      if (diag) {
+        p = a;
+      } else {
+        const double xj = (fwd ? (j < i) : (j > i)) ? ld_relaxed_f64(xout + j) : (xin ? __ldg(xin + j) : 0.0);
+        p = __dmul_rn(a, xj);
+      }
+    }
+    row_accumulate(p, __ballot_sync(0xffffffffu, diag), min(32, e - k0), s, d);
+  }
+  if (lane == 0) {
+    if (d == 0.0) atomicCAS(err, 0, RD_EZERODIAG);
+    xout[i] = __ddiv_rn(s, d);
+    st_release_u32(flags + i, epoch);
+  }
+}
+
+// The same warp-per-row scheme inside ONE block for small levels (<= kGsCtaMaxRows rows): old and
+// new values and the readiness flags all in shared memory, so a dependency hop is a shared-memory
+// round trip.  Warp w relaxes rows w, w + 32, ... in sweep order.
+constexpr int kGscNT = 1024;
+__global__ void __launch_bounds__(kGscNT, 1) gs_syncfree_cta_warp_kernel(int n, const int* __restrict__ rp,
+                                                                        const int* __restrict__ ci,
+                                                                        const double* __restrict__ val,
+                                                                        const double* __restrict__ f,
+                                                                        const double* __restrict__ xin,
+                                                                        double* xout, int* err, int fwd) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  double* xo = reinterpret_cast<double*>(gsm);  // old values (xin, or 0)
+  double* xn = xo + n;                          // new values
+  unsigned char* ready = reinterpret_cast<unsigned char*>(xn + n);
+  for (int k = threadIdx.x; k < n; k += kGscNT) {
+    xo[k] = xin ? xin[k] : 0.0;
+    ready[k] = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned rbase = (unsigned)__cvta_generic_to_shared(ready);
+  for (int t = w; t < n; t += kGscNT / 32) {
+    const int i = fwd ? t : n - 1 - t;
+    const int b = rp[i], e = rp[i + 1];
+    double s = f[i], d = 0.0;
+    for (int k0 = b; k0 < e; k0 += 32) {
+      const int k = k0 + lane;
+      double p = 0.0, a = 0.0;
+      bool diag = false, fresh = false;
+      int j = 0;
+      if (k < e) {  // everything that does not wait on a neighbour first
+        j = ci[k];
+        a = val[k];
+        diag = j == i;
+        fresh = !diag && (fwd ? (j < i) : (j > i));
+        p = diag ? a : fresh ? 0.0 : __dmul_rn(a, xo[j]);
+      }
+      if (fresh) {
+        unsigned r;
+        do {
+          asm volatile("ld.acquire.cta.shared.u8 %0, [%1];" : "=r"(r) : "r"(rbase + (unsigned)j) : "memory");
+        } while (r == 0u);
+        p = __dmul_rn(a, *reinterpret_cast<volatile double*>(xn + j));
+      }
+      row_accumulate(p, __ballot_sync(0xffffffffu, diag), min(32, e - k0), s, d);
+    }
+    if (lane == 0) {
+      if (d == 0.0) atomicCAS(err, 0, RD_EZERODIAG);
+      *reinterpret_cast<volatile double*>(xn + i) = __ddiv_rn(s, d);
+      asm volatile("st.release.cta.shared.u8 [%0], %1;" ::"r"(rbase + (unsigned)i), "r"(1u) : "memory");
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < n; k += kGscNT) xout[k] = xn[k];
+}
+
 }  // namespace
 
 void gs_pass(Ctx& c, const DCsr& A, const double* f, const double* xin, double* xout, bool fwd, double* dot_out,
@@ -131,15 +264,28 @@ void gs_pass(Ctx& c, const DCsr& A, const double* f, const double* xin, double* 
 void gs_pass_generic(Ctx& c, const DCsr& A, const double* f, const double* xin, double* xout, bool fwd,
                      double* dot_out, const double* dot_with) {
   const int n = A.rows;
+  static const int variant = getenv("RD_GS_GENERIC") ? atoi(getenv("RD_GS_GENERIC")) : 1;  // A/B only
   if (n <= kGsCtaMaxRows) {
-    static bool attr = false;
-    if (!attr) {
-      RDG_CUDA(cudaFuncSetAttribute(gs_syncfree_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kGsCtaMaxRows));
-      attr = true;
+    if (variant == 1) {  // warp per row, values and flags in shared memory
+      const size_t smem = (size_t)n * (2 * sizeof(double) + 1) + 16;
+      static bool attr = false;
+      if (!attr) {
+        RDG_CUDA(cudaFuncSetAttribute(gs_syncfree_cta_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)((size_t)kGsCtaMaxRows * (2 * sizeof(double) + 1) + 16)));
+        attr = true;
+      }
+      gs_syncfree_cta_warp_kernel<<<1, kGscNT, smem, c.stream>>>(n, A.rp.p, A.ci.p, A.v.p, f, xin, xout, c.d_err,
+                                                                 fwd ? 1 : 0);
+    } else {
+      static bool attr = false;
+      if (!attr) {
+        RDG_CUDA(cudaFuncSetAttribute(gs_syncfree_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kGsCtaMaxRows));
+        attr = true;
+      }
+      gs_syncfree_cta_kernel<<<1, kGsCtaNT, n, c.stream>>>(n, A.rp.p, A.ci.p, A.v.p, f, xin, xout, c.d_err,
+                                                           fwd ? 1 : 0);
     }
-    gs_syncfree_cta_kernel<<<1, kGsCtaNT, n, c.stream>>>(n, A.rp.p, A.ci.p, A.v.p, f, xin, xout, c.d_err,
-                                                         fwd ? 1 : 0);
     RDG_LAUNCH_CHECK();
     ++c.launches;
     if (dot_out) dot(c, n, dot_with, xout, dot_out);
@@ -156,9 +302,13 @@ void gs_pass_generic(Ctx& c, const DCsr& A, const double* f, const double* xin, 
   }
   int* ticket = reinterpret_cast<int*>(c.d_counter + 32);
   RDG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), c.stream));
-  gs_syncfree_kernel<<<div_up(n, kGsNT), kGsNT, 0, c.stream>>>(n, A.rp.p, A.ci.p, A.v.p, f, xin, xout,
-                                                               A.gs_flags.p, A.gs_epoch, ticket, c.d_err,
-                                                               fwd ? 1 : 0);
+  if (variant == 1)
+    gs_syncfree_warp_kernel<<<div_up(n, kGswNT / 32), kGswNT, 0, c.stream>>>(
+        n, A.rp.p, A.ci.p, A.v.p, f, xin, xout, A.gs_flags.p, A.gs_epoch, ticket, c.d_err, fwd ? 1 : 0);
+  else
+    gs_syncfree_kernel<<<div_up(n, kGsNT), kGsNT, 0, c.stream>>>(n, A.rp.p, A.ci.p, A.v.p, f, xin, xout,
+                                                                 A.gs_flags.p, A.gs_epoch, ticket, c.d_err,
+                                                                 fwd ? 1 : 0);
   RDG_LAUNCH_CHECK();
   ++c.launches;
   if (dot_out) dot(c, n, dot_with, xout, dot_out);

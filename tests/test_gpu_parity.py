@@ -548,11 +548,13 @@ def test_l2_error_target_squared(rd, O, n, rho, target):
         1e-12 * O.l2_error_target_squared(om, os_, z, target, n)
 
 
-@pytest.mark.parametrize("n,rho,target", [(8, 1e-2, "smooth"), (8, 1.0, "ball"), (16, 2.0 ** -8, "ball"),
-                                          (16, 1e-4, "sine_random")])
+@pytest.mark.parametrize("n,rho,target", [(4, 1.0, "box"), (8, 1e-2, "smooth"), (8, 1.0, "ball"),
+                                          (13, 1e-3, "ball"), (16, 2.0 ** -8, "ball"), (16, 1e-4, "sine_random")])
 def test_target_dual_norm(rd, O, n, rho, target):
-    """bench.cpp:55-63 on the device: dense LLT of K for n_dofs <= 2000 (n=8: agreement to
-    rounding), AMG(K)-PCG to 1e-11 above (n=16: the generic, non-lattice K hierarchy)."""
+    """bench.cpp:55-63 on the device: dense LLT of K for n_dofs <= 2000 (n=4: the one-CTA
+    shared-memory factorization; n=8, 13: the cooperative whole-GPU one -- both the oracle's
+    operation order, agreement to rounding in the final dot), AMG(K)-PCG to 1e-11 above (n=16:
+    the generic, non-lattice K hierarchy)."""
     om = O.build_structured_cube(n)
     os_ = O.build_system(om, rho, target)
     u = O.solve_system_amg(os_, 1e-10).u
