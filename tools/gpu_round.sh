@@ -17,7 +17,7 @@ if [ $rc -eq 0 ]; then
     --log-file $O/${T}_launches.csv python bench.py --profile --steps 1 --warmup 1 > $O/${T}_ncu.log 2>&1
   echo "ncu launch list rc=$?"
   timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"gs_lattice5_kernel|spmv_staged_kernel|coarse_tail_kernel|stencil_spmv_kernel" -c 6 -o $O/${T}_full \
+    -k regex:"gs_lattice5_kernel|spmv_staged_kernel|coarse_tail_kernel|stencil_spmv_tiled_kernel" -c 10 -o $O/${T}_full \
     python bench.py --profile --steps 1 --warmup 0 > $O/${T}_ncu2.log 2>&1; echo "ncu full rc=$?"
   ncu -i $O/${T}_full.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.avg.per_cycle_active,launch__grid_size,launch__block_size > $O/${T}_full_raw.csv 2>&1
 fi
