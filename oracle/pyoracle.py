@@ -100,6 +100,16 @@ def lib():
         "or_h1_semi_error_manufactured": (_I, [_P, _P, _pd, _D, C.POINTER(_D)]),
         "or_error_norms_target": (_I, [_P, _P, _pd, _I, _I, C.c_uint64, C.POINTER(_D), C.POINTER(_D)]),
         "or_target_grad": (_I, [_I, _I, C.c_uint64, _I, _pd, _pd]),
+        "or_partition_geometric": (_I, [_P, _P, _I, _pi, _pi, _pi]),
+        "or_bddc_create": (_I, [_P, _P, _I, C.POINTER(_P)]),
+        "or_bddc_free": (None, [_P]),
+        "or_bddc_info": (None, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
+        "or_bddc_interface": (None, [_P, _pi]),
+        "or_bddc_coarse": (None, [_P, _pd]),
+        "or_bddc_sub_info": (None, [_P, _I, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
+        "or_bddc_sub_get": (None, [_P, _I, _pi, _pi, _pi, _pd, _pd, _pd, _pd]),
+        "or_bddc_op": (_I, [_P, _I, _I, _pd, _pd, _pd]),
+        "or_bddc_solve": (_I, [_P, _P, _I, _D, _I, _pd, C.POINTER(_I), C.POINTER(_I), _pd]),
         "or_estimate": (_I, [_P, _P, _pd, _I, C.c_uint64, _pd, C.POINTER(_D)]),
         "or_mark_dorfler": (_I, [_I, _pd, _D, _pi, C.POINTER(_I)]),
         "or_bisect_marked": (_I, [_P, _I, _pi, C.POINTER(_P)]),
@@ -568,3 +578,80 @@ def adaptive_solve(mesh: Mesh, target: str, rho: float, dof_budget: int, tol: fl
                  err_l2_sq=float(hd[3 * i + 1]), err_hm1_sq=float(hd[3 * i + 2])) for i in range(min(k.value, cap))]
     final = _mesh_from_handle(fm)
     return rows, final, co[: rows[-1]["dofs"]].copy()
+
+
+# ---------------------------------------------------------------- BDDC (§8(f)4)
+def partition_geometric(mesh: Mesh, sys: FemSystem, p: int):
+    """bddc.cpp:45-111 -> (owner per tet, dof_subdomains list per dof)."""
+    nt, nd = mesh.tets.shape[0], sys.n_dofs
+    owner = np.zeros(max(nt, 1), np.int32)
+    cnt = np.zeros(max(nd, 1), np.int32)
+    subs = np.zeros(max(8 * nd, 1), np.int32)
+    _check(lib().or_partition_geometric(mesh._h.h, sys._h.h, int(p), owner, cnt, subs))
+    return owner[:nt], [list(subs[8 * d:8 * d + cnt[d]]) for d in range(nd)]
+
+
+class Bddc:
+    """bddc.hpp BddcOperator (the oracle's restatement)."""
+
+    def __init__(self, mesh: Mesh, sys: FemSystem, p: int):
+        h = _P()
+        _check(lib().or_bddc_create(mesh._h.h, sys._h.h, int(p), C.byref(h)))
+        self._h = _Handle(h, lib().or_bddc_free)
+        self.n_dofs = sys.n_dofs
+        ni, npr, pp = _I(), _I(), _I()
+        lib().or_bddc_info(h, C.byref(ni), C.byref(npr), C.byref(pp))
+        self.n_interface, self.n_primal, self.p = ni.value, npr.value, pp.value
+        self.interface_dofs = np.zeros(max(ni.value, 1), np.int32)
+        lib().or_bddc_interface(h, self.interface_dofs)
+        self.interface_dofs = self.interface_dofs[: ni.value]
+
+    def coarse_matrix(self):
+        out = np.zeros(max(self.n_primal ** 2, 1))
+        lib().or_bddc_coarse(self._h.h, out)
+        return out[: self.n_primal ** 2].reshape(self.n_primal, self.n_primal)
+
+    def sub(self, s: int) -> dict:
+        nI, nB, nc = _I(), _I(), _I()
+        lib().or_bddc_sub_info(self._h.h, int(s), C.byref(nI), C.byref(nB), C.byref(nc))
+        nB_, nc_ = nB.value, nc.value
+        b = np.zeros(max(nB_, 1), np.int32)
+        bi = np.zeros(max(nB_, 1), np.int32)
+        pi = np.zeros(max(nc_, 1), np.int32)
+        sc = np.zeros(max(nB_, 1))
+        Cm = np.zeros(max(nc_ * nB_, 1))
+        Ph = np.zeros(max(nc_ * nB_, 1))
+        S = np.zeros(max(nB_ * nB_, 1))
+        lib().or_bddc_sub_get(self._h.h, int(s), b, bi, pi, sc, Cm, Ph, S)
+        return dict(nI=nI.value, nB=nB_, ncon=nc_, boundary=b[:nB_], boundary_index=bi[:nB_], primal_index=pi[:nc_],
+                    scaling=sc[:nB_], C=Cm[:nc_ * nB_].reshape(nc_, nB_), Phi=Ph[:nc_ * nB_].reshape(nB_, nc_),
+                    S=S[:nB_ * nB_].reshape(nB_, nB_))
+
+    def _op(self, which, x, f=None, n_out=None):
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.zeros(max(n_out, 1))
+        fv = np.ascontiguousarray(f if f is not None else np.zeros(max(self.n_dofs, 1)), np.float64)
+        _check(lib().or_bddc_op(self._h.h, which, x.size, x if x.size else np.zeros(1), fv, out))
+        return out[:n_out]
+
+    def schur_apply(self, x):
+        return self._op(0, x, n_out=self.n_interface)
+
+    def reduce_rhs(self, f):
+        return self._op(1, f, n_out=self.n_interface)
+
+    def expand_solution(self, uC, f):
+        return self._op(2, uC, f=f, n_out=self.n_dofs)
+
+    def apply(self, r):
+        return self._op(3, r, n_out=self.n_interface)
+
+
+def bddc_solve(mesh: Mesh, sys: FemSystem, p: int, tol: float = 1e-8, max_iter: int = 500) -> PcgResult:
+    """bddc.cpp:440-456."""
+    u = np.zeros(max(sys.n_dofs, 1))
+    hist = np.zeros(max(max_iter, 1))
+    it, conv = _I(), _I()
+    _check(lib().or_bddc_solve(mesh._h.h, sys._h.h, int(p), float(tol), int(max_iter), u, C.byref(it), C.byref(conv),
+                               hist))
+    return PcgResult(u[: sys.n_dofs], it.value, bool(conv.value), hist[: it.value].copy())

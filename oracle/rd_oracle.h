@@ -133,6 +133,22 @@ int or_adaptive_solve(const or_mesh* initial, int kind, uint64_t seed, double rh
                       double theta, int cap, int* n_levels, int* hist_i, double* hist_d, or_mesh** final_mesh,
                       double* coeffs, int coeffs_cap);
 
+/* §8(f)4 BDDC (bddc.hpp / bddc.cpp:45-456) */
+typedef struct or_bddc or_bddc;
+int or_partition_geometric(const or_mesh* m, const or_system* s, int p, int* owner, int* n_subdomains_per_dof,
+                           int* subdomains);
+int or_bddc_create(const or_mesh* m, const or_system* s, int p, or_bddc** out);
+void or_bddc_free(or_bddc* b);
+void or_bddc_info(const or_bddc* b, int* n_interface, int* n_primal, int* p);
+void or_bddc_interface(const or_bddc* b, int* dofs);
+void or_bddc_coarse(const or_bddc* b, double* out);
+void or_bddc_sub_info(const or_bddc* b, int s, int* nI, int* nB, int* ncon);
+void or_bddc_sub_get(const or_bddc* b, int s, int* boundary, int* bidx, int* pidx, double* scaling, double* C,
+                     double* Phi, double* S);
+int or_bddc_op(const or_bddc* b, int which, int n_in, const double* in, const double* f, double* out);
+int or_bddc_solve(const or_mesh* m, const or_system* s, int p, double tol, int max_iter, double* u, int* iterations,
+                  int* converged, double* history);
+
 #ifdef __cplusplus
 }
 #endif
