@@ -223,6 +223,32 @@ int rd_gpu_linop_apply(rd_ctx* ctx, rd_linop op, int64_t n, const double* x, dou
 int rd_gpu_pcg_linop(rd_ctx* ctx, int64_t n, rd_linop apply_a, rd_linop apply_p, const double* f, double tol,
                      int max_iter, double* x, rd_pcg_report* report, double* residual_history);
 
+/* ------------------------------------------------------------ BDDC (bddc.hpp) */
+typedef struct rd_bddc rd_bddc;
+/* replaces rd::partition_geometric(mesh, dof_map, p)    bddc.hpp:30, bddc.cpp:45-111: the RCB owner
+ * of every tet (n_tets ints, host); RD_EINVAL for p < 2 or p > n_tets */
+int rd_gpu_partition_geometric(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, int p, int32_t* owner);
+/* replaces rd::build_bddc(mesh, sys, partition_geometric(mesh, dof_map, p))   bddc.hpp:58-59, bddc.cpp:113-301 */
+int rd_gpu_bddc_create(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, int p, rd_bddc** out);
+void rd_gpu_bddc_free(rd_bddc* b);
+int rd_gpu_bddc_info(const rd_bddc* b, int* n_interface, int* n_primal);
+int rd_gpu_bddc_interface_dofs(const rd_bddc* b, int32_t* dofs);    /* ascending interior-dof ids (host) */
+int rd_gpu_bddc_coarse_matrix(const rd_bddc* b, double* out);       /* n_primal^2, row-major (host) */
+/* schur_apply / reduce_rhs / expand_solution / bddc_apply   bddc.hpp:61-75, bddc.cpp:303-430;
+ * host or device vectors (n_interface, n_dofs as the reference's) */
+int rd_gpu_bddc_schur_apply(rd_bddc* b, const double* x, double* y);
+int rd_gpu_bddc_reduce_rhs(rd_bddc* b, const double* f, double* g);
+int rd_gpu_bddc_expand(rd_bddc* b, const double* u_interface, const double* f, double* u);
+int rd_gpu_bddc_apply(rd_bddc* b, const double* r, double* z);
+/* schur_op(op), bddc_precond(op) as rd_linop operators (borrow b)   bddc.hpp:77-78 */
+int rd_gpu_linop_bddc_schur(rd_bddc* b, rd_linop* out);
+int rd_gpu_linop_bddc(rd_bddc* b, rd_linop* out);
+/* replaces rd::bddc_solve(mesh, sys, p, tol, max_iter)   bddc.hpp:85-87, bddc.cpp:440-456:
+ * u = n_dofs (host or device), residual_history host (>= max_iter) or NULL */
+int rd_gpu_bddc_solve(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, int p, double tol, int max_iter,
+                      double* u, rd_pcg_report* report, double* residual_history);
+
+
 /* replaces rd::solve_system(mesh, sys, PrecondKind::amg, p, tol)  bench.hpp:48-57, bench.cpp:185-225:
  * build_amg(A) [setup_seconds], pcg(A, amg, f, tol, 500) [solve_seconds]. */
 typedef struct {

@@ -207,6 +207,10 @@ struct rd_jacobi {
   DBuf<double> d;
   int64_t n = 0;
 };
+struct rd_bddc {
+  rd_ctx* ctx = nullptr;
+  std::unique_ptr<rdg::Bddc, void (*)(rdg::Bddc*)> b{nullptr, rdg::bddc_free};
+};
 
 namespace {
 
@@ -235,6 +239,35 @@ int linop_jacobi_fn(void* u, rd_ctx* ctx, int64_t n, const double* x, double* y)
   return guard(ctx, [&] {
     require(n == j->n, "jacobi_precond: dimension mismatch");
     jacobi_apply(ctx->c, n, j->d.p, x, y);
+  });
+}
+
+int linop_bddc_schur_fn(void* u, rd_ctx* ctx, int64_t n, const double* x, double* y) {
+  rd_bddc* b = static_cast<rd_bddc*>(u);
+  return guard(ctx, [&] {
+    require(n == bddc_n_interface(*b->b), "schur_apply: dimension mismatch");
+    bddc_schur_apply(*b->b, x, y);
+  });
+}
+int linop_bddc_fn(void* u, rd_ctx* ctx, int64_t n, const double* x, double* y) {
+  rd_bddc* b = static_cast<rd_bddc*>(u);
+  return guard(ctx, [&] {
+    require(n == bddc_n_interface(*b->b), "bddc_apply: dimension mismatch");
+    bddc_apply(*b->b, x, y);
+  });
+}
+
+template <class F>
+int bddc_vec_op(rd_bddc* b, const double* in, int64_t n_in, double* out, int64_t n_out, F&& body) {
+  return guard(b ? b->ctx : nullptr, [&] {
+    require(b != nullptr, "bddc: null operator");
+    Ctx& c = b->ctx->c;
+    DBuf<double> ti;
+    const double* di = in_dev(c, in, (size_t)n_in, ti);
+    OutVec<double> o(c, out, (size_t)n_out);
+    body(di, o.dev());
+    o.finish();
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
 
@@ -823,6 +856,118 @@ int rd_gpu_adaptive_solve(rd_ctx* ctx, const rd_mesh* initial, const rd_target* 
                                      std::to_string(n) + " dofs)");
       mesh = std::move(refined);
     }
+  });
+}
+
+// ------------------------------------------------------------ BDDC (§8(f)4)
+int rd_gpu_partition_geometric(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, int p, int32_t* owner) {
+  return guard(ctx, [&] {
+    require(mesh && sys && owner, "partition_geometric: null argument");
+    require(sys->s.nv == mesh->m.nv, "partition_geometric: system does not belong to the mesh");
+    std::vector<int> own;
+    std::vector<std::vector<int>> ds;
+    partition_geometric(ctx->c, mesh->m, sys->s, p, own, ds);
+    std::memcpy(owner, own.data(), own.size() * sizeof(int));
+  });
+}
+int rd_gpu_bddc_create(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, int p, rd_bddc** out) {
+  return guard(ctx, [&] {
+    require(mesh && sys && out, "build_bddc: null argument");
+    require(sys->s.nv == mesh->m.nv, "build_bddc: system does not belong to the mesh");
+    auto h = std::make_unique<rd_bddc>();
+    h->ctx = ctx;
+    h->b.reset(build_bddc(ctx->c, mesh->m, sys->s, p));
+    *out = h.release();
+  });
+}
+void rd_gpu_bddc_free(rd_bddc* b) {
+  if (!b) return;
+  PoolScope ps(b->ctx->c.pool);
+  delete b;
+}
+int rd_gpu_bddc_info(const rd_bddc* b, int* n_interface, int* n_primal) {
+  if (!b) return RD_EINVAL;
+  if (n_interface) *n_interface = bddc_n_interface(*b->b);
+  if (n_primal) *n_primal = bddc_n_primal(*b->b);
+  return RD_OK;
+}
+int rd_gpu_bddc_interface_dofs(const rd_bddc* b, int32_t* dofs) {
+  if (!b || !dofs) return RD_EINVAL;
+  const auto& v = bddc_interface(*b->b);
+  std::memcpy(dofs, v.data(), v.size() * sizeof(int));
+  return RD_OK;
+}
+int rd_gpu_bddc_coarse_matrix(const rd_bddc* b, double* out) {
+  return guard(b ? b->ctx : nullptr, [&] {
+    require(b && out, "bddc_coarse_matrix: null argument");
+    const auto m = bddc_coarse_matrix(*b->b);
+    std::memcpy(out, m.data(), m.size() * sizeof(double));
+  });
+}
+int rd_gpu_bddc_schur_apply(rd_bddc* b, const double* x, double* y) {
+  const int nC = b ? bddc_n_interface(*b->b) : 0;
+  return bddc_vec_op(b, x, nC, y, nC, [&](const double* xi, double* yo) { bddc_schur_apply(*b->b, xi, yo); });
+}
+int rd_gpu_bddc_reduce_rhs(rd_bddc* b, const double* f, double* g) {
+  const int nd = b ? bddc_n_dofs(*b->b) : 0, nC = b ? bddc_n_interface(*b->b) : 0;
+  return bddc_vec_op(b, f, nd, g, nC, [&](const double* fi, double* go) { bddc_reduce_rhs(*b->b, fi, go); });
+}
+int rd_gpu_bddc_expand(rd_bddc* b, const double* uC, const double* f, double* u) {
+  const int nd = b ? bddc_n_dofs(*b->b) : 0, nC = b ? bddc_n_interface(*b->b) : 0;
+  return guard(b ? b->ctx : nullptr, [&] {
+    Ctx& c = b->ctx->c;
+    DBuf<double> t1, t2;
+    const double* du = in_dev(c, uC, (size_t)nC, t1);
+    const double* df = in_dev(c, f, (size_t)nd, t2);
+    OutVec<double> o(c, u, (size_t)nd);
+    bddc_expand(*b->b, du, df, o.dev());
+    o.finish();
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int rd_gpu_bddc_apply(rd_bddc* b, const double* r, double* z) {
+  const int nC = b ? bddc_n_interface(*b->b) : 0;
+  return bddc_vec_op(b, r, nC, z, nC, [&](const double* ri, double* zo) { bddc_apply(*b->b, ri, zo); });
+}
+int rd_gpu_linop_bddc_schur(rd_bddc* b, rd_linop* out) {
+  if (!b || !out) return RD_EINVAL;
+  *out = rd_linop{linop_bddc_schur_fn, b};
+  return RD_OK;
+}
+int rd_gpu_linop_bddc(rd_bddc* b, rd_linop* out) {
+  if (!b || !out) return RD_EINVAL;
+  *out = rd_linop{linop_bddc_fn, b};
+  return RD_OK;
+}
+int rd_gpu_bddc_solve(rd_ctx* ctx, const rd_mesh* mesh, const rd_system* sys, int p, double tol, int max_iter,
+                      double* u, rd_pcg_report* rep, double* hist) {
+  return guard(ctx, [&] {
+    require(mesh && sys && (u || sys->s.n_dofs == 0), "bddc_solve: null argument");
+    Ctx& c = ctx->c;
+    std::unique_ptr<Bddc, void (*)(Bddc*)> b(build_bddc(c, mesh->m, sys->s, p), bddc_free);  // bddc.cpp:440-456
+    const int nC = bddc_n_interface(*b), nd = sys->s.n_dofs;
+    DBuf<double> g(std::max(nC, 1), c.stream), x(std::max(nC, 1), c.stream), hd(std::max(max_iter, 1), c.stream);
+    bddc_reduce_rhs(*b, sys->s.f.p, g.p);
+    const PcgOp A = [&](const double* in, double* o, double* d) {
+      bddc_schur_apply(*b, in, o);
+      dot(c, nC, in, o, d);
+    };
+    const PcgOp P = [&](const double* in, double* o, double* d) {
+      bddc_apply(*b, in, o);
+      dot(c, nC, in, o, d);
+    };
+    PcgResultDev r = pcg_ops(c, nC, A, P, g.p, tol, max_iter, x.p, hd.p);
+    OutVec<double> uo(c, u, (size_t)nd);
+    bddc_expand(*b, x.p, sys->s.f.p, uo.dev());
+    uo.finish();
+    if (hist && r.iterations > 0)
+      RDG_CUDA(cudaMemcpyAsync(hist, hd.p, sizeof(double) * r.iterations, cudaMemcpyDefault, c.stream));
+    RDG_CUDA(cudaStreamSynchronize(c.stream));
+    if (rep) {
+      rep->iterations = r.iterations;
+      rep->converged = r.converged ? 1 : 0;
+    }
+    b.reset();
   });
 }
 

@@ -216,6 +216,22 @@ double l2_error_target_squared(Ctx& c, const DMesh& m, const DSystem& s, const d
 // mesh.cpp:67-145 (out: a new mesh; marked: device ids)
 void mark_dorfler(Ctx& c, int n, const double* eta, double theta, int* marked, int* count);
 void bisect_marked(Ctx& c, const DMesh& in, const int* marked, int n_marked, DMesh& out);
+// bddc.cu -- bddc.cpp:45-456 (setup on the host's index lists, numerics on the device)
+struct Bddc;
+void partition_geometric(Ctx& c, const DMesh& m, const DSystem& s, int p, std::vector<int>& owner,
+                         std::vector<std::vector<int>>& dof_subdomains);
+Bddc* build_bddc(Ctx& c, const DMesh& m, const DSystem& sys, int p);  // free with bddc_free
+void bddc_free(Bddc* b);
+int bddc_n_interface(const Bddc& b);
+int bddc_n_primal(const Bddc& b);
+int bddc_n_dofs(const Bddc& b);
+const std::vector<int>& bddc_interface(const Bddc& b);
+std::vector<double> bddc_coarse_matrix(const Bddc& b);
+// device vectors, stream-ordered on the Bddc's context
+void bddc_schur_apply(Bddc& b, const double* x, double* y);            // n_interface -> n_interface
+void bddc_reduce_rhs(Bddc& b, const double* f, double* g);             // n_dofs -> n_interface
+void bddc_expand(Bddc& b, const double* uC, const double* f, double* u);  // -> n_dofs
+void bddc_apply(Bddc& b, const double* r, double* z);                  // n_interface -> n_interface
 // adapt.cpp:35-124: per_tet (device, n_tets) = eta_tau, optional eta_tau^2 copy, global = sqrt(sum eta^2)
 void estimate(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, int kind, double* per_tet,
               double* eta_sq_out, double* global);

@@ -148,6 +148,19 @@ def lib():
         "rd_gpu_estimate": (_I, [_P, _P, _P, _P, _P, _P, _P]),
         "rd_gpu_mark_dorfler": (_I, [_P, _I, _P, _D, _P, _P]),
         "rd_gpu_adaptive_solve": (_I, [_P, _P, _P, _D, _I, _D, _D, _P, _I, _P, _P, _P, _I]),
+        "rd_gpu_partition_geometric": (_I, [_P, _P, _P, _I, _P]),
+        "rd_gpu_bddc_create": (_I, [_P, _P, _P, _I, _P]),
+        "rd_gpu_bddc_free": (None, [_P]),
+        "rd_gpu_bddc_info": (_I, [_P, _P, _P]),
+        "rd_gpu_bddc_interface_dofs": (_I, [_P, _P]),
+        "rd_gpu_bddc_coarse_matrix": (_I, [_P, _P]),
+        "rd_gpu_bddc_schur_apply": (_I, [_P, _P, _P]),
+        "rd_gpu_bddc_reduce_rhs": (_I, [_P, _P, _P]),
+        "rd_gpu_bddc_expand": (_I, [_P, _P, _P, _P]),
+        "rd_gpu_bddc_apply": (_I, [_P, _P, _P]),
+        "rd_gpu_linop_bddc_schur": (_I, [_P, _P]),
+        "rd_gpu_linop_bddc": (_I, [_P, _P]),
+        "rd_gpu_bddc_solve": (_I, [_P, _P, _P, _I, _D, _I, _P, _P, _P]),
         "rd_gpu_linop_identity": (_I, [_P]),
         "rd_gpu_linop_csr": (_I, [_P, _P]),
         "rd_gpu_linop_amg": (_I, [_P, _P]),
@@ -883,3 +896,80 @@ def adaptive_solve(initial: TetMesh, target: str, rho: float, dof_budget: int, t
     rows = [dict(level=r.level, dofs=r.dofs, iterations=r.iterations, eta=r.eta, err_l2_sq=r.err_l2_sq,
                  err_hm1_sq=r.err_hm1_sq, seconds=r.seconds) for r in hist[: min(k.value, cap)]]
     return AdaptResult(rows, TetMesh(fm, ctx), co[: rows[-1]["dofs"]].copy())
+
+
+# ------------------------------------------------------------------ BDDC
+def partition_geometric(sys: FemSystem, p: int) -> np.ndarray:
+    """bddc.hpp:30 / bddc.cpp:45-111: the RCB owner of every tet."""
+    out = np.zeros(max(sys.mesh.n_tets, 1), np.int32)
+    sys.ctx.check(lib().rd_gpu_partition_geometric(sys.ctx.h, sys.mesh.h, sys.h, int(p), _ptr(out)))
+    return out[: sys.mesh.n_tets]
+
+
+class Bddc:
+    """bddc.hpp BddcOperator on the device."""
+
+    def __init__(self, sys: FemSystem, p: int):
+        self.ctx = sys.ctx
+        self.sys = sys
+        h = _P()
+        self.ctx.check(lib().rd_gpu_bddc_create(self.ctx.h, sys.mesh.h, sys.h, int(p), C.byref(h)))
+        self.h = h
+        ni, npr = C.c_int(), C.c_int()
+        lib().rd_gpu_bddc_info(h, C.byref(ni), C.byref(npr))
+        self.n_interface, self.n_primal, self.n_dofs = ni.value, npr.value, sys.n_dofs
+        d = np.zeros(max(self.n_interface, 1), np.int32)
+        lib().rd_gpu_bddc_interface_dofs(h, _ptr(d))
+        self.interface_dofs = d[: self.n_interface]
+
+    def coarse_matrix(self):
+        out = np.zeros(max(self.n_primal ** 2, 1))
+        self.ctx.check(lib().rd_gpu_bddc_coarse_matrix(self.h, _ptr(out)))
+        return out[: self.n_primal ** 2].reshape(self.n_primal, self.n_primal)
+
+    def _vec(self, fn, x, n_out, *extra):
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.zeros(max(n_out, 1))
+        args = [self.h, _ptr(x) if x.size else None] + [(_ptr(np.ascontiguousarray(e, np.float64))) for e in extra]
+        self.ctx.check(fn(*args, _ptr(out)))
+        return out[:n_out]
+
+    def schur_apply(self, x):
+        return self._vec(lib().rd_gpu_bddc_schur_apply, x, self.n_interface)
+
+    def reduce_rhs(self, f):
+        return self._vec(lib().rd_gpu_bddc_reduce_rhs, f, self.n_interface)
+
+    def expand_solution(self, uC, f):
+        return self._vec(lib().rd_gpu_bddc_expand, uC, self.n_dofs, f)
+
+    def apply(self, r):
+        return self._vec(lib().rd_gpu_bddc_apply, r, self.n_interface)
+
+    def schur_op(self) -> LinOp:
+        st = _LinOp()
+        self.ctx.check(lib().rd_gpu_linop_bddc_schur(self.h, C.byref(st)))
+        return LinOp(st, keep=(self,))
+
+    def precond(self) -> LinOp:
+        st = _LinOp()
+        self.ctx.check(lib().rd_gpu_linop_bddc(self.h, C.byref(st)))
+        return LinOp(st, keep=(self,))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and not _closing:
+                lib().rd_gpu_bddc_free(self.h)
+        except Exception:
+            pass
+        self.h = None
+
+
+def bddc_solve(sys: FemSystem, p: int, tol: float = 1e-8, max_iter: int = 500) -> PcgResult:
+    """bddc.hpp:85-87 / bddc.cpp:440-456 on the device."""
+    u = np.zeros(max(sys.n_dofs, 1))
+    hist = np.zeros(max(max_iter, 1))
+    rep = _PcgReport()
+    sys.ctx.check(lib().rd_gpu_bddc_solve(sys.ctx.h, sys.mesh.h, sys.h, int(p), float(tol), int(max_iter), _ptr(u),
+                                          C.byref(rep), _ptr(hist)))
+    return PcgResult(u[: sys.n_dofs], rep.iterations, bool(rep.converged), hist[: rep.iterations].copy())
