@@ -13,4 +13,4 @@ for f in csrc/*.cu; do
 done
 wait
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o _build/variants/$name.so $out/*.o \
-  -lcudart_static -lrt -ldl -lpthread
+  -lcublas -lcusolver -lcudart_static -lrt -ldl -lpthread
