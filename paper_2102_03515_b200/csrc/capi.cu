@@ -13,6 +13,10 @@
 using namespace rdg;
 
 namespace rdg {
+bool pdl_enabled() {
+  static const bool on = !(getenv("RD_NO_PDL") && atoi(getenv("RD_NO_PDL")) != 0);
+  return on;
+}
 cudaMemPool_t library_pool(int device) {
   static std::mutex mu;
   static std::vector<cudaMemPool_t> pools;

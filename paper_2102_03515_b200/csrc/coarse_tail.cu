@@ -263,6 +263,8 @@ __global__ void __launch_bounds__(kTailNT, 1) coarse_tail_kernel(TailParams p) {
     if (p.clk && tid == 0) p.clk[ck] = clock64();
     ++ck;
   };
+  pdl_wait();
+  pdl_trigger();
   mark();
   // pull P / P^T into L2 first: between V-cycles the fine-level streams evict them
   if (tid >= 32 && tid - 32 < p.nlev) {
@@ -456,7 +458,7 @@ void coarse_tail(Ctx& c, Hierarchy& h, int c0, const double* r, double* z) {
   p.clk = nullptr;
 #endif
 
-  coarse_tail_kernel<<<1, kTailNT, tail_smem(h, c0), c.stream>>>(p);
+  launch_pdl(coarse_tail_kernel, 1, kTailNT, tail_smem(h, c0), c.stream, p);
   RDG_LAUNCH_CHECK();
   ++c.launches;
 #if RD_PROBES

@@ -170,6 +170,8 @@ __global__ void __launch_bounds__(kSpmvNT) spmv_staged_kernel(int rows, const in
                                                               double* dot_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SpmvSmem& sm = *reinterpret_cast<SpmvSmem*>(smem_raw);
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = (blockIdx.x * kSpmvWarps + warp) * 32;
   double contrib = 0.0;
@@ -272,6 +274,8 @@ __global__ void __launch_bounds__(kStNT) stencil_spmv_tiled_kernel(int L, int gx
   double(*rr)[kStRows * kStNT] = reinterpret_cast<double(*)[kStRows * kStNT]>(st_dyn + kStNR * kStPlane);
   __shared__ double red[kStNT / 32];
   const int tid = threadIdx.x, tx = tid % kStTX, ty = tid / kStTX;
+  pdl_wait();
+  pdl_trigger();
   for (int k = tid; k < (CLS ? 64 * 16 : 16); k += kStNT) st[k] = __ldg(tab + k);
   const int b = blockIdx.x;
   const int a0 = (b % gx) * kStTX, y0 = ((b / gx) % gy) * kStTY, z0 = (b / (gx * gy)) * zc;
@@ -423,9 +427,8 @@ void launch_spmv(Ctx& c, const DCsr& A, const double* x, double* y, const double
         RDG_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr = true;
     }
-    k<<<(unsigned)nb, kStNT, smem, c.stream>>>(L, gx, gy, zc, cls ? A.lat_cls.p : A.lat_uni.p, x, y, r, c.d_partials,
-                                            c.d_counter, dot_out);
-    RDG_LAUNCH_CHECK();
+    launch_pdl(k, (unsigned)nb, kStNT, smem, c.stream, L, gx, gy, zc, cls ? A.lat_cls.p : A.lat_uni.p, x, y, r,
+               c.d_partials, c.d_counter, dot_out);
     ++c.launches;
     if (!fused) dot(c, A.rows, x, y, dot_out);
     return;
@@ -440,16 +443,14 @@ void launch_spmv(Ctx& c, const DCsr& A, const double* x, double* y, const double
   }
   if (MODE == kDot && nb > Ctx::kMaxPartials) {
     // too many blocks for one partials array: plain SpMV then a separate dot
-    spmv_staged_kernel<kPlain><<<nb, kSpmvNT, smem, c.stream>>>(A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, nullptr,
-                                                               nullptr, nullptr);
-    RDG_LAUNCH_CHECK();
+    launch_pdl(spmv_staged_kernel<kPlain>, nb, kSpmvNT, smem, c.stream, A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, nullptr,
+               nullptr, nullptr);
     ++c.launches;
     dot(c, A.rows, x, y, dot_out);
     return;
   }
-  spmv_staged_kernel<MODE><<<nb, kSpmvNT, smem, c.stream>>>(A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, c.d_partials,
-                                                           c.d_counter, dot_out);
-  RDG_LAUNCH_CHECK();
+  launch_pdl(spmv_staged_kernel<MODE>, nb, kSpmvNT, smem, c.stream, A.rows, A.rp.p, A.ci.p, A.v.p, x, y, r, c.d_partials,
+             c.d_counter, dot_out);
   ++c.launches;
 }
 
@@ -457,6 +458,8 @@ void launch_spmv(Ctx& c, const DCsr& A, const double* x, double* y, const double
 __global__ void prolong_add_kernel(int rows, const int* __restrict__ rp, const int* __restrict__ ci,
                                    const double* __restrict__ val, const double* __restrict__ zc,
                                    double* __restrict__ z) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows) return;
   double s = 0.0;
@@ -470,6 +473,8 @@ __global__ void __launch_bounds__(kDotNT) dot_kernel(int64_t n, const double* __
                                                      const double* __restrict__ b, double* partials,
                                                      unsigned* counter, double* out) {
   __shared__ double sh[kDotNT / 32];
+  pdl_wait();
+  pdl_trigger();
   // fixed contiguous chunk per block, strided per thread -> deterministic
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t beg = (int64_t)blockIdx.x * per, end = min(n, beg + per);
@@ -490,8 +495,7 @@ void residual(Ctx& c, const DCsr& A, const double* r, const double* z, double* r
 }
 void prolong_add(Ctx& c, const DCsr& P, const double* zc, double* z) {
   if (P.rows == 0) return;
-  prolong_add_kernel<<<div_up(P.rows, 256), 256, 0, c.stream>>>(P.rows, P.rp.p, P.ci.p, P.v.p, zc, z);
-  RDG_LAUNCH_CHECK();
+  launch_pdl(prolong_add_kernel, div_up(P.rows, 256), 256, 0, c.stream, P.rows, P.rp.p, P.ci.p, P.v.p, zc, z);
   ++c.launches;
 }
 
@@ -505,8 +509,7 @@ void dot(Ctx& c, int64_t n, const double* a, const double* b, double* out_dev) {
     RDG_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), c.stream));
     return;
   }
-  dot_kernel<<<dot_grid(n), kDotNT, 0, c.stream>>>(n, a, b, c.d_partials, c.d_counter + 1, out_dev);
-  RDG_LAUNCH_CHECK();
+  launch_pdl(dot_kernel, dot_grid(n), kDotNT, 0, c.stream, n, a, b, c.d_partials, c.d_counter + 1, out_dev);
   ++c.launches;
 }
 

@@ -24,6 +24,8 @@ struct PcgState {
 namespace {
 
 __global__ void pcg_init_kernel(PcgState* st) {
+  pdl_wait();
+  pdl_trigger();
   // rz already in st->rz (written by the dot)
   const double rz = st->rz;
   st->done = 0;
@@ -39,6 +41,8 @@ __global__ void pcg_init_kernel(PcgState* st) {
 
 __global__ void pcg_xr_kernel(int64_t n, PcgState* st, const double* __restrict__ p, const double* __restrict__ Ap,
                               double* __restrict__ x, double* __restrict__ r) {
+  pdl_wait();
+  pdl_trigger();
   if (st->done || st->status) return;
   const double pAp = st->pAp;
   if (!(pAp > 0.0)) {
@@ -53,6 +57,8 @@ __global__ void pcg_xr_kernel(int64_t n, PcgState* st, const double* __restrict_
 }
 
 __global__ void pcg_check_kernel(PcgState* st, double tol, double* hist, int hist_cap) {
+  pdl_wait();
+  pdl_trigger();
   if (st->done || st->status) return;
   const double rzn = st->rz_next;
   if (rzn < 0.0) {
@@ -73,6 +79,8 @@ __global__ void pcg_check_kernel(PcgState* st, double tol, double* hist, int his
 }
 
 __global__ void pcg_p_kernel(int64_t n, const PcgState* st, const double* __restrict__ z, double* __restrict__ p) {
+  pdl_wait();
+  pdl_trigger();
   if (st->done || st->status) return;
   const double beta = st->beta;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -99,8 +107,7 @@ PcgResultDev pcg_ops(Ctx& c, int64_t n, const PcgOp& apply_A, const PcgOp& apply
   RDG_CUDA(cudaMemcpyAsync(r.p, f, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
   auto precond = [&](double* dot_out) { apply_P(r.p, z.p, dot_out); };
   precond(&st.p->rz);
-  pcg_init_kernel<<<1, 1, 0, c.stream>>>(st.p);
-  RDG_LAUNCH_CHECK();
+  launch_pdl(pcg_init_kernel, 1, 1, 0, c.stream, st.p);
   ++c.launches;
   PcgState* hs = reinterpret_cast<PcgState*>(c.h_pinned);
   RDG_CUDA(cudaMemcpyAsync(hs, st.p, sizeof(PcgState), cudaMemcpyDeviceToHost, c.stream));
@@ -117,8 +124,7 @@ PcgResultDev pcg_ops(Ctx& c, int64_t n, const PcgOp& apply_A, const PcgOp& apply
   // once converged they are no-ops (pcg_xr_kernel reads st->done; Ap and pAp are scratch)
   auto enqueue_ap_xr = [&]() {
     apply_A(p.p, Ap.p, &st.p->pAp);
-    pcg_xr_kernel<<<g, 256, 0, c.stream>>>(n, st.p, p.p, Ap.p, x, r.p);
-    RDG_LAUNCH_CHECK();
+    launch_pdl(pcg_xr_kernel, g, 256, 0, c.stream, n, st.p, p.p, Ap.p, x, r.p);
     ++c.launches;
   };
   static_assert(sizeof(PcgState) <= 8 * sizeof(double), "PcgState overlaps the pinned scratch");
@@ -126,10 +132,8 @@ PcgResultDev pcg_ops(Ctx& c, int64_t n, const PcgOp& apply_A, const PcgOp& apply
   if (max_iter >= 1) enqueue_ap_xr();  // max_iter <= 0: x stays 0 (linalg.cpp:66,77)
   for (int it = 1; it <= max_iter; ++it) {
     precond(&st.p->rz_next);
-    pcg_check_kernel<<<1, 1, 0, c.stream>>>(st.p, tol, hist_dev, max_iter);
-    RDG_LAUNCH_CHECK();
-    pcg_p_kernel<<<g, 256, 0, c.stream>>>(n, st.p, z.p, p.p);
-    RDG_LAUNCH_CHECK();
+    launch_pdl(pcg_check_kernel, 1, 1, 0, c.stream, st.p, tol, hist_dev, max_iter);
+    launch_pdl(pcg_p_kernel, g, 256, 0, c.stream, n, st.p, z.p, p.p);
     c.launches += 2;
     RDG_CUDA(cudaMemcpyAsync(hs, st.p, sizeof(PcgState), cudaMemcpyDeviceToHost, c.stream));
     RDG_CUDA(cudaMemcpyAsync(herr, c.d_err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));

@@ -40,3 +40,13 @@ for tile in (0, 1, 2, 8, 9, 15):
     print(f"tile {tile:2d}: " + " | ".join(row) + f" | w0 by (s+1)%4 {m4}")
     if full:
         print("  warp0 steps 20..60:", " ".join(str(v) for v in d[20:60]))
+cta = np.zeros((16, 4), dtype=np.uint64)
+if hasattr(lib, "rd_gpu_debug_gs_trace_cta") and lib.rd_gpu_debug_gs_trace_cta(cta.ctypes.data_as(C.c_void_p)) == 0:
+    cta = cta.astype(np.int64)
+    for tile in (0, 1, 2, 8, 15):
+        t = T[tile, 0]
+        k = np.nonzero(t)[0]
+        if len(k) == 0:
+            continue
+        print(f"tile {tile:2d}: prologue {cta[tile, 1] - cta[tile, 0]} cycles, first step end +{t[k[0]] - cta[tile, 1]}, "
+              f"steps {t[k[-1]] - t[k[0]]} over {len(k) - 1}, warp-0 end +{cta[tile, 2] - t[k[-1]]} (total {cta[tile, 2] - cta[tile, 0]})")
