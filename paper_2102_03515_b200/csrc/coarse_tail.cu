@@ -30,6 +30,9 @@ namespace {
 
 constexpr int kTailNT = 256;
 constexpr int kTailMaxL = 16;  // lattice side: L^2 <= kTailNT lines
+// shared-memory stride (doubles) of a class row: odd in 8-byte words * 2, so the same slot of
+// different rows falls in different banks (a warp's rows of one step span several classes)
+constexpr int kTbS = 17;
 
 struct TailLev {
   int n, L;
@@ -70,7 +73,16 @@ extern __shared__ __align__(16) double tail_sm[];  // every vector of the tail (
 // row is +0 and reads a halo +0, so its term is +0 * +0 = +0 and s - (+0) == s for
 // every s -- the boundary rows need no predicates and the row sum is a plain chain.
 __device__ __forceinline__ int padi(int a, int y, int z, int L) { return (a + 1) + (L + 2) * ((y + 1) + (L + 2) * (z + 1)); }
-__device__ __forceinline__ int padof(int i, int L) { return padi(i % L, (i / L) % L, i / (L * L), L); }
+// (the phases between the sweeps run once per V-cycle from a cold instruction cache, so their
+// code is kept compact: no inlined integer divisions, one copy of tail_spmv)
+__device__ __noinline__ int padof_div(int i, int L) { return padi(i % L, (i / L) % L, i / (L * L), L); }
+__device__ __forceinline__ int padof(int i, int L) {
+  if ((L & (L - 1)) == 0) {  // power-of-two side: shifts (uniform branch)
+    const int sh = 31 - __clz(L);
+    return padi(i & (L - 1), (i >> sh) & (L - 1), i >> (2 * sh), L);
+  }
+  return padof_div(i, L);
+}
 
 // one Gauss-Seidel pass in place on the padded x (shared), f (shared), the level's
 // class rows (tb, shared): nothing in the step loop touches global memory (a
@@ -97,6 +109,12 @@ __device__ void tail_sweep(const TailLev& lv, int fo, int xo, int tbo, int* err)
   const int oYp = sg * (1 + Q), oZp = sg * (1 + QQ), oYZp = sg * (1 + Q + QQ);
   double X1 = 0.0, Y1 = 0.0, Z1 = 0.0, D1 = 0.0;  // row a-1 of this / y-1 / z-1 / yz-1 lines (fresh)
   double Yp0 = 0.0, Zp0 = 0.0, YZp0 = 0.0;         // row a of the +y / +z / +yz lines (old)
+  // the class row of this line's x-interior rows lives in registers; the rows at a = 0, L-2,
+  // L-1 come from the table on a rarely taken branch (every class row starts at the same
+  // shared-memory bank, so a warp reading n different rows per step pays an n-way conflict)
+  double U[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) U[k] = tb[(1 * 16 + cyz) * kTbS + k];
   const int steps = 3 * (L - 1) + 1;
   for (int s = -1; s < steps; ++s) {
     const int a = s - y - z;
@@ -107,13 +125,14 @@ __device__ void tail_sweep(const TailLev& lv, int fo, int xo, int tbo, int* err)
       const double Yp1 = x[ip + oYp], Zp1 = x[ip + oZp], YZp1 = x[ip + oYZp];
       double xn = 0.0;
       if (a >= 0) {
-        const double2* row = reinterpret_cast<const double2*>(tb + (pos_class(ao, L) * 16 + cyz) * 16);
+        const int cx = pos_class(ao, L);
         double v[16];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const double2 t = row[k];
-          v[2 * k] = t.x;
-          v[2 * k + 1] = t.y;
+        for (int k = 0; k < 16; ++k) v[k] = U[k];
+        if (cx != 1) {
+          const double* row = tb + (cx * 16 + cyz) * kTbS;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = row[k];
         }
         // ascending original column order: the sweep-offset slots in the reference's order
         const double nf[15] = {D1, D0, Z1, Z0, Y1, Y0, X1, 0.0, Xp, Yp0, Yp1, Zp0, Zp1, YZp0, YZp1};
@@ -150,9 +169,36 @@ __device__ void tail_residual(const TailLev& lv, int ro, int zo, int reso, int t
   const double* tb = tail_sm + tbo;
   const int L = lv.L, P = L * L, Q = L + 2, QQ = Q * Q;
   const int off[15] = {-1 - Q - QQ, -Q - QQ, -1 - QQ, -QQ, -1 - Q, -Q, -1, 0, 1, Q, 1 + Q, QQ, 1 + QQ, Q + QQ, 1 + Q + QQ};
+  if ((L & (L - 1)) == 0 && (kTailNT % P == 0 || P % kTailNT == 0)) {
+    // power-of-two side: a thread's rows i = tid + j * kTailNT share (a, y) and walk z, so the
+    // row of its z-interior class lives in registers; the rows at z = 0, L-2, L-1 come from
+    // the table (z is warp-uniform for L >= 8, so the branch does not diverge)
+    const int sh = 31 - __clz(L);
+    const int a = threadIdx.x & (L - 1), y = (threadIdx.x >> sh) & (L - 1);
+    const int cay = (pos_class(a, L) * 4 + pos_class(y, L)) * 4;
+    double U[15];
+#pragma unroll
+    for (int k = 0; k < 15; ++k) U[k] = tb[(cay + 1) * kTbS + k];
+    for (int i = threadIdx.x; i < lv.n; i += kTailNT) {
+      const int zz = i >> (2 * sh), cz = pos_class(zz, L);
+      double v[15];
+#pragma unroll
+      for (int k = 0; k < 15; ++k) v[k] = U[k];
+      if (cz != 1) {
+#pragma unroll
+        for (int k = 0; k < 15; ++k) v[k] = tb[(cay + cz) * kTbS + k];
+      }
+      const int ip = padi(a, y, zz, L);
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 15; ++k) s = __dadd_rn(s, __dmul_rn(v[k], z[ip + off[k]]));
+      res[i] = __dsub_rn(r[i], s);
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < lv.n; i += kTailNT) {
     const int a = i % L, y = (i / L) % L, zz = i / P;
-    const double* v = tb + ((pos_class(a, L) * 4 + pos_class(y, L)) * 4 + pos_class(zz, L)) * 16;
+    const double* v = tb + ((pos_class(a, L) * 4 + pos_class(y, L)) * 4 + pos_class(zz, L)) * kTbS;
     const int ip = padi(a, y, zz, L);
     double s = 0.0;
 #pragma unroll
@@ -163,7 +209,7 @@ __device__ void tail_residual(const TailLev& lv, int ro, int zo, int reso, int t
 
 // y = M x for a CSR block in global memory (x, y shared; xL / yL > 0: that vector is
 // padded for a side-L lattice), sums from +0; four rows in flight per thread
-__device__ void tail_spmv(int rows, const int* rp, const int* ci, const double* val, int xo, int xL, int yo, int yL,
+__device__ __noinline__ void tail_spmv(int rows, const int* rp, const int* ci, const double* val, int xo, int xL, int yo, int yL,
                           bool add) {
   const double* x = tail_sm + xo;
   double* y = tail_sm + yo;
@@ -176,12 +222,28 @@ __device__ void tail_spmv(int rows, const int* rp, const int* ci, const double* 
       b[u] = i < rows ? __ldg(rp + i) : 0;
       e[u] = i < rows ? __ldg(rp + i + 1) : 0;
     }
+    // the first E entries of all U rows are loaded before any is used (global latency is
+    // paid once per batch, not once per entry); longer rows finish in a plain loop
+    constexpr int E = 4;
+    int cc[U][E];
+    double vv[U][E];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        const bool in = b[u] + j < e[u];
+        cc[u][j] = in ? __ldg(ci + b[u] + j) : 0;
+        vv[u][j] = in ? __ldg(val + b[u] + j) : 0.0;
+      }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * kTailNT;
       if (i >= rows) break;
       double s = 0.0;
-      for (int k = b[u]; k < e[u]; ++k) {
+#pragma unroll
+      for (int j = 0; j < E; ++j)
+        if (b[u] + j < e[u]) s = __dadd_rn(s, __dmul_rn(vv[u][j], x[xL ? padof(cc[u][j], xL) : cc[u][j]]));
+      for (int k = b[u] + E; k < e[u]; ++k) {
         const int c = __ldg(ci + k);
         s = __dadd_rn(s, __dmul_rn(__ldg(val + k), x[xL ? padof(c, xL) : c]));
       }
@@ -194,15 +256,18 @@ __device__ void tail_spmv(int rows, const int* rp, const int* ci, const double* 
 // the coarsest LLT substitutions (the order of llt_solve_kernel) by warp 0 alone:
 // lane l keeps rows l, l+32, ... in registers, the pivot's quotient is broadcast by
 // shuffle, divisions on the diagonal's precomputed reciprocal (exact fallback)
+// (the factor sits in shared memory with the odd row stride n | 1: the forward substitution
+// reads a column, which at stride n = 64 would put all 32 lanes in one bank)
 __device__ void tail_llt(int n, const double* Lm, const double* rcp, double* rc) {
   if (threadIdx.x >= 32) return;
+  const int ld = n | 1;
   const int lane = threadIdx.x;
   constexpr int R = 4;  // n <= 128
   double v[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) v[j] = lane + 32 * j < n ? rc[lane + 32 * j] : 0.0;
   auto quot = [&](double sk, int k) {
-    const double d = Lm[k * n + k], y = rcp[k];
+    const double d = Lm[k * ld + k], y = rcp[k];
     double q = div_fast(sk, d, y);
     if (!(sk == 0.0 || div_is_fast(sk, d, q))) q = div_exact(sk, d);
     return sk == 0.0 ? __dmul_rn(sk, y) : q;
@@ -219,7 +284,7 @@ __device__ void tail_llt(int n, const double* Lm, const double* rcp, double* rc)
     for (int j = 0; j < R; ++j) {
       const int i = lane + 32 * j;
       if (i == k) v[j] = yk;
-      if (i > k && i < n) v[j] = __dsub_rn(v[j], __dmul_rn(Lm[i * n + k], yk));
+      if (i > k && i < n) v[j] = __dsub_rn(v[j], __dmul_rn(Lm[i * ld + k], yk));
     }
   }
   for (int k = n - 1; k >= 0; --k) {
@@ -234,7 +299,7 @@ __device__ void tail_llt(int n, const double* Lm, const double* rcp, double* rc)
     for (int j = 0; j < R; ++j) {
       const int i = lane + 32 * j;
       if (i == k) v[j] = xk;
-      if (i < k) v[j] = __dsub_rn(v[j], __dmul_rn(Lm[k * n + i], xk));
+      if (i < k) v[j] = __dsub_rn(v[j], __dmul_rn(Lm[k * ld + i], xk));
     }
   }
 #pragma unroll
@@ -254,8 +319,9 @@ __global__ void __launch_bounds__(kTailNT, 1) coarse_tail_kernel(TailParams p) {
   auto zo = [&](int k) { return ro(k) + p.lv[k].n; };
   int maxn = 0;
   for (int k = 0; k < p.nlev; ++k) maxn = max(maxn, p.lv[k].n);
-  const int reso = ro(p.nlev), rco = reso + maxn, lo = rco + p.nc, dro = lo + p.nc * p.nc;
-  auto tbo = [&](int k) { return ((dro + p.nc + 1) & ~1) + k * 64 * 16; };  // class rows (16-B aligned)
+  const int ldc = p.nc | 1;
+  const int reso = ro(p.nlev), rco = reso + maxn, lo = rco + p.nc, dro = lo + p.nc * ldc;
+  auto tbo = [&](int k) { return ((dro + p.nc + 1) & ~1) + k * 64 * kTbS; };  // class rows
   double* Rc = tail_sm + rco;
   const int tid = threadIdx.x;
   int ck = 0;
@@ -275,11 +341,17 @@ __global__ void __launch_bounds__(kTailNT, 1) coarse_tail_kernel(TailParams p) {
     l2_prefetch(lv.tci, np * 4);
     l2_prefetch(lv.tv, np * 8);
   }
-  for (int i = tid; i < p.lv[0].n; i += kTailNT) tail_sm[i] = p.r[i];
+  // r, the class rows and the coarsest factor arrive through cp.async (all in flight at once)
+  auto cp8 = [](double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+  };
+  for (int i = tid; i < p.lv[0].n; i += kTailNT) cp8(tail_sm + i, p.r + i);
   for (int k = 0; k < p.nlev; ++k)
-    for (int i = tid; i < 64 * 16; i += kTailNT) tail_sm[tbo(k) + i] = __ldg(p.lv[k].table + i);
-  for (int i = tid; i < p.nc * p.nc; i += kTailNT) tail_sm[lo + i] = __ldg(p.Lc + i);
+    for (int i = tid; i < 64 * 16; i += kTailNT) cp8(tail_sm + tbo(k) + (i >> 4) * kTbS + (i & 15), p.lv[k].table + i);
+  for (int i = tid; i < p.nc * p.nc; i += kTailNT) cp8(tail_sm + lo + (i / p.nc) * ldc + i % p.nc, p.Lc + i);
   for (int i = tid; i < p.nc; i += kTailNT) tail_sm[dro + i] = div_recip(__ldg(p.Lc + i * p.nc + i));
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   mark();
   // ---- down: pre-smooth from zero, residual, restrict
@@ -367,7 +439,7 @@ size_t tail_smem(const Hierarchy& h, int c0) {
     maxn = std::max(maxn, (size_t)h.levels[l].A.rows);
   }
   if (h.nc > 128) return SIZE_MAX;  // tail_llt keeps at most 4 rows per lane
-  d += maxn + 2 * (size_t)h.nc + (size_t)h.nc * h.nc + 1 + (size_t)(h.levels.size() - 1 - c0) * 64 * 16;
+  d += maxn + 2 * (size_t)h.nc + (size_t)h.nc * (h.nc | 1) + 1 + (size_t)(h.levels.size() - 1 - c0) * 64 * kTbS;
   return d * sizeof(double);
 }
 
