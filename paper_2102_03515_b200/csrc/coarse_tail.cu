@@ -209,6 +209,7 @@ __device__ void tail_residual(const TailLev& lv, int ro, int zo, int reso, int t
 
 // y = M x for a CSR block in global memory (x, y shared; xL / yL > 0: that vector is
 // padded for a side-L lattice), sums from +0; four rows in flight per thread
+template <bool CHUNKED>
 __device__ __noinline__ void tail_spmv(int rows, const int* rp, const int* ci, const double* val, int xo, int xL, int yo, int yL,
                           bool add) {
   const double* x = tail_sm + xo;
@@ -222,33 +223,57 @@ __device__ __noinline__ void tail_spmv(int rows, const int* rp, const int* ci, c
       b[u] = i < rows ? __ldg(rp + i) : 0;
       e[u] = i < rows ? __ldg(rp + i + 1) : 0;
     }
-    // the first E entries of all U rows are loaded before any is used (global latency is
-    // paid once per batch, not once per entry); longer rows finish in a plain loop
-    constexpr int E = 4;
-    int cc[U][E];
-    double vv[U][E];
+    if constexpr (!CHUNKED) {  // long rows (P^T: up to 15 entries), few of them per thread
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int j = 0; j < E; ++j) {
-        const bool in = b[u] + j < e[u];
-        cc[u][j] = in ? __ldg(ci + b[u] + j) : 0;
-        vv[u][j] = in ? __ldg(val + b[u] + j) : 0.0;
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * kTailNT;
+        if (i >= rows) break;
+        double s = 0.0;
+        for (int k = b[u]; k < e[u]; ++k) {
+          const int c = __ldg(ci + k);
+          s = __dadd_rn(s, __dmul_rn(__ldg(val + k), x[xL ? padof(c, xL) : c]));
+        }
+        const int yi = yL ? padof(i, yL) : i;
+        y[yi] = add ? __dadd_rn(y[yi], s) : s;
       }
+      continue;
+    }
+    // short rows (P): entries in chunks of E per row, the chunk's loads of all U rows issued
+    // before any is used (global latency is paid once per chunk, not once per entry); sums in
+    // entry order
+    constexpr int E = 4;
+    double sacc[U];
+    int len = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      sacc[u] = 0.0;
+      len = max(len, e[u] - b[u]);
+    }
+    for (int o = 0; o < len; o += E) {
+      int cc[U][E];
+      double vv[U][E];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const int k = b[u] + o + j;
+          const bool in = k < e[u];
+          cc[u][j] = in ? __ldg(ci + k) : 0;
+          vv[u][j] = in ? __ldg(val + k) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < E; ++j)
+          if (b[u] + o + j < e[u])
+            sacc[u] = __dadd_rn(sacc[u], __dmul_rn(vv[u][j], x[xL ? padof(cc[u][j], xL) : cc[u][j]]));
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * kTailNT;
       if (i >= rows) break;
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < E; ++j)
-        if (b[u] + j < e[u]) s = __dadd_rn(s, __dmul_rn(vv[u][j], x[xL ? padof(cc[u][j], xL) : cc[u][j]]));
-      for (int k = b[u] + E; k < e[u]; ++k) {
-        const int c = __ldg(ci + k);
-        s = __dadd_rn(s, __dmul_rn(__ldg(val + k), x[xL ? padof(c, xL) : c]));
-      }
       const int yi = yL ? padof(i, yL) : i;
-      y[yi] = add ? __dadd_rn(y[yi], s) : s;
+      y[yi] = add ? __dadd_rn(y[yi], sacc[u]) : sacc[u];
     }
   }
 }
@@ -367,7 +392,7 @@ __global__ void __launch_bounds__(kTailNT, 1) coarse_tail_kernel(TailParams p) {
     tail_residual(lv, ro(k), zo(k), reso, tbo(k));
     __syncthreads();
     mark();
-    tail_spmv(k + 1 < p.nlev ? p.lv[k + 1].n : p.nc, lv.trp, lv.tci, lv.tv, reso, 0, k + 1 < p.nlev ? ro(k + 1) : rco,
+    tail_spmv<false>(k + 1 < p.nlev ? p.lv[k + 1].n : p.nc, lv.trp, lv.tci, lv.tv, reso, 0, k + 1 < p.nlev ? ro(k + 1) : rco,
               0, false);
     __syncthreads();
     mark();
@@ -380,7 +405,7 @@ __global__ void __launch_bounds__(kTailNT, 1) coarse_tail_kernel(TailParams p) {
   for (int k = p.nlev - 1; k >= 0; --k) {
     const TailLev& lv = p.lv[k];
     const bool fromc = k + 1 == p.nlev;
-    tail_spmv(lv.n, lv.prp, lv.pci, lv.pv, fromc ? rco : zo(k + 1), fromc ? 0 : p.lv[k + 1].L, zo(k), lv.L, true);
+    tail_spmv<true>(lv.n, lv.prp, lv.pci, lv.pv, fromc ? rco : zo(k + 1), fromc ? 0 : p.lv[k + 1].L, zo(k), lv.L, true);
     __syncthreads();
     mark();
     for (int s = 0; s < p.m; ++s) {
