@@ -766,6 +766,9 @@ def main():
         backend = "nccl" if torch.cuda.is_available() else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(local_rank)
+            # NCCL_DEBUG=VERSION prints "NCCL version ..." on stdout, which must carry one JSON line only
+            if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+                os.environ["NCCL_DEBUG"] = "WARN"
         torch.distributed.init_process_group(backend=backend)
     if args.impl == "reference":
         res = run_reference(args, rank, world)
