@@ -914,10 +914,11 @@ __device__ __forceinline__ int support_class(int kind, const double (&V)[4][3]) 
 }
 
 // per tet: vol (mesh.cpp:188-191 cross-product formula) and acc[iv] =
-// sum_q (w_q u(x_q)) lambda_q,iv for all four iv (assembly.cpp:152-171)
+// sum_q (w_q u(x_q)) lambda_q,iv for all four iv (assembly.cpp:152-171); stored as the four
+// products vol * acc[iv] the gather adds up (one array, one read per incident tet)
 template <int NQ>
 __global__ void load_tet_kernel(int nt, const int* __restrict__ tets, const double* __restrict__ xyz, int kind,
-                                const double* __restrict__ nodal, int n, double* tacc, double* tvol) {
+                                const double* __restrict__ nodal, int n, double* tacc) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nt) return;
   // tets == null: a Kuhn-lattice mesh, its tets by formula (the same ids the check compared)
@@ -939,7 +940,7 @@ __global__ void load_tet_kernel(int nt, const int* __restrict__ tets, const doub
   const double x1 = __dsub_rn(__dmul_rn(a[2], b[0]), __dmul_rn(a[0], b[2]));
   const double x2 = __dsub_rn(__dmul_rn(a[0], b[1]), __dmul_rn(a[1], b[0]));
   const double dt = __dadd_rn(__dadd_rn(__dmul_rn(x0, d[0]), __dmul_rn(x1, d[1])), __dmul_rn(x2, d[2]));
-  tvol[t] = div_tail(fabs(dt), 6.0, div_recip(6.0));  // == __ddiv_rn(|dt|, 6.0)
+  const double vol = div_tail(fabs(dt), 6.0, div_recip(6.0));  // == __ddiv_rn(|dt|, 6.0)
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   // Indicator targets: a tet whose closed hull is (with a 1e-9 margin, far above
   // the rounding of a quadrature point) entirely outside the support integrates
@@ -949,8 +950,9 @@ __global__ void load_tet_kernel(int nt, const int* __restrict__ tets, const doub
   if (cls != 0) {
     const double* in = NQ == 14 ? c_rules.in14 : c_rules.in64;
     const bool inside = cls > 0;
-    reinterpret_cast<double4*>(tacc)[t] = inside ? make_double4(in[0], in[1], in[2], in[3])
-                                                 : make_double4(0.0, 0.0, 0.0, 0.0);
+    reinterpret_cast<double4*>(tacc)[t] =
+        inside ? make_double4(__dmul_rn(vol, in[0]), __dmul_rn(vol, in[1]), __dmul_rn(vol, in[2]), __dmul_rn(vol, in[3]))
+               : make_double4(__dmul_rn(vol, 0.0), __dmul_rn(vol, 0.0), __dmul_rn(vol, 0.0), __dmul_rn(vol, 0.0));
     return;
   }
   for (int q = 0; q < NQ; ++q) {
@@ -968,12 +970,13 @@ __global__ void load_tet_kernel(int nt, const int* __restrict__ tets, const doub
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc[k] = __dadd_rn(acc[k], __dmul_rn(wu, lam[k]));
   }
-  reinterpret_cast<double4*>(tacc)[t] = make_double4(acc[0], acc[1], acc[2], acc[3]);
+  reinterpret_cast<double4*>(tacc)[t] =
+      make_double4(__dmul_rn(vol, acc[0]), __dmul_rn(vol, acc[1]), __dmul_rn(vol, acc[2]), __dmul_rn(vol, acc[3]));
 }
 
 __global__ void load_gather_kernel(int nd, const int* __restrict__ d2v, const int* __restrict__ vto,
                                    const int* __restrict__ vt, const int* __restrict__ tets,
-                                   const double* __restrict__ tacc, const double* __restrict__ tvol, double* f) {
+                                   const double* __restrict__ tacc, double* f) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nd) return;
   const int v = d2v[r];
@@ -982,7 +985,7 @@ __global__ void load_gather_kernel(int nd, const int* __restrict__ d2v, const in
     const int t = vt[k];
     const int4 t4 = reinterpret_cast<const int4*>(tets)[t];
     const int iv = t4.x == v ? 0 : t4.y == v ? 1 : t4.z == v ? 2 : 3;
-    s = __dadd_rn(s, __dmul_rn(tvol[t], tacc[4 * (int64_t)t + iv]));
+    s = __dadd_rn(s, tacc[4 * (int64_t)t + iv]);
   }
   f[r] = s;
 }
@@ -990,25 +993,25 @@ __global__ void load_gather_kernel(int nd, const int* __restrict__ d2v, const in
 // load_gather_kernel on the lattice: the 24 incident tets by formula
 template <int E>
 __device__ __forceinline__ void lat_load_tet(int ci, int cj, int ck, int n, const double* __restrict__ tacc,
-                                             const double* __restrict__ tvol, double& s) {
+                                             double& s) {
   constexpr LatRowTet T = kLatTab.t[E];
   const int64_t cell = ((int64_t)(ck - (T.o >> 2 & 1)) * n + (cj - (T.o >> 1 & 1))) * n + (ci - (T.o & 1));
   const int64_t t = cell * 6 + T.p;
-  s = __dadd_rn(s, __dmul_rn(tvol[t], tacc[4 * t + T.iv]));
+  s = __dadd_rn(s, tacc[4 * t + T.iv]);
 }
 template <int... E>
 __device__ __forceinline__ void lat_load_all(std::integer_sequence<int, E...>, int i, int j, int k, int n,
-                                             const double* tacc, const double* tvol, double& s) {
-  (lat_load_tet<E>(i, j, k, n, tacc, tvol, s), ...);
+                                             const double* tacc, double& s) {
+  (lat_load_tet<E>(i, j, k, n, tacc, s), ...);
 }
 __global__ void lat_load_gather_kernel(int nd, int n, const int* __restrict__ d2v, const double* __restrict__ tacc,
-                                       const double* __restrict__ tvol, double* f) {
+                                       double* f) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nd) return;
   const int nv = n + 1;
   const int v = d2v[r];
   double s = 0.0;
-  lat_load_all(std::make_integer_sequence<int, 24>{}, v % nv, v / nv % nv, v / (nv * nv), n, tacc, tvol, s);
+  lat_load_all(std::make_integer_sequence<int, 24>{}, v % nv, v / nv % nv, v / (nv * nv), n, tacc, s);
   f[r] = s;
 }
 
@@ -1224,6 +1227,32 @@ void launch_lattice_tets_check(Ctx& c, cudaStream_t st, int n, const int* tets, 
   ++c.launches;
 }
 
+// the unit-cube lattice's vertices and boundary flags (build_structured_cube's) on stream st
+void launch_cube_vertices(Ctx& c, cudaStream_t st, int n, double* xyz, uint8_t* bnd) {
+  const int64_t nv = (int64_t)(n + 1) * (n + 1) * (n + 1);
+  cube_vertices_kernel<<<div_up(nv, 256), 256, 0, st>>>(n, xyz, bnd);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+}
+
+// *bad = 1 unless the two vertex arrays (bit for bit) and boundary flags are equal
+__global__ void verts_equal_kernel(int64_t nv, const unsigned long long* __restrict__ a,
+                                   const unsigned long long* __restrict__ b, const uint8_t* __restrict__ fa,
+                                   const uint8_t* __restrict__ fb, int* bad) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  if (a[3 * v] != b[3 * v] || a[3 * v + 1] != b[3 * v + 1] || a[3 * v + 2] != b[3 * v + 2] ||
+      (fa[v] != 0) != (fb[v] != 0))
+    *bad = 1;
+}
+void launch_verts_equal(Ctx& c, cudaStream_t st, int64_t nv, const double* a, const double* b, const uint8_t* fa,
+                        const uint8_t* fb, int* bad) {
+  verts_equal_kernel<<<div_up(nv, 256), 256, 0, st>>>(nv, reinterpret_cast<const unsigned long long*>(a),
+                                                      reinterpret_cast<const unsigned long long*>(b), fa, fb, bad);
+  RDG_LAUNCH_CHECK();
+  ++c.launches;
+}
+
 void detect_cube_lattice(Ctx& c, DMesh& m) {
   m.lattice_n = -1;
   if (m.nt < 6 || m.nt % 6) return;
@@ -1419,19 +1448,19 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
       RDG_LAUNCH_CHECK();
       ++c.launches;
     }
-    DBuf<double> tacc((size_t)nt * 4, c.stream), tvol(nt, c.stream);
+    DBuf<double> tacc((size_t)nt * 4, c.stream);
     const bool disc = kind == RD_TARGET_BOX || kind == RD_TARGET_BALL;  // Smoothness::discontinuous
     const int* tp = lattice ? nullptr : m.tets.p;  // the lattice path reads no tets
     if (disc)
-      load_tet_kernel<64><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, tp, m.xyz.p, kind, nodal.p, n, tacc.p, tvol.p);
+      load_tet_kernel<64><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, tp, m.xyz.p, kind, nodal.p, n, tacc.p);
     else
-      load_tet_kernel<14><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, tp, m.xyz.p, kind, nodal.p, n, tacc.p, tvol.p);
+      load_tet_kernel<14><<<div_up(nt, 128), 128, 0, c.stream>>>(nt, tp, m.xyz.p, kind, nodal.p, n, tacc.p);
     RDG_LAUNCH_CHECK();
     if (lattice)
-      lat_load_gather_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, n, s.d2v.p, tacc.p, tvol.p, s.f.p);
+      lat_load_gather_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, n, s.d2v.p, tacc.p, s.f.p);
     else
       load_gather_kernel<<<div_up(nd, 256), 256, 0, c.stream>>>(nd, s.d2v.p, vto.p, vt.p, m.tets.p, tacc.p,
-                                                                tvol.p, s.f.p);
+                                                                s.f.p);
     RDG_LAUNCH_CHECK();
     c.launches += 2;
   }

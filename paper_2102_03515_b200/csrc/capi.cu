@@ -1119,62 +1119,90 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
     m.xyz.alloc((size_t)nv * 3, c.stream);
     m.tets.alloc((size_t)nt * 4, c.stream);
     m.boundary.alloc(nv, c.stream);
-    if (nv) RDG_CUDA(cudaMemcpyAsync(m.xyz.p, xyz, sizeof(double) * 3 * nv, cudaMemcpyDefault, c.stream));
-    if (nv) RDG_CUDA(cudaMemcpyAsync(m.boundary.p, bnd, nv, cudaMemcpyDefault, c.stream));
-    // A mesh of Kuhn-lattice size is assembled and solved by the lattice path (which reads
-    // no tets) while its tets upload on a second stream and are checked against the Kuhn
-    // enumeration there; the check gates the result.  The host arrays live for this call.
+    // A mesh of Kuhn-lattice size is assembled and solved provisionally as build_structured_cube's
+    // mesh: its vertices and boundary flags are generated on the device, the lattice path reads no
+    // tets, and the solve starts at once.  The host arrays upload meanwhile on a second stream and
+    // are compared there -- vertices and flags bit for bit with the generated ones, tets with the
+    // Kuhn enumeration.  The vertex verdict is read after the setup phase (the upload is short):
+    // a different geometry restarts on the uploaded vertices.  The tets verdict gates the result:
+    // a mismatch reruns on the generic path.  The host arrays live for this call.
     const int cand = cube_lattice_candidate(nv, nt);
-    DBuf<int> bad(1, c.stream);
-    RDG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
+    static const bool noprov = getenv("RD_NO_PROVISIONAL_MESH") && atoi(getenv("RD_NO_PROVISIONAL_MESH")) != 0;
+    const bool prov = cand > 0 && nt > 0 && nv > 0 && !noprov;
+    DBuf<int> bad(2, c.stream);  // [0]: tets differ from the Kuhn enumeration, [1]: vertices / flags differ
+    RDG_CUDA(cudaMemsetAsync(bad.p, 0, 2 * sizeof(int), c.stream));
+    DBuf<double> xyz_up;
+    DBuf<uint8_t> bnd_up;
+    if (prov) {
+      xyz_up.alloc((size_t)nv * 3, c.stream);
+      bnd_up.alloc(nv, c.stream);
+      launch_cube_vertices(c, c.stream, cand, m.xyz.p, m.boundary.p);
+    } else if (nv) {
+      RDG_CUDA(cudaMemcpyAsync(m.xyz.p, xyz, sizeof(double) * 3 * nv, cudaMemcpyDefault, c.stream));
+      RDG_CUDA(cudaMemcpyAsync(m.boundary.p, bnd, nv, cudaMemcpyDefault, c.stream));
+    }
     // the upload stream and its events; declared after the buffers it writes, so on any
     // exit (including a throw before the work below is resolved) the upload is waited
-    // for before m.tets and bad are freed
+    // for before the buffers are freed
     struct Upload {
       cudaStream_t s = nullptr;
-      cudaEvent_t alloc = nullptr, done = nullptr;
+      cudaEvent_t alloc = nullptr, vdone = nullptr, done = nullptr;
       void close() {
         if (s) cudaStreamSynchronize(s);
         if (alloc) cudaEventDestroy(alloc);
+        if (vdone) cudaEventDestroy(vdone);
         if (done) cudaEventDestroy(done);
         if (s) cudaStreamDestroy(s);
         s = nullptr;
-        alloc = done = nullptr;
+        alloc = vdone = done = nullptr;
       }
       ~Upload() { close(); }
     } upl;
-    bool pending = false;
-    if (cand > 0 && nt > 0) {
+    if (prov) {
       RDG_CUDA(cudaStreamCreateWithFlags(&upl.s, cudaStreamNonBlocking));
       RDG_CUDA(cudaEventCreateWithFlags(&upl.alloc, cudaEventDisableTiming));
+      RDG_CUDA(cudaEventCreateWithFlags(&upl.vdone, cudaEventDisableTiming));
       RDG_CUDA(cudaEventCreateWithFlags(&upl.done, cudaEventDisableTiming));
-      RDG_CUDA(cudaEventRecord(upl.alloc, c.stream));  // the allocations and the flag reset
+      RDG_CUDA(cudaEventRecord(upl.alloc, c.stream));  // the allocations, the flag reset, the generated vertices
       RDG_CUDA(cudaStreamWaitEvent(upl.s, upl.alloc, 0));
+      RDG_CUDA(cudaMemcpyAsync(xyz_up.p, xyz, sizeof(double) * 3 * (size_t)nv, cudaMemcpyDefault, upl.s));
+      RDG_CUDA(cudaMemcpyAsync(bnd_up.p, bnd, nv, cudaMemcpyDefault, upl.s));
+      launch_verts_equal(c, upl.s, nv, xyz_up.p, m.xyz.p, bnd_up.p, m.boundary.p, bad.p + 1);
+      RDG_CUDA(cudaEventRecord(upl.vdone, upl.s));
       RDG_CUDA(cudaMemcpyAsync(m.tets.p, tets, sizeof(int) * 4 * (size_t)nt, cudaMemcpyDefault, upl.s));
       launch_lattice_tets_check(c, upl.s, cand, m.tets.p, nt, bad.p);
       RDG_CUDA(cudaEventRecord(upl.done, upl.s));
       m.lattice_n = cand;  // provisional until upl.done
       m.tets_ready = upl.done;
-      pending = true;
     } else {
       if (nt) RDG_CUDA(cudaMemcpyAsync(m.tets.p, tets, sizeof(int) * 4 * (size_t)nt, cudaMemcpyDefault, c.stream));
       detect_cube_lattice(c, m);
     }
-    // the upload stream's work is done (and checked) before anything here is freed
-    int verdict = pending ? -1 : 1;  // -1: the tets check has not been read yet
-    auto resolve = [&]() -> bool {   // true: the provisional lattice path stands
-      if (verdict < 0) {
+    // verdicts: -1 not read yet, 1 the provisional assumption stands, 0 it does not
+    int vverts = prov ? -1 : 1, vtets = prov ? -1 : 1;
+    auto verts_ok = [&]() -> bool {
+      if (vverts < 0) {
+        int hb = 1;
+        if (cudaEventSynchronize(upl.vdone) == cudaSuccess)
+          cudaMemcpy(&hb, bad.p + 1, sizeof(int), cudaMemcpyDeviceToHost);
+        vverts = hb ? 0 : 1;
+      }
+      return vverts == 1;
+    };
+    auto tets_ok = [&]() -> bool {  // also the point after which nothing runs on the upload stream
+      if (vtets < 0) {
         int hb = 1;
         if (cudaEventSynchronize(upl.done) == cudaSuccess)
           cudaMemcpy(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost);
         m.tets_ready = nullptr;
         upl.close();
-        verdict = hb ? 0 : 1;
+        vtets = hb ? 0 : 1;
         if (hb) m.lattice_n = -1;
       }
-      return verdict == 1;
+      return vtets == 1;
     };
-    auto run = [&](bool final) {
+    // one attempt; false: abandoned because a provisional assumption failed (nothing written to u)
+    auto run = [&](bool check_verts, bool check_tets) -> bool {
       using clk = std::chrono::steady_clock;
       DSystem sys;
       build_system(c, m, rho, target->kind, target->seed, sys);
@@ -1183,8 +1211,9 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
       if (n_dofs_out) *n_dofs_out = n;
       *out = rd_solve_outcome{0, 0, 0.0, 0.0};
       if (n == 0) {  // bench.cpp:187-191
+        if ((check_verts && !verts_ok()) || (check_tets && !tets_ok())) return false;
         out->converged = 1;
-        return;
+        return true;
       }
       OutVec<double> uo(c, u, n);
       RDG_CUDA(cudaStreamSynchronize(c.stream));
@@ -1193,6 +1222,7 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
       build_hierarchy(c, A, 64, 1, h, /*borrow=*/true);
       RDG_CUDA(cudaStreamSynchronize(c.stream));
       const auto t1 = clk::now();
+      if (check_verts && !verts_ok()) return false;  // the vertices arrived long ago: restart early
       PcgResultDev r;
       exact_retry(c, [&] {
         r = pcg_device(c, A, &h, sys.f.p, tol, 500, uo.dev(), nullptr);
@@ -1200,19 +1230,40 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
         sync_and_raise(c);
       });
       const auto t2 = clk::now();
-      if (final || resolve()) uo.finish();  // a mismatch reruns below; u is written by that run
+      // the download of u overlaps the rest of the tets upload; on a mismatch the rerun below
+      // overwrites it (as it does a device-resident u)
+      uo.finish();
+      if (check_tets && !tets_ok()) {
+        RDG_CUDA(cudaStreamSynchronize(c.stream));
+        return false;
+      }
       sync_and_raise(c);
       out->iterations = r.iterations;
       out->converged = r.converged ? 1 : 0;
       out->setup_seconds = std::chrono::duration<double>(t1 - t0).count();
       out->solve_seconds = std::chrono::duration<double>(t2 - t1).count();
+      return true;
     };
-    try {
-      run(false);
-    } catch (...) {
-      if (resolve()) throw;  // an error of the provisional path stands only for lattice tets
+    // an error of a provisional attempt stands only if its assumptions hold
+    auto attempt = [&](bool check_verts, bool check_tets) -> bool {
+      try {
+        return run(check_verts, check_tets);
+      } catch (...) {
+        if ((!check_verts || verts_ok()) && (!check_tets || tets_ok())) throw;
+        return false;
+      }
+    };
+    bool done = attempt(prov, prov);
+    if (!done && !verts_ok()) {  // the uploaded geometry replaces the generated one
+      // (the verdict was read after the upload stream's vdone event: xyz_up / bnd_up are complete)
+      RDG_CUDA(cudaMemcpyAsync(m.xyz.p, xyz_up.p, sizeof(double) * 3 * (size_t)nv, cudaMemcpyDeviceToDevice, c.stream));
+      RDG_CUDA(cudaMemcpyAsync(m.boundary.p, bnd_up.p, nv, cudaMemcpyDeviceToDevice, c.stream));
+      done = vtets == 0 ? false : attempt(false, vtets < 0);
     }
-    if (!resolve()) run(true);  // the generic path (lattice_n = -1), tets already on the device
+    if (!done) {
+      tets_ok();  // the generic path (lattice_n = -1 on a mismatch), tets already on the device
+      run(false, false);
+    }
   });
 }
 

@@ -203,6 +203,9 @@ void detect_cube_lattice(Ctx& c, DMesh& m);
 int cube_lattice_candidate(int nv, int nt);
 // bad[0] = 1 unless tets[0, nt) is the Kuhn enumeration of build_structured_cube(n); on stream st
 void launch_lattice_tets_check(Ctx& c, cudaStream_t st, int n, const int* tets, int nt, int* bad);
+void launch_cube_vertices(Ctx& c, cudaStream_t st, int n, double* xyz, uint8_t* bnd);
+void launch_verts_equal(Ctx& c, cudaStream_t st, int64_t nv, const double* a, const double* b, const uint8_t* fa,
+                        const uint8_t* fb, int* bad);
 void build_system(Ctx& c, const DMesh& m, double rho, int target_kind, uint64_t seed, DSystem& s);
 // l2 / h1-semi error of the P1 field `coeffs` (device, n_dofs) vs the manufactured exact solution
 void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, double rho, double* l2, double* h1);

@@ -1,7 +1,8 @@
 """rd_gpu_solve_host_mesh: the bench-precond row from a host TetMesh in one C-ABI call.
 
-For a mesh of Kuhn-lattice size the tet array uploads on a second stream while the lattice
-path assembles and solves; the uploaded tets are then checked against the Kuhn enumeration.
+For a mesh of Kuhn-lattice size the solve starts on generated unit-cube vertices while the host
+arrays upload on a second stream; the uploaded vertices / flags are compared with the generated
+ones and the uploaded tets with the Kuhn enumeration before any result stands.
 Checked against the three-call path (rd_gpu_mesh_create -> rd_gpu_build_system ->
 rd_gpu_solve_system_amg), which the parity suite pins to the oracle: the same u bit for bit
 and the same iteration count, on lattice meshes, on a lattice-sized mesh whose tets are not
@@ -76,6 +77,25 @@ def test_shuffled_tets_fall_back_to_generic_path(rd):
     tt = tets.copy()
     tt[[0, 1]] = tt[[1, 0]]
     _check(rd, xyz, np.ascontiguousarray(tt), b, 1.0 / (n * n), "smooth")
+
+
+def test_other_geometry_on_lattice_sized_mesh(rd):
+    """The solve starts on generated unit-cube vertices while the host vertices upload; any
+    other geometry (or boundary flags) must restart on the uploaded arrays."""
+    n = 16
+    xyz, tets, b = rd.build_structured_cube(n).download()
+    rng = np.random.default_rng(11)
+    xj = xyz.copy()
+    inner = b == 0
+    xj[inner] += (rng.random((int(inner.sum()), 3)) - 0.5) * (0.4 / n)  # jittered interior: lattice tets, other geometry
+    _check(rd, xj, tets, b, 1.0 / (n * n), "ball")
+    _check(rd, np.ascontiguousarray(xyz * 2.0), tets, b, 1.0 / (n * n), "smooth")  # a cube of side 2
+    xz = xyz.copy()
+    xz[0, 0] = -0.0  # equal as numbers, not as bits: handled like any other difference
+    _check(rd, xz, tets, b, 1.0 / (n * n), "smooth")
+    # both provisional assumptions fail: other geometry and tets that are not the enumeration
+    ts = np.ascontiguousarray(tets[rng.permutation(tets.shape[0])])
+    _check(rd, xj, ts, b, 1.0 / (n * n), "smooth")
 
 
 def test_custom_boundary_and_non_lattice_sizes(rd):
