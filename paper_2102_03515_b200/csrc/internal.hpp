@@ -44,6 +44,7 @@ struct DCsr {
   mutable DBuf<int> lat_uni_flag;   // device: [0] 1 = some row differs from the centre row,
                                     //         [1] 1 = some row differs from its class row
   mutable DBuf<double> lat_cls;     // [64][16] class rows (slot order, absent +0, reciprocal in 15)
+  mutable DBuf<int> lat_order;      // ticket -> tile, wavefront order (levels with more tiles than SMs)
   mutable int lat_uni_state = -1;
 };
 
