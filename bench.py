@@ -483,8 +483,9 @@ def run_ours(args, rank, world, local_rank):
         u_host = torch.empty(ndofs, dtype=torch.float64).pin_memory()
 
         def e2e_step():
-            # one C-ABI call: mesh upload (the tets overlap the lattice-path solve and are
-            # checked after it), build_system, build_amg + pcg, u back to pinned host memory
+            # one C-ABI call: mesh upload (overlapping the provisional lattice-path solve, every
+            # array checked before the result stands), build_system, build_amg + pcg, u back to
+            # pinned host memory
             out = rd.solve_host_mesh(pxyz.numpy(), ptets.numpy(), pbnd.numpy(), rho, args.target, TOL,
                                      u=u_host, ctx=ctx)
             return out.iterations
@@ -512,7 +513,9 @@ def run_ours(args, rank, world, local_rank):
                          "h2d_bytes_per_step": int(xyz.nbytes + tets.nbytes + bnd.nbytes),
                          "d2h_bytes_per_step": int(8 * ndofs),
                          "path": "rd_gpu_solve_host_mesh(pinned host TetMesh -> build_system -> build_amg + "
-                                 "pcg -> u in pinned host memory; tets upload overlapped, then checked)"}
+                                 "pcg -> u in pinned host memory; the solve starts on generated lattice "
+                                 "vertices while vertices, flags and tets upload, all three checked "
+                                 "against the upload before the result stands)"}
 
     # ---------------- the other BASELINE sizes on this GPU (C4 n=256, C5 n=512 = 133M dofs):
     # one timed solve each after a warm-up, same path; reported beside the C2 headline
