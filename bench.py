@@ -163,6 +163,24 @@ def run_dist(args, rank, world, local_rank):
         return _run_dist(args, rank, world, local_rank, dev, stream)
 
 
+def rank_memory(ctx, comm, last, make_solver):
+    """Pool bytes in use per rank with a distributed solver alive whose replicated setup objects
+    were released after localisation (rank 0 keeps the hierarchy for the coarse levels, the
+    other ranks their slabs only), and the peak the replicated setup reserved.  Measured on one
+    extra, untimed setup (the timed steps keep the setup objects: releasing them costs ~1 ms)."""
+    import gc
+
+    last.clear()
+    gc.collect()
+    solver = make_solver()
+    gc.collect()
+    used, reserved = ctx.pool_bytes()
+    del solver
+    return {"used_bytes_per_rank": comm.allgather_int(int(used)),
+            "reserved_bytes_per_rank": comm.allgather_int(int(reserved)),
+            "note": "steady state after localisation; the setup itself is still replicated (peak = reserved)"}
+
+
 def _run_dist(args, rank, world, local_rank, dev, stream):
     import torch
 
@@ -271,6 +289,12 @@ def _run_dist(args, rank, world, local_rank, dev, stream):
                           "achieved": by / (ms * 1e-3) / 1e9, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                           "frac": by / (ms * 1e-3) / 1e9 / peak, "traffic": None, "bytes_per_launch": by,
                           "launch_ms": ms}
+    # per-rank memory in steady state (one extra, untimed setup whose replicated objects are released)
+    del ops, f, xin, xo
+    solver = None
+    result["memory"] = rank_memory(ctx, comm, last, lambda: DistSolver(
+        comm, DeviceOps(n, rho, args.target, ctx=ctx, device=local_rank, mesh=mesh),
+        gather_rows=args.gather_rows, mode=args.mode, release_replicated=True))
     # e2e: the same distributed solve, u gathered on rank 0 and read back to pinned host memory
     u_host = torch.empty(ndofs, dtype=torch.float64).pin_memory()
 

@@ -55,6 +55,11 @@ void* rd_gpu_ctx_stream(rd_ctx* ctx);
 int rd_gpu_synchronize(rd_ctx* ctx);
 /* Number of rd_gpu kernels launched on this context so far. */
 int64_t rd_gpu_launch_count(const rd_ctx* ctx);
+/* Bytes of the library's stream-ordered pool on the context's device: in use by live objects
+ * (*used) and held from the driver (*reserved).  One pool per device and process: with one
+ * process per GPU this is the rank's device footprint (the smoother's peer-mappable cell
+ * buffers, plain allocations, are not counted).  No reference counterpart. */
+int rd_gpu_pool_bytes(rd_ctx* ctx, uint64_t* used, uint64_t* reserved);
 const char* rd_gpu_version(void);
 /* cudaMemcpyDefault between any host/device buffers, ordered on the ctx stream, synchronous */
 int rd_gpu_copy(rd_ctx* ctx, void* dst, const void* src, size_t bytes);

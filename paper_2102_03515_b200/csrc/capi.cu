@@ -361,6 +361,18 @@ const char* rd_gpu_last_error(const rd_ctx* ctx) { return ctx ? ctx->c.err.c_str
 void* rd_gpu_ctx_stream(rd_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.stream) : nullptr; }
 int64_t rd_gpu_launch_count(const rd_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
+int rd_gpu_pool_bytes(rd_ctx* ctx, uint64_t* used, uint64_t* reserved) {
+  return guard(ctx, [&] {
+    require(used || reserved, "rd_gpu_pool_bytes: null argument");
+    RDG_CUDA(cudaStreamSynchronize(ctx->c.stream));  // stream-ordered frees have landed
+    uint64_t u = 0, r = 0;
+    RDG_CUDA(cudaMemPoolGetAttribute(ctx->c.pool, cudaMemPoolAttrUsedMemCurrent, &u));
+    RDG_CUDA(cudaMemPoolGetAttribute(ctx->c.pool, cudaMemPoolAttrReservedMemCurrent, &r));
+    if (used) *used = u;
+    if (reserved) *reserved = r;
+  });
+}
+
 int rd_gpu_copy(rd_ctx* ctx, void* dst, const void* src, size_t bytes) {
   return guard(ctx, [&] {
     if (!bytes) return;

@@ -301,6 +301,7 @@ class DeviceOps:
             # order with torch's current stream (handle 0 = the legacy default stream: cudaStreamLegacy)
             ctx = rd.Context(device, torch.cuda.current_stream(self.device).cuda_stream or 1)
         self.ctx = ctx or mesh.ctx
+        self.mesh_owned = mesh is None
         self.mesh = mesh if mesh is not None else rd.build_structured_cube(n, self.ctx)
         self.sys = rd.build_system(self.mesh, rho, target, seed)
         self.A = self.sys.A
@@ -312,7 +313,11 @@ class DeviceOps:
                            for l in range(nl)]
 
     # -- setup
-    def localize(self, plan: SlabPlan, rank: int):
+    def localize(self, plan: SlabPlan, rank: int, release_replicated: bool = False):
+        """Keep this rank's row blocks, slab smoothers and load-vector slab.  With
+        `release_replicated` the whole-box objects of the replicated setup are dropped afterwards
+        (everything on ranks > 0; rank 0 keeps the hierarchy, whose coarse levels it runs): the
+        steady-state footprint of a rank is then its slabs, not the whole problem."""
         rd, lib, C = self.rd, self.rd.lib(), __import__("ctypes")
         self.plan, self.rank = plan, rank
         self.blkA, self.blkP, self.blkPt, self.slab = [], [], [], []
@@ -347,8 +352,12 @@ class DeviceOps:
         self.f_local = self.vec(0)
         self.f_local[(lo - g0) * P0:(hi - g0) * P0].copy_(f_all[lo * P0:hi * P0])
         del f_all
-        if rank != 0:
-            pass  # the coarse tail runs on rank 0 only (the replicated hierarchy stays for now)
+        if release_replicated:
+            self.sys = self.A = None  # K, M, A, f of the whole box (build_amg keeps its own A)
+            if rank != 0:
+                self.h = None  # the coarse tail runs on rank 0 only
+            if self.mesh_owned:
+                self.mesh = None
 
     # -- vectors
     def vec(self, l: int, full: bool = False) -> torch.Tensor:
@@ -513,7 +522,7 @@ class DistSolver:
     """Slab-distributed AMG-PCG (linalg.cpp:64-102 with amg_precond, amg.cpp:119-145)."""
 
     def __init__(self, comm, ops, gather_rows: int | None = None, mode: str = "exact",
-                 dist_levels: int | None = None):
+                 dist_levels: int | None = None, release_replicated: bool = False):
         if mode not in ("exact", "block", "pipelined"):
             raise ValueError("mode must be 'exact', 'block' or 'pipelined'")
         self.comm, self.ops, self.mode = comm, ops, mode
@@ -521,7 +530,10 @@ class DistSolver:
         G = dist_levels or choose_dist_levels(ops.sides, ops.rows, ops.structured, self.world, gather_rows)
         self.plan = SlabPlan(ops.sides, self.world, G)
         self.G = G
-        ops.localize(self.plan, self.rank)
+        try:
+            ops.localize(self.plan, self.rank, release_replicated=release_replicated)
+        except TypeError:  # an ops class without the option (the host ops of the CPU tests)
+            ops.localize(self.plan, self.rank)
         if mode == "pipelined":
             # peer mapping of the neighbours' cell buffers; if any rank cannot map (no P2P
             # path, IPC unavailable) every rank falls back to the NCCL plane hand-off

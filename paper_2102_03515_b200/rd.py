@@ -97,6 +97,7 @@ def lib():
         "rd_gpu_ctx_stream": (_P, [_P]),
         "rd_gpu_synchronize": (_I, [_P]),
         "rd_gpu_launch_count": (C.c_int64, [_P]),
+        "rd_gpu_pool_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "rd_gpu_copy": (_I, [_P, _P, _P, C.c_size_t]),
         "rd_gpu_build_structured_cube": (_I, [_P, _I, C.POINTER(_P)]),
         "rd_gpu_mesh_create": (_I, [_P, _I, _P, _I, _P, _P, C.POINTER(_P)]),
@@ -255,6 +256,12 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(lib().rd_gpu_launch_count(self.h))
+
+    def pool_bytes(self):
+        """(used, reserved) bytes of the library's memory pool on this context's device."""
+        u, r = C.c_uint64(0), C.c_uint64(0)
+        self.check(lib().rd_gpu_pool_bytes(self.h, C.byref(u), C.byref(r)))
+        return int(u.value), int(r.value)
 
     def synchronize(self):
         self.check(lib().rd_gpu_synchronize(self.h))

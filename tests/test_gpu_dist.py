@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 pytestmark = pytest.mark.gpu
 
 
-def _run_ranks(world, n, rho, target, mode, gather_rows, solve=True):
+def _run_ranks(world, n, rho, target, mode, gather_rows, solve=True, release=False):
     import torch
 
     from paper_2102_03515_b200 import rd
@@ -38,11 +38,13 @@ def _run_ranks(world, n, rho, target, mode, gather_rows, solve=True):
             with torch.cuda.stream(s):
                 ctx = rd.Context(0, s.cuda_stream)
                 ops = DeviceOps(n, rho, target, ctx=ctx)
-                solver = DistSolver(ThreadComm(hub, rank), ops, gather_rows=gather_rows, mode=mode)
+                solver = DistSolver(ThreadComm(hub, rank), ops, gather_rows=gather_rows, mode=mode,
+                                    release_replicated=release)
                 z = ops.vec(0)
                 solver.apply(ops.f_local, z)
                 zf = solver.gather_solution(solver.own(0, z))
-                out = dict(G=solver.G, cuts=solver.plan.cuts, launches0=ctx.launch_count)
+                out = dict(G=solver.G, cuts=solver.plan.cuts, launches0=ctx.launch_count,
+                           kept=(ops.sys is not None, ops.h is not None), pool=ctx.pool_bytes())
                 if solve:
                     res = solver.pcg(1e-8, 500)
                     xf = solver.gather_solution(res.x_local)
@@ -94,6 +96,21 @@ def test_exact_slabs_match_single_gpu(world, gather_rows, G, mode):
     assert all(o["it"] == ref["it"] and o["conv"] for o in outs)
     assert all(o["hist"] == o0["hist"] for o in outs)
     err = np.abs(o0["x"] - ref["x"]).max() / np.abs(ref["x"]).max()
+    assert err <= 1e-10, err
+
+
+@pytest.mark.parametrize("mode", ["exact", "pipelined"])
+def test_replicated_setup_released_after_localisation(mode):
+    """release_replicated: the whole-box system goes on every rank and the hierarchy on ranks
+    > 0 once the row blocks and slab smoothers exist; the solve is unchanged."""
+    n, rho = 32, 2.0 ** -10
+    ref = _single(n, rho, "smooth")
+    outs = _run_ranks(2, n, rho, "smooth", mode, 600, release=True)
+    assert outs[0]["kept"] == (False, True) and outs[1]["kept"] == (False, False)
+    assert all(o["pool"][0] > 0 and o["pool"][1] >= o["pool"][0] for o in outs)
+    assert np.array_equal(outs[0]["z"], ref["z"])
+    assert all(o["it"] == ref["it"] and o["conv"] for o in outs)
+    err = np.abs(outs[0]["x"] - ref["x"]).max() / np.abs(ref["x"]).max()
     assert err <= 1e-10, err
 
 
