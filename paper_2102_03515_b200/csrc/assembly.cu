@@ -737,8 +737,8 @@ __global__ void __launch_bounds__(kLatNT) lat_split_kernel(int nd, int n, double
     }
     __syncwarp();
   };
-  emit(krp, kci, kv, 0);
-  emit(mrp, mci, mv, 1);
+  if (krp) emit(krp, kci, kv, 0);  // null: the caller wants A only
+  if (mrp) emit(mrp, mci, mv, 1);
   emit(arp, aci, av, 2);
 }
 
@@ -1285,7 +1285,7 @@ void build_structured_cube(Ctx& c, int n, DMesh& m) {
   c.launches += 2;
 }
 
-void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, DSystem& s) {
+void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, DSystem& s, bool a_only) {
   if (!(rho > 0.0)) throw Error(RD_EINVAL, "build_system: rho must be > 0");
   if (kind < 0 || kind > RD_TARGET_QUADRATIC) throw Error(RD_EINVAL, "build_system: unknown target kind");
   if (kind == RD_TARGET_SINE_RANDOM && m.lattice_n < 1)
@@ -1308,10 +1308,11 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
   RDG_LAUNCH_CHECK();
   c.launches += 2;
   DCsr* mats[3] = {&s.K, &s.M, &s.A};
-  auto alloc_split = [&](int* const* cnts) {
+  auto alloc_split = [&](int* const* cnts, bool only_a = false) {
     for (int w = 0; w < 3; ++w) {
       DCsr& X = *mats[w];
       X = DCsr{};
+      if (only_a && w < 2) continue;  // K, M stay empty
       X.rows = X.cols = nd;
       X.rp.alloc(nd + 1, c.stream);
       X.nnz = exclusive_scan(c, cnts[w], X.rp.p, nd);
@@ -1346,7 +1347,7 @@ void build_system(Ctx& c, const DMesh& m, double rho, int kind, uint64_t seed, D
     if (e == RD_EDEGENERATE) throw Error(RD_EDEGENERATE, "assembly: degenerate tet");
     if (e == 0) {
       int* cnts[3] = {kc.p, mc.p, ac.p};
-      alloc_split(cnts);
+      alloc_split(cnts, a_only);
       lat_split_kernel<<<div_up(nd, kLatNT), kLatNT, 0, c.stream>>>(
           nd, n, rho, s.d2v.p, s.v2d.p, Kp.p, Mp.p, mask.p, s.K.rp.p, s.K.ci.p, s.K.v.p, s.M.rp.p, s.M.ci.p,
           s.M.v.p, s.A.rp.p, s.A.ci.p, s.A.v.p, geo.p, km.p);

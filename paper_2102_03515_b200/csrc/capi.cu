@@ -1226,7 +1226,7 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
     auto run = [&](bool check_verts, bool check_tets) -> bool {
       using clk = std::chrono::steady_clock;
       DSystem sys;
-      build_system(c, m, rho, target->kind, target->seed, sys);
+      build_system(c, m, rho, target->kind, target->seed, sys, /*a_only=*/true);
       const DCsr& A = sys.A;
       const int n = A.rows;
       if (n_dofs_out) *n_dofs_out = n;

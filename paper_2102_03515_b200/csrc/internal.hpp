@@ -207,7 +207,10 @@ void launch_lattice_tets_check(Ctx& c, cudaStream_t st, int n, const int* tets, 
 void launch_cube_vertices(Ctx& c, cudaStream_t st, int n, double* xyz, uint8_t* bnd);
 void launch_verts_equal(Ctx& c, cudaStream_t st, int64_t nv, const double* a, const double* b, const uint8_t* fa,
                         const uint8_t* fb, int* bad);
-void build_system(Ctx& c, const DMesh& m, double rho, int target_kind, uint64_t seed, DSystem& s);
+// a_only: the caller needs A and f only (rd_gpu_solve_host_mesh returns u); on the lattice path
+// K and M are then not written (left empty), two thirds of the system's bytes
+void build_system(Ctx& c, const DMesh& m, double rho, int target_kind, uint64_t seed, DSystem& s,
+                  bool a_only = false);
 // l2 / h1-semi error of the P1 field `coeffs` (device, n_dofs) vs the manufactured exact solution
 void error_norms(Ctx& c, const DMesh& m, const DSystem& s, const double* coeffs, double rho, double* l2, double* h1);
 // l2 / h1-semi error of `coeffs` vs a target field u_bar (value and exact gradient)
