@@ -654,3 +654,20 @@ def test_amg_apply_smoothing_steps(rd, O, n, thr, m):
     dh = rd.build_amg(ds.A, thr, m)
     r = O.pseudo_random_vec(os_.A.rows, 5)
     assert np.array_equal(dh.apply(r), oh.apply(r))
+
+
+@pytest.mark.parametrize("n", [64, 129])
+def test_repeated_solves_bit_identical(rd, n):
+    """The solve loop's kernels overlap (programmatic dependent launch: a kernel's blocks are
+    scheduled while its predecessor drains) and the sweep's tiles hand values on through memory:
+    any race there would make runs differ.  Ten full build + setup + solve runs, bit for bit."""
+    mesh = rd.build_structured_cube(n)
+    ref = None
+    for k in range(10):
+        s = rd.build_system(mesh, 1.0 / n ** 2, "ball")
+        out = rd.solve_system_amg(s.A, s.f(), 1e-8)
+        if ref is None:
+            ref = (out.u.copy(), out.iterations)
+        else:
+            assert out.iterations == ref[1]
+            assert np.array_equal(out.u, ref[0]), f"run {k} differs from run 0"
