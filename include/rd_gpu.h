@@ -268,10 +268,13 @@ int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, doubl
 /* The bench-precond row end to end from a host TetMesh (mesh.hpp:13-24 arrays, as for
  * rd_gpu_mesh_create) in one call: upload, rd::build_system (assembly.cpp:225-238), then
  * solve_system's AMG branch (bench.cpp:185-225) with u (n_dofs doubles, host or device) read
- * back.  The host arrays need only live for the call, so for a mesh of Kuhn-lattice size the
- * tet array uploads on a second stream while the lattice path (which reads no tets) assembles
- * and solves; the uploaded tets are then checked against the Kuhn enumeration and a mismatch
- * reruns the work on the generic path.  Same results, errors and timing split as
+ * back.  The host arrays need only live for the call.  A mesh of Kuhn-lattice size is solved
+ * provisionally as rd::build_structured_cube's mesh (vertices and boundary flags generated on
+ * the device, tets by formula) while the host arrays upload on a second stream; the uploaded
+ * vertices and flags are compared bit for bit with the generated ones (any difference restarts
+ * on the uploaded arrays) and the uploaded tets with the Kuhn enumeration (a mismatch reruns on
+ * the generic path) before the call returns.  u may be written by a provisional attempt and is
+ * always overwritten by the attempt that stands.  Same results, errors and timing split as
  * rd_gpu_build_system + rd_gpu_solve_system_amg.  n_dofs_out may be NULL. */
 int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const int32_t* tets, const uint8_t* bnd,
                            double rho, const rd_target* target, double tol, double* u, int* n_dofs_out,
