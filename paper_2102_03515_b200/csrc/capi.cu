@@ -1120,6 +1120,12 @@ int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, doubl
 }
 
 namespace {
+// Share of a host tet array that the host threads compare (the rest uploads and is compared on
+// the device).  Adapted from the measured rate of the host comparison after every call: as much
+// as the host threads finish in ~7 ms (well inside a solve of the sizes where it matters), since
+// the host comparison, unlike the upload, does not disturb the kernels running meanwhile.
+std::atomic<double> g_host_tets_share{0.5};
+
 // Do tets [t0, t1) of a host array equal the build_structured_cube(n) enumeration (mesh.cpp:46-58:
 // cell t / 6, chain t % 6)?  Sets *bad on the first difference; gives up early once it is set.
 void host_kuhn_check(int n, const int32_t* tets, int64_t t0, int64_t t1, std::atomic<int>* bad) {
@@ -1166,6 +1172,8 @@ void host_kuhn_check(int n, const int32_t* tets, int64_t t0, int64_t t1, std::at
 }
 }  // namespace
 
+double rd_gpu_host_tets_share(void) { return g_host_tets_share.load(); }
+
 int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const int32_t* tets, const uint8_t* bnd,
                            double rho, const rd_target* target, double tol, double* u, int* n_dofs_out,
                            rd_solve_outcome* out) {
@@ -1204,11 +1212,25 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
     struct HostCheck {
       std::vector<std::thread> th;
       std::atomic<int> bad{0};
+      std::atomic<long long> last_end_ns{0};  // latest finish of a thread (steady clock)
+      long long start_ns = 0;
+      int64_t tets = 0;
+      static long long now_ns() {
+        return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+            .count();
+      }
       void join() {
+        const bool ran = !th.empty();
         for (auto& t : th)
           if (t.joinable()) t.join();
         th.clear();
+        if (ran && !bad.load() && tets > 0 && last_end_ns.load() > start_ns) {
+          // ms the host threads would need for the whole array -> the share they finish in ~7 ms
+          const double ms = 1e-6 * (double)(last_end_ns.load() - start_ns);
+          g_host_tets_share.store(std::min(1.0, std::max(0.1, 7.0 / std::max(ms, 1e-3) * g_share_used)));
+        }
       }
+      double g_share_used = 0.5;
       ~HostCheck() { join(); }
     } hc;
     static const bool nohost = getenv("RD_NO_HOST_TETS_CHECK") && atoi(getenv("RD_NO_HOST_TETS_CHECK")) != 0;
@@ -1263,11 +1285,21 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
         const unsigned hw = std::thread::hardware_concurrency();
         const int nth = (int)std::max(1u, std::min(8u, hw ? hw / 2 : 4u));
         const int64_t ncell = (int64_t)nt / 6;
-        host_end = 6 * (ncell / 2);
+        hc.g_share_used = g_host_tets_share.load();
+        host_end = 6 * std::min<int64_t>(ncell, (int64_t)((double)ncell * hc.g_share_used));
+        hc.tets = host_end;
+        hc.start_ns = HostCheck::now_ns();
         const int64_t per = 6 * ((host_end / 6 + nth - 1) / nth);  // whole cells per thread
         for (int k = 0; k < nth; ++k) {
           const int64_t t0 = std::min<int64_t>(host_end, k * per), t1 = std::min<int64_t>(host_end, t0 + per);
-          if (t0 < t1) hc.th.emplace_back(host_kuhn_check, cand, tets, t0, t1, &hc.bad);
+          if (t0 < t1)
+            hc.th.emplace_back([&hc, cand, tets, t0, t1] {
+              host_kuhn_check(cand, tets, t0, t1, &hc.bad);
+              const long long e = HostCheck::now_ns();
+              long long cur = hc.last_end_ns.load();
+              while (cur < e && !hc.last_end_ns.compare_exchange_weak(cur, e)) {
+              }
+            });
         }
       }
       upload(m.tets.p + 4 * host_end, tets + 4 * host_end, sizeof(int) * 4 * (size_t)(nt - host_end));
