@@ -1290,17 +1290,19 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
         hc.tets = host_end;
         hc.start_ns = HostCheck::now_ns();
         const int64_t per = 6 * ((host_end / 6 + nth - 1) / nth);  // whole cells per thread
-        for (int k = 0; k < nth; ++k) {
-          const int64_t t0 = std::min<int64_t>(host_end, k * per), t1 = std::min<int64_t>(host_end, t0 + per);
-          if (t0 < t1)
-            hc.th.emplace_back([&hc, cand, tets, t0, t1] {
-              host_kuhn_check(cand, tets, t0, t1, &hc.bad);
-              const long long e = HostCheck::now_ns();
-              long long cur = hc.last_end_ns.load();
-              while (cur < e && !hc.last_end_ns.compare_exchange_weak(cur, e)) {
-              }
-            });
-        }
+        // one thread starts the others (thread creation stays off this thread, which is about to
+        // drive the solve)
+        hc.th.emplace_back([&hc, cand, tets, host_end, per, nth] {
+          auto part = [&hc, cand, tets, host_end, per](int k) {
+            const int64_t t0 = std::min<int64_t>(host_end, k * per), t1 = std::min<int64_t>(host_end, t0 + per);
+            if (t0 < t1) host_kuhn_check(cand, tets, t0, t1, &hc.bad);
+          };
+          std::vector<std::thread> more;
+          for (int k = 1; k < nth; ++k) more.emplace_back(part, k);
+          part(0);
+          for (auto& t : more) t.join();
+          hc.last_end_ns.store(HostCheck::now_ns());
+        });
       }
       upload(m.tets.p + 4 * host_end, tets + 4 * host_end, sizeof(int) * 4 * (size_t)(nt - host_end));
       launch_lattice_tets_check(c, upl.s, cand, m.tets.p, nt, bad.p, (int)host_end);
