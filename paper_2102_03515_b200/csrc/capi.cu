@@ -1233,7 +1233,7 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
       double g_share_used = 0.5;
       ~HostCheck() { join(); }
     } hc;
-    static const bool nohost = getenv("RD_NO_HOST_TETS_CHECK") && atoi(getenv("RD_NO_HOST_TETS_CHECK")) != 0;
+    const bool nohost = getenv("RD_NO_HOST_TETS_CHECK") && atoi(getenv("RD_NO_HOST_TETS_CHECK")) != 0;  // read per call
     const bool host_tets = prov && !nohost && !is_device_ptr(tets);
     int64_t host_half = 0;  // tets [0, host_half) were not uploaded
     if (prov) {
