@@ -514,7 +514,6 @@ def run_ours(args, rank, world, local_rank):
                                      u=u_host, ctx=ctx)
             return out.iterations
 
-        all_up = any(os.environ.get(k, "0") not in ("", "0") for k in ("RD_NO_HOST_TETS_CHECK", "RD_NO_PROVISIONAL_MESH"))
         for _ in range(max(1, args.warmup)):
             e2e_step()
         barrier()
@@ -533,45 +532,14 @@ def run_ours(args, rank, world, local_rank):
         b.record(stream)
         torch.cuda.synchronize()
         e2e_ms, e2e_value = job_rate(a.elapsed_time(b), float(ndofs) * sum(e2e_its), world, dev)
-        # the same with every input byte over PCIe (the tet array uploaded whole and compared on the
-        # device): reported beside the headline so both readings of "end to end" are on the line
-        e2e_all = None
-        if not all_up:
-            os.environ["RD_NO_HOST_TETS_CHECK"] = "1"
-            try:
-                e2e_step()
-                torch.cuda.synchronize()
-                a2 = torch.cuda.Event(enable_timing=True)
-                b2 = torch.cuda.Event(enable_timing=True)
-                a2.record(stream)
-                its2 = [e2e_step() for _ in range(args.steps)]
-                b2.record(stream)
-                torch.cuda.synchronize()
-                ms2, v2 = job_rate(a2.elapsed_time(b2), float(ndofs) * sum(its2), world, dev)
-                e2e_all = {"value": v2, "ms_per_step": ms2 / args.steps,
-                           "h2d_bytes_per_step": int(xyz.nbytes + bnd.nbytes + tets.nbytes)}
-            finally:
-                del os.environ["RD_NO_HOST_TETS_CHECK"]
-        # the tet array of a Kuhn-lattice mesh: a share (adapted to the host's speed) is compared on
-        # the host and not uploaded, the rest uploads and is compared on the device
-        share = float(rd.lib().rd_gpu_host_tets_share())
-        ncell = tets.shape[0] // 6
-        tets_up = tets.nbytes if all_up else tets.nbytes - 6 * min(ncell, int(ncell * share)) * 16
         result["e2e"] = {"value": e2e_value, "unit": UNIT,
                          "ms_per_step": e2e_ms / args.steps,
-                         # the tet array of a Kuhn-lattice mesh is verified on the host (never read by
-                         # the lattice path, so not uploaded) unless that is switched off
-                         "h2d_bytes_per_step": int(xyz.nbytes + bnd.nbytes + tets_up),
-                         "host_tets_share": None if all_up else share,
-                         "all_inputs_uploaded": e2e_all,
-                         "host_verified_bytes_per_step": int(tets.nbytes - tets_up),
+                         "h2d_bytes_per_step": int(xyz.nbytes + tets.nbytes + bnd.nbytes),
                          "d2h_bytes_per_step": int(8 * ndofs),
                          "path": "rd_gpu_solve_host_mesh(pinned host TetMesh -> build_system -> build_amg + "
                                  "pcg -> u in pinned host memory; the solve starts on generated lattice "
-                                 "vertices while vertices and flags upload and are compared with them on "
-                                 "the device; the tet array is compared with the Kuhn enumeration partly by host "
-                                 "threads (host_tets_share), the rest uploaded and on the device; every input "
-                                 "is checked before the result stands)"}
+                                 "vertices while vertices, flags and tets upload, all three checked "
+                                 "against the upload before the result stands)"}
 
     # ---------------- the other BASELINE sizes on this GPU (C4 n=256, C5 n=512 = 133M dofs):
     # one timed solve each after a warm-up, same path; reported beside the C2 headline

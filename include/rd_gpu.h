@@ -272,14 +272,10 @@ int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, doubl
  * provisionally as rd::build_structured_cube's mesh (vertices and boundary flags generated on
  * the device, tets by formula) while the host arrays upload on a second stream; the uploaded
  * vertices and flags are compared bit for bit with the generated ones (any difference restarts
- * on the uploaded arrays) and the tets with the Kuhn enumeration -- a leading share by host
- * threads where the array lives (rd_gpu_host_tets_share), the rest uploaded and on the device; a
- * mismatch uploads what is missing and reruns on the generic path -- before the call returns.  u may be written by a provisional attempt and is
+ * on the uploaded arrays) and the uploaded tets with the Kuhn enumeration (a mismatch reruns on
+ * the generic path) before the call returns.  u may be written by a provisional attempt and is
  * always overwritten by the attempt that stands.  Same results, errors and timing split as
  * rd_gpu_build_system + rd_gpu_solve_system_amg.  n_dofs_out may be NULL. */
-/* The share of a host tet array rd_gpu_solve_host_mesh currently compares on the host (the rest
- * uploads); adapted after every call from the measured rate of the host comparison. */
-double rd_gpu_host_tets_share(void);
 int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const int32_t* tets, const uint8_t* bnd,
                            double rho, const rd_target* target, double tol, double* u, int* n_dofs_out,
                            rd_solve_outcome* out);

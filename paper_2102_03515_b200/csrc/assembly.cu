@@ -743,8 +743,8 @@ __global__ void __launch_bounds__(kLatNT) lat_split_kernel(int nd, int n, double
 }
 
 // Does the tet array equal the build_structured_cube enumeration for n?
-__global__ void lattice_tets_check_kernel(int n, const int* __restrict__ tets, int* bad, int64_t t_begin = 0) {
-  const int64_t t = t_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void lattice_tets_check_kernel(int n, const int* __restrict__ tets, int* bad) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n * n * n * 6) return;
   const int nv = n + 1;
   const int p = (int)(t % 6);
@@ -1221,9 +1221,8 @@ int cube_lattice_candidate(int nv, int nt) {
   return n;
 }
 
-void launch_lattice_tets_check(Ctx& c, cudaStream_t st, int n, const int* tets, int nt, int* bad, int t_begin) {
-  if (nt <= t_begin) return;
-  lattice_tets_check_kernel<<<div_up(nt - t_begin, 256), 256, 0, st>>>(n, tets, bad, t_begin);
+void launch_lattice_tets_check(Ctx& c, cudaStream_t st, int n, const int* tets, int nt, int* bad) {
+  lattice_tets_check_kernel<<<div_up(nt, 256), 256, 0, st>>>(n, tets, bad);
   RDG_LAUNCH_CHECK();
   ++c.launches;
 }

@@ -7,9 +7,7 @@
 #include <cstdlib>
 #include <chrono>
 #include <cstring>
-#include <atomic>
 #include <mutex>
-#include <thread>
 
 #include "internal.hpp"
 
@@ -1119,61 +1117,6 @@ int rd_gpu_solve_system_amg(rd_ctx* ctx, const rd_csr* a, const double* f, doubl
   });
 }
 
-namespace {
-// Share of a host tet array that the host threads compare (the rest uploads and is compared on
-// the device).  Adapted from the measured rate of the host comparison after every call: as much
-// as the host threads finish in ~7 ms (well inside a solve of the sizes where it matters), since
-// the host comparison, unlike the upload, does not disturb the kernels running meanwhile.
-std::atomic<double> g_host_tets_share{0.5};
-
-// Do tets [t0, t1) of a host array equal the build_structured_cube(n) enumeration (mesh.cpp:46-58:
-// cell t / 6, chain t % 6)?  Sets *bad on the first difference; gives up early once it is set.
-void host_kuhn_check(int n, const int32_t* tets, int64_t t0, int64_t t1, std::atomic<int>* bad) {
-  // whole cells [t0 / 6, t1 / 6) (the callers' ranges are multiples of 6), the cell's coordinates
-  // carried along (no divisions in the loop), the six chains of a cell as vertex-id offsets
-  const int nv = n + 1;
-  const int d[3] = {1, nv, nv * nv};
-  static const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-  int off[6][3];
-  for (int p = 0; p < 6; ++p) {
-    off[p][0] = d[perms[p][0]];
-    off[p][1] = off[p][0] + d[perms[p][1]];
-    off[p][2] = off[p][1] + d[perms[p][2]];
-  }
-  int64_t cell = t0 / 6;
-  const int64_t cend = t1 / 6;
-  int c0 = (int)(cell % n), c1 = (int)((cell / n) % n), c2 = (int)(cell / ((int64_t)n * n));
-  const int32_t* g = tets + 24 * cell;
-  while (cell < cend) {
-    if (bad->load(std::memory_order_relaxed)) return;
-    const int64_t stop = std::min<int64_t>(cend, cell + 4096);
-    int diff = 0;
-    for (; cell < stop; ++cell, g += 24) {
-      const int v0 = (c2 * nv + c1) * nv + c0;
-      for (int p = 0; p < 6; ++p) {
-        diff |= g[4 * p] ^ v0;
-        diff |= g[4 * p + 1] ^ (v0 + off[p][0]);
-        diff |= g[4 * p + 2] ^ (v0 + off[p][1]);
-        diff |= g[4 * p + 3] ^ (v0 + off[p][2]);
-      }
-      if (++c0 == n) {
-        c0 = 0;
-        if (++c1 == n) {
-          c1 = 0;
-          ++c2;
-        }
-      }
-    }
-    if (diff) {
-      bad->store(1, std::memory_order_relaxed);
-      return;
-    }
-  }
-}
-}  // namespace
-
-double rd_gpu_host_tets_share(void) { return g_host_tets_share.load(); }
-
 int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const int32_t* tets, const uint8_t* bnd,
                            double rho, const rd_target* target, double tol, double* u, int* n_dofs_out,
                            rd_solve_outcome* out) {
@@ -1196,12 +1139,6 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
     // Kuhn enumeration.  The vertex verdict is read after the setup phase (the upload is short):
     // a different geometry restarts on the uploaded vertices.  The tets verdict gates the result:
     // a mismatch reruns on the generic path.  The host arrays live for this call.
-    // A tet array in host memory is compared with the enumeration from both ends while the device
-    // solves: host threads take the first half where it lives, the second half uploads and is
-    // compared on the device.  The lattice path never reads tets, so the first half crosses PCIe
-    // only if a comparison fails and the generic path needs it.  Boxes differ by 2x in upload
-    // bandwidth and in host memory speed; either half alone stays well inside the solve on all
-    // of them.  (A tet array already in device memory is checked there, as before.)
     const int cand = cube_lattice_candidate(nv, nt);
     static const bool noprov = getenv("RD_NO_PROVISIONAL_MESH") && atoi(getenv("RD_NO_PROVISIONAL_MESH")) != 0;
     const bool prov = cand > 0 && nt > 0 && nv > 0 && !noprov;
@@ -1209,33 +1146,6 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
     RDG_CUDA(cudaMemsetAsync(bad.p, 0, 2 * sizeof(int), c.stream));
     DBuf<double> xyz_up;
     DBuf<uint8_t> bnd_up;
-    struct HostCheck {
-      std::vector<std::thread> th;
-      std::atomic<int> bad{0};
-      std::atomic<long long> last_end_ns{0};  // latest finish of a thread (steady clock)
-      long long start_ns = 0;
-      int64_t tets = 0;
-      static long long now_ns() {
-        return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
-            .count();
-      }
-      void join() {
-        const bool ran = !th.empty();
-        for (auto& t : th)
-          if (t.joinable()) t.join();
-        th.clear();
-        if (ran && !bad.load() && tets > 0 && last_end_ns.load() > start_ns) {
-          // ms the host threads would need for the whole array -> the share they finish in ~7 ms
-          const double ms = 1e-6 * (double)(last_end_ns.load() - start_ns);
-          g_host_tets_share.store(std::min(1.0, std::max(0.1, 7.0 / std::max(ms, 1e-3) * g_share_used)));
-        }
-      }
-      double g_share_used = 0.5;
-      ~HostCheck() { join(); }
-    } hc;
-    const bool nohost = getenv("RD_NO_HOST_TETS_CHECK") && atoi(getenv("RD_NO_HOST_TETS_CHECK")) != 0;  // read per call
-    const bool host_tets = prov && !nohost && !is_device_ptr(tets);
-    int64_t host_half = 0;  // tets [0, host_half) were not uploaded
     if (prov) {
       xyz_up.alloc((size_t)nv * 3, c.stream);
       bnd_up.alloc(nv, c.stream);
@@ -1280,33 +1190,8 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
       RDG_CUDA(cudaMemcpyAsync(bnd_up.p, bnd, nv, cudaMemcpyDefault, upl.s));
       launch_verts_equal(c, upl.s, nv, xyz_up.p, m.xyz.p, bnd_up.p, m.boundary.p, bad.p + 1);
       RDG_CUDA(cudaEventRecord(upl.vdone, upl.s));
-      int64_t host_end = 0;  // tets [0, host_end) are compared on the host
-      if (host_tets) {
-        const unsigned hw = std::thread::hardware_concurrency();
-        const int nth = (int)std::max(1u, std::min(8u, hw ? hw / 2 : 4u));
-        const int64_t ncell = (int64_t)nt / 6;
-        hc.g_share_used = g_host_tets_share.load();
-        host_end = 6 * std::min<int64_t>(ncell, (int64_t)((double)ncell * hc.g_share_used));
-        hc.tets = host_end;
-        hc.start_ns = HostCheck::now_ns();
-        const int64_t per = 6 * ((host_end / 6 + nth - 1) / nth);  // whole cells per thread
-        // one thread starts the others (thread creation stays off this thread, which is about to
-        // drive the solve)
-        hc.th.emplace_back([&hc, cand, tets, host_end, per, nth] {
-          auto part = [&hc, cand, tets, host_end, per](int k) {
-            const int64_t t0 = std::min<int64_t>(host_end, k * per), t1 = std::min<int64_t>(host_end, t0 + per);
-            if (t0 < t1) host_kuhn_check(cand, tets, t0, t1, &hc.bad);
-          };
-          std::vector<std::thread> more;
-          for (int k = 1; k < nth; ++k) more.emplace_back(part, k);
-          part(0);
-          for (auto& t : more) t.join();
-          hc.last_end_ns.store(HostCheck::now_ns());
-        });
-      }
-      upload(m.tets.p + 4 * host_end, tets + 4 * host_end, sizeof(int) * 4 * (size_t)(nt - host_end));
-      launch_lattice_tets_check(c, upl.s, cand, m.tets.p, nt, bad.p, (int)host_end);
-      host_half = host_end;
+      upload(m.tets.p, tets, sizeof(int) * 4 * (size_t)nt);
+      launch_lattice_tets_check(c, upl.s, cand, m.tets.p, nt, bad.p);
       RDG_CUDA(cudaEventRecord(upl.done, upl.s));
       m.lattice_n = cand;  // provisional until upl.done
       m.tets_ready = upl.done;
@@ -1328,14 +1213,8 @@ int rd_gpu_solve_host_mesh(rd_ctx* ctx, int nv, const double* xyz, int nt, const
     auto tets_ok = [&]() -> bool {  // also the point after which nothing runs on the upload stream
       if (vtets < 0) {
         int hb = 1;
-        hc.join();
         if (cudaEventSynchronize(upl.done) == cudaSuccess)
           cudaMemcpy(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost);
-        hb |= hc.bad.load();
-        if (hb && host_half > 0) {  // the generic path needs the first half on the device after all
-          cudaMemcpyAsync(m.tets.p, tets, sizeof(int) * 4 * (size_t)host_half, cudaMemcpyDefault, upl.s);
-          if (cudaStreamSynchronize(upl.s) != cudaSuccess) cudaGetLastError();
-        }
         m.tets_ready = nullptr;
         upl.close();
         vtets = hb ? 0 : 1;

@@ -203,8 +203,7 @@ void detect_cube_lattice(Ctx& c, DMesh& m);
 // n when (nv, nt) are the sizes of build_structured_cube(n), else -1 (no check of the tets)
 int cube_lattice_candidate(int nv, int nt);
 // bad[0] = 1 unless tets[0, nt) is the Kuhn enumeration of build_structured_cube(n); on stream st
-// (tets [t_begin, nt) only)
-void launch_lattice_tets_check(Ctx& c, cudaStream_t st, int n, const int* tets, int nt, int* bad, int t_begin = 0);
+void launch_lattice_tets_check(Ctx& c, cudaStream_t st, int n, const int* tets, int nt, int* bad);
 void launch_cube_vertices(Ctx& c, cudaStream_t st, int n, double* xyz, uint8_t* bnd);
 void launch_verts_equal(Ctx& c, cudaStream_t st, int64_t nv, const double* a, const double* b, const uint8_t* fa,
                         const uint8_t* fb, int* bad);

@@ -98,7 +98,6 @@ def lib():
         "rd_gpu_synchronize": (_I, [_P]),
         "rd_gpu_launch_count": (C.c_int64, [_P]),
         "rd_gpu_pool_bytes": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
-        "rd_gpu_host_tets_share": (C.c_double, []),
         "rd_gpu_copy": (_I, [_P, _P, _P, C.c_size_t]),
         "rd_gpu_build_structured_cube": (_I, [_P, _I, C.POINTER(_P)]),
         "rd_gpu_mesh_create": (_I, [_P, _I, _P, _I, _P, _P, C.POINTER(_P)]),

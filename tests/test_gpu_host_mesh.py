@@ -2,8 +2,7 @@
 
 For a mesh of Kuhn-lattice size the solve starts on generated unit-cube vertices while the host
 arrays upload on a second stream; the uploaded vertices / flags are compared with the generated
-ones, and the tets with the Kuhn enumeration (first half by host threads where the array lives,
-second half uploaded and on the device), before any result stands.
+ones and the uploaded tets with the Kuhn enumeration before any result stands.
 Checked against the three-call path (rd_gpu_mesh_create -> rd_gpu_build_system ->
 rd_gpu_solve_system_amg), which the parity suite pins to the oracle: the same u bit for bit
 and the same iteration count, on lattice meshes, on a lattice-sized mesh whose tets are not
@@ -100,9 +99,8 @@ def test_other_geometry_on_lattice_sized_mesh(rd):
 
 
 def test_tets_differ_in_either_half(rd):
-    """The tet array is compared with the enumeration half on the host (first half, not
-    uploaded) and half on the device (second half): a difference in either half, or in the very
-    last tet, must send the solve down the generic path with the whole array on the device."""
+    """A difference from the Kuhn enumeration anywhere in the tet array -- front, middle, the
+    very last tet -- must send the solve down the generic path."""
     n = 12
     xyz, tets, b = rd.build_structured_cube(n).download()
     nt = tets.shape[0]
